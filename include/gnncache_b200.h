@@ -1,0 +1,218 @@
+/*
+ * gnncache_b200.h — C-ABI of libgnncache_b200.so, the B200 (sm_100a) data-preparation
+ * path of Legion (arXiv 2305.16588): local shuffle, k-hop CSR sampling, sub-graph
+ * dedup + relabel, three-tier feature gather, presampling hotness, cache-plan scans.
+ *
+ * The reference (`gnncache` 0.1.0, /root/reference/pkg/src/gnncache) is pure
+ * Python/numpy and has no FFI: its boundary is a set of Python functions over
+ * numpy arrays. Each entry point below names the reference function it replaces
+ * (file:line, relative to pkg/src/gnncache/). The Python package
+ * paper_2305_16588_b200 binds these through ctypes and keeps the reference's
+ * Python signatures, dataclasses and exception types on top of them.
+ *
+ * Conventions
+ *  - every function returns int status: GC_OK (0) or a negative GC_ERR_* code;
+ *    gc_last_error() returns a thread-local message for the last failure.
+ *  - all buffers are caller-owned. "d_" = device pointer (local HBM, a mapped peer
+ *    pointer, or a UVA pointer to mapped pinned host memory); sizes are element counts.
+ *  - `stream` is a cudaStream_t passed as void*; every call is asynchronous on it
+ *    and never synchronises the device (so a caller may capture calls in a CUDA graph).
+ *  - vertex ids are uint32 (the reference guarantees n < 2^32, graph.py:158-159);
+ *    row offsets are uint64 (graph.py:65-66).
+ *  - "batched" entry points process a window of W independent mini-batches in one
+ *    launch; batch b's data lives at base + b*stride and its element count is read
+ *    from a device array, so no host round trip is needed between hops.
+ */
+#ifndef GNNCACHE_B200_H
+#define GNNCACHE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GC_ABI_VERSION 1
+
+#define GC_OK 0
+#define GC_ERR_VALUE (-1)       /* -> ValueError      (sampling.py:42-48, :128-131; planner.py:107,:119) */
+#define GC_ERR_OVERFLOW (-2)    /* -> OverflowError   (sampling.py:298-299) */
+#define GC_ERR_CUDA (-3)        /* -> RuntimeError    (device failure; no CPU fallback exists) */
+#define GC_ERR_UNSUPPORTED (-4) /* -> NotImplementedError */
+#define GC_ERR_ASSERT (-5)      /* -> AssertionError  (planner.py:317-318) */
+
+#define GC_MAX_PEERS 8
+#define GC_TIER_HOST 0xFFFFFFFFu /* location-table value for host-resident rows */
+
+int gc_abi_version(void);
+const char* gc_last_error(void);
+/* device ordinal of the calling thread's current device; -1 if none */
+int gc_current_device(void);
+
+/* ------------------------------------------------------------------ RNG (rng.py) */
+
+/* mix64_array, rng.py:34-42 */
+int gc_mix64(const uint64_t* d_in, uint64_t* d_out, int64_t n, void* stream);
+/* KeyedRng.hash_counters, rng.py:64-66 */
+int gc_hash_counters(uint64_t key, const int64_t* d_counters, uint64_t* d_out, int64_t n, void* stream);
+/* KeyedRng.hash_pairs, rng.py:68-72 */
+int gc_hash_pairs(uint64_t key, const int64_t* d_a, const int64_t* d_b, uint64_t* d_out, int64_t n,
+                  void* stream);
+
+/* K1: KeyedRng.permutation (rng.py:78-82) = stable argsort of hash_counters(0..n-1),
+ * optionally fused with the gather `pool[perm]` of run_sampling_epoch (sampling.py:231).
+ * d_pool may be NULL (then d_out receives perm itself). n < 2^31. */
+size_t gc_permutation_temp_bytes(int64_t n);
+int gc_permutation(uint64_t key, int64_t n, const int64_t* d_pool, int64_t* d_out, void* d_temp,
+                   size_t temp_bytes, void* stream);
+
+/* ---------------------------------------------------------- topology (graph.py) */
+
+/* CsrGraph layout, graph.py:62-96: row_offsets u64[n+1], col_indices u32[m]. The
+ * pointers may be local HBM or UVA-mapped pinned host memory (the host topology tier). */
+typedef struct gc_csr {
+    int64_t num_vertices;
+    int64_t num_edges;
+    const uint64_t* row_offsets;
+    const uint32_t* col_indices;
+} gc_csr_t;
+
+/* ------------------------------------------------- hotness (sampling.py:146-289) */
+
+/* Device hotness counters of one GPU (GpuTrace, sampling.py:190-197). Any pointer may
+ * be NULL to skip that counter. Counters are u64 (the u32 dump limit, sampling.py:298,
+ * only applies when writing the file). */
+typedef struct gc_hotness {
+    uint64_t* topo_reads;      /* [n] frontier occurrences (sampling.py:238) */
+    uint64_t* edge_traversals; /* [n] sampled edges out of v (sampling.py:239-241) */
+    uint64_t* feat_lookups;    /* [n] per-batch distinct appearances (sampling.py:242) */
+    uint64_t* txn_total;       /* [1] sum of t(v) over reads (sampling.py:284-288) */
+    uint32_t cache_line_bytes; /* HardwareSpec.cache_line_bytes (hardware.py:167) */
+    uint32_t uint32_bytes;     /* HardwareSpec.uint32_bytes (hardware.py:168) */
+} gc_hotness_t;
+
+/* ------------------------------------------- K2: hop expansion (sampling.py:84-143) */
+
+/* One hop of _expand_frontier (sampling.py:84-117) for W batches at once.
+ *  frontier of batch b: d_frontier + b*frontier_stride, d_frontier_count[b] entries
+ *  hop key of batch b : d_hop_keys[b] = stream.derive(h).key (sampling.py:135)
+ *  output offsets     : d_out_offsets + b*offsets_stride, count+1 entries (u32, exclusive scan of take)
+ *  output neighbors   : d_out_nbrs + b*nbrs_stride, d_out_count[b] entries
+ *  d_bitmap (optional): per-batch visited bitmap (bitmap_words u32 words per batch); every
+ *                       emitted neighbor is marked, and the frontier too if mark_frontier.
+ *  hot (optional)     : presampling counters of the sampling GPU.
+ * Selection is bit-exact with the reference: deg<=fanout copies the CSR slice in order,
+ * otherwise the fanout smallest (hash_pairs(i,j), j) are emitted in ascending order.
+ * Requires max_frontier*fanout < 2^32. */
+size_t gc_hop_expand_temp_bytes(uint32_t num_batches, uint32_t max_frontier);
+int gc_hop_expand(const gc_csr_t* graph, const uint32_t* d_frontier, uint64_t frontier_stride,
+                  const uint32_t* d_frontier_count, uint32_t max_frontier, uint32_t fanout,
+                  const uint64_t* d_hop_keys, uint32_t num_batches, uint32_t* d_out_offsets,
+                  uint64_t offsets_stride, uint32_t* d_out_nbrs, uint64_t nbrs_stride, uint32_t* d_out_count,
+                  uint32_t* d_bitmap, uint64_t bitmap_words, int mark_frontier, const gc_hotness_t* hot,
+                  void* d_temp, size_t temp_bytes, void* stream);
+
+/* ------------------------------- K3: dedup + relabel (BatchSample.distinct_vertices) */
+
+/* Words per batch bitmap for n vertices (padded for 16-byte vector access). */
+uint64_t gc_bitmap_words(int64_t num_vertices);
+/* np.unique of seeds ∪ all hop neighbors (sampling.py:73-75) from the visited bitmaps:
+ * sorted distinct ids of batch b -> d_unique + b*unique_stride, count -> d_unique_count[b];
+ * d_word_prefix (optional) receives the exclusive popcount prefix per word for gc_relabel.
+ * feat_lookups (optional) += 1 per distinct id (sampling.py:242). clear_bitmap zeroes the
+ * bitmap as it is consumed (only valid if no later gc_relabel reads it). */
+size_t gc_unique_temp_bytes(uint32_t num_batches, uint64_t bitmap_words);
+int gc_unique_compact(uint32_t* d_bitmap, uint64_t bitmap_words, uint32_t num_batches, uint32_t* d_unique,
+                      uint64_t unique_stride, uint32_t* d_unique_count, uint32_t* d_word_prefix,
+                      uint64_t* d_feat_lookups, int clear_bitmap, void* d_temp, size_t temp_bytes,
+                      void* stream);
+/* Relabel (not in the reference; CPU restatement np.searchsorted(unique, ids)):
+ * d_local[b*stride + k] = index of d_ids[b*stride + k] in batch b's unique list. */
+int gc_relabel(const uint32_t* d_ids, uint64_t ids_stride, const uint32_t* d_ids_count, uint32_t max_count,
+               uint32_t num_batches, const uint32_t* d_bitmap, const uint32_t* d_word_prefix,
+               uint64_t bitmap_words, uint32_t* d_local, void* stream);
+/* Mark ids in the per-batch visited bitmaps (seeds of a zero-hop config). */
+int gc_mark_visited(const uint32_t* d_ids, uint64_t ids_stride, const uint32_t* d_count, uint32_t max_count,
+                    uint32_t num_batches, uint32_t* d_bitmap, uint64_t bitmap_words, void* stream);
+/* Zero the bitmap words touched by batch b's unique ids (cheap reset for the next window). */
+int gc_bitmap_clear(uint32_t* d_bitmap, uint64_t bitmap_words, uint32_t num_batches, const uint32_t* d_unique,
+                    uint64_t unique_stride, const uint32_t* d_unique_count, uint32_t max_unique, void* stream);
+
+/* ------------------------------------------------ K4: three-tier feature gather */
+
+/* Feature store of one GPU (the tier rule of account_assignment, simulator.py:161-202).
+ * location[v] == GC_TIER_HOST -> host_rows + v*row_bytes (UVA over PCIe)
+ * location[v] == (g<<28)|slot -> slabs[g] + slot*row_bytes (g == self_rank: local HBM,
+ *                                otherwise the owner's slab read over NVLink/NVSwitch)
+ * location == NULL            -> slabs[self_rank] + v*row_bytes (fully resident table) */
+typedef struct gc_feature_store {
+    uint32_t row_bytes; /* FeatureSpec.row_bytes (graph.py:220-222); multiple of 4 */
+    uint32_t self_rank;
+    uint32_t num_ranks;
+    uint32_t reserved;
+    const uint32_t* location;
+    const void* slabs[GC_MAX_PEERS];
+    const void* host_rows;
+} gc_feature_store_t;
+
+/* out[b*out_stride_rows + k] = row(d_ids[b*ids_stride + k]) for k < min(d_count[b], max_count).
+ * d_tier_rows (optional, u64[3]) += rows served by local / peer / host. */
+int gc_gather(const gc_feature_store_t* store, const uint32_t* d_ids, uint64_t ids_stride,
+              const uint32_t* d_count, uint32_t max_count, uint32_t num_batches, void* d_out,
+              uint64_t out_stride_rows, uint64_t* d_tier_rows, void* stream);
+
+/* Deterministic synthetic feature rows [first_row, first_row+rows) of a dim-wide fp32
+ * table: X[v,d] = (mix64(v*dim+d) >> 40) * 2^-24 - 0.5 (bench/test input only). */
+int gc_synth_features(uint64_t first_row, uint64_t rows, uint32_t dim, float* d_out, void* stream);
+
+/* ---------------------------------------------- K5: hotness scatter (sampling.py:164-174) */
+
+/* accumulate_hotness's bincount: d_counter[d_ids[k]] += (d_weights ? d_weights[k] : 1). */
+int gc_scatter_add(const uint32_t* d_ids, const uint32_t* d_weights, int64_t count, uint64_t* d_counter,
+                   void* stream);
+
+/* ------------------------------------------- K6/K7: cost model (planner.py:42-261) */
+
+/* Column sums and first argmax over K rows (planner.py:50-55): rows are int64 [K][n]. */
+int gc_colsum_argmax(const int64_t* d_rows, uint32_t k_rows, int64_t n, int64_t* d_totals, int32_t* d_owner,
+                     void* stream);
+/* hotness_descending_order (planner.py:42-45): ids sorted by totals descending, ties by
+ * ascending id. totals must be >= 0. */
+size_t gc_descending_order_temp_bytes(int64_t n);
+int gc_descending_order(const int64_t* d_totals, int64_t n, int64_t* d_order, void* d_temp, size_t temp_bytes,
+                        void* stream);
+/* Inclusive scans along an order (planner.py:87-95, :239-240):
+ *   d_topo_bytes[i] = sum_{k<=i} deg(order[k])*u32_bytes + u64_bytes   (needs graph offsets)
+ *   d_hot_cum[i]    = sum_{k<=i} totals[order[k]] */
+size_t gc_order_scan_temp_bytes(int64_t n);
+int gc_topo_prefix_bytes(const uint64_t* d_row_offsets, const int64_t* d_order, int64_t n, uint32_t u32_bytes,
+                         uint32_t u64_bytes, int64_t* d_out, void* d_temp, size_t temp_bytes, void* stream);
+int gc_hot_prefix(const int64_t* d_totals, const int64_t* d_order, int64_t n, int64_t* d_out, void* d_temp,
+                  size_t temp_bytes, void* stream);
+/* np.searchsorted(prefix, budgets, side="right") with float64 budgets compared as
+ * (double)prefix <= budget (planner.py:236-237). */
+int gc_searchsorted_right(const int64_t* d_prefix, int64_t n, const double* d_budgets, int32_t num_budgets,
+                          int64_t* d_out, void* stream);
+/* distribute_prefix (planner.py:264-267): stable split of order[0:len) by owner.
+ * d_out receives the concatenation of the k_rows queues, d_counts[g] their lengths. */
+size_t gc_distribute_prefix_temp_bytes(int64_t len, uint32_t k_rows);
+int gc_distribute_prefix(const int64_t* d_order, int64_t len, const int32_t* d_owner, uint32_t k_rows,
+                         int64_t* d_out, int64_t* d_counts, void* d_temp, size_t temp_bytes, void* stream);
+
+/* --------------------------------------- host tier + peer mapping (plumbing) */
+
+/* Register host memory as mapped, read-only pinned memory (UVA host tier). */
+int gc_host_register(void* host_ptr, size_t bytes, void** d_alias);
+int gc_host_unregister(void* host_ptr);
+/* Cross-process NVLink peer slabs: 64-byte cudaIpcMemHandle_t export/import. */
+int gc_ipc_export(void* d_ptr, uint8_t* handle64);
+int gc_ipc_import(const uint8_t* handle64, void** d_ptr);
+int gc_ipc_close(void* d_ptr);
+/* Enable peer access from the current device to `peer` (same-process multi-GPU). */
+int gc_enable_peer(int peer);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GNNCACHE_B200_H */

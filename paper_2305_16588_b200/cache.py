@@ -1,0 +1,131 @@
+"""Unified feature cache and the three-tier gather (K4).
+
+The reference stores no feature values; it only defines which tier
+serves a row — local cache, the lowest-index clique peer holding it, else the CPU
+(account_assignment, simulator.py:161-202) — and materialize_assignment
+(planner.py:289-319) decides cache contents. This module builds the physical
+layout for one GPU from a CacheAssignment:
+
+  location table  u32 [n]: (owner_gpu << 28) | slot, or GC_TIER_HOST
+  slabs           fp32 [rows_g, D] per clique GPU: the local one in this GPU's HBM,
+                  the others mapped from the peers (CUDA IPC handles across processes,
+                  or device pointers when one process drives several GPUs)
+  host tier       the full fp32 table in pinned, mapped host memory (UVA over PCIe)
+
+and gathers rows with gc_gather: 16-byte vector loads, one thread per vector.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .graph import FeatureSpec
+
+TIER_NAMES = ("local", "peer", "host")
+
+
+@dataclass
+class FeatureStore:
+    """Feature rows of one GPU's view of the clique cache."""
+
+    spec: FeatureSpec
+    self_rank: int
+    num_ranks: int
+    location: torch.Tensor | None  # int32 view of u32 [n]; None = fully resident local table
+    slabs: list  # per clique rank: torch.Tensor (local/same-process) or int address (IPC-mapped)
+    host_table: torch.Tensor | None = None  # pinned fp32 [n, D]
+    tier_rows: torch.Tensor = field(default=None)  # u64[3] cumulative rows served per tier
+    _keep: list = field(default_factory=list, repr=False)
+
+    def __post_init__(self):
+        if self.tier_rows is None:
+            self.tier_rows = torch.zeros(3, dtype=torch.int64, device="cuda")
+        s = _lib.GcFeatureStore()
+        s.row_bytes = self.spec.row_bytes
+        s.self_rank = self.self_rank
+        s.num_ranks = self.num_ranks
+        s.location = _lib.ptr(self.location)
+        for g, slab in enumerate(self.slabs):
+            s.slabs[g] = slab if isinstance(slab, int) else (slab.data_ptr() if slab is not None else None)
+        s.host_rows = _lib.ptr(self.host_table)
+        self.c_struct = s
+
+    # ---------------------------------------------------------------- builders
+    @classmethod
+    def resident(cls, table: torch.Tensor) -> "FeatureStore":
+        """Whole table in local HBM (BASELINE config 2: fully HBM-cached)."""
+        if table.dtype != torch.float32 or not table.is_cuda or table.dim() != 2:
+            raise ValueError("table must be a 2-D float32 CUDA tensor")
+        return cls(FeatureSpec(table.shape[1]), 0, 1, None, [table.contiguous()])
+
+    @classmethod
+    def from_assignment(cls, host_table: np.ndarray | torch.Tensor, feat_vertices: list[np.ndarray], self_rank: int,
+                        peer_slabs: list | None = None) -> "FeatureStore":
+        """Cache laid out from CacheAssignment.feat_vertices of one clique (local ids).
+
+        Slot order is the assignment's priority order. When peer_slabs is None every
+        slab of the clique is built in this process on the current device (single
+        process driving the whole clique, or a test of the peer path on one GPU);
+        otherwise peer_slabs[g] is the mapped address of GPU g's slab."""
+        host = torch.as_tensor(host_table)
+        if host.dtype != torch.float32 or host.dim() != 2:
+            raise ValueError("host_table must be float32 [n, D]")
+        n, dim = host.shape
+        k = len(feat_vertices)
+        if not 0 <= self_rank < k or k > _lib.GC_MAX_PEERS:
+            raise ValueError("self_rank must index the clique (at most 8 GPUs)")
+        loc = np.full(n, _lib.GC_TIER_HOST, dtype=np.uint32)
+        for g, verts in enumerate(feat_vertices):
+            verts = np.asarray(verts, dtype=np.int64)
+            if len(verts) >= 1 << 28:
+                raise ValueError("at most 2^28 cached rows per GPU")
+            if len(verts) and (loc[verts] != _lib.GC_TIER_HOST).any():
+                raise ValueError("a vertex is cached on two GPUs; the clique cache is partitioned")
+            loc[verts] = (np.uint32(g) << np.uint32(28)) | np.arange(len(verts), dtype=np.uint32)
+        pinned = host.contiguous().pin_memory() if not host.is_pinned() else host
+        slabs: list = []
+        for g, verts in enumerate(feat_vertices):
+            if peer_slabs is not None and g != self_rank:
+                slabs.append(int(peer_slabs[g]))
+                continue
+            idx = torch.from_numpy(np.asarray(verts, dtype=np.int64))
+            slabs.append(pinned.index_select(0, idx).cuda() if len(idx) else torch.empty((0, dim), device="cuda"))
+        location = torch.from_numpy(loc.view(np.int32)).cuda()
+        return cls(FeatureSpec(dim), self_rank, k, location, slabs, pinned)
+
+    # ---------------------------------------------------------------- gather
+    def gather(self, ids: torch.Tensor, counts: torch.Tensor, out: torch.Tensor, num_batches: int | None = None,
+               stream=None) -> torch.Tensor:
+        """out[b, k] = X[ids[b, k]] for k < min(counts[b], out.shape[1]) (K4).
+
+        ids: int32 [W, cap] CUDA, counts: int32 [W] CUDA, out: float32 [W, rows, D]."""
+        lib = _lib.lib()
+        if ids.dim() == 1:
+            ids, out = ids.view(1, -1), out.view(1, *out.shape)
+        W = ids.shape[0] if num_batches is None else num_batches
+        if out.shape[-1] * 4 != self.spec.row_bytes:
+            raise ValueError("output row width does not match the feature store")
+        _lib.check(
+            lib.gc_gather(self.c_struct, ids.data_ptr(), ids.shape[1], counts.data_ptr(), out.shape[1], W,
+                          out.data_ptr(), out.shape[1], self.tier_rows.data_ptr(), _lib.stream_handle(stream)),
+            "gather",
+        )
+        return out
+
+    def tier_counts(self) -> dict:
+        v = self.tier_rows.cpu().numpy()
+        return {name: int(x) for name, x in zip(TIER_NAMES, v)}
+
+
+def gather_rows(store: FeatureStore, ids: np.ndarray) -> np.ndarray:
+    """Host convenience: X[ids] through the device gather (ids int64 numpy)."""
+    ids = np.asarray(ids, dtype=np.int64)
+    d = torch.from_numpy(ids.astype(np.uint32).view(np.int32)).cuda().view(1, -1)
+    cnt = torch.tensor([len(ids)], dtype=torch.int32, device="cuda")
+    out = torch.empty((1, max(len(ids), 1), store.spec.dimension), dtype=torch.float32, device="cuda")
+    store.gather(d, cnt, out)
+    return out[0, : len(ids)].cpu().numpy()

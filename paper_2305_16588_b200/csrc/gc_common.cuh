@@ -1,0 +1,127 @@
+// Shared device helpers for libgnncache_b200: the reference's splitmix64 stream,
+// status/error plumbing, and the single-pass (decoupled look-back) tile scan used
+// by the hop expansion and the bitmap compaction.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "gnncache_b200.h"
+
+namespace gc {
+
+// rng.py:13-16
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t kMixA = 0xBF58476D1CE4E5B9ull;
+constexpr uint64_t kMixB = 0x94D049BB133111EBull;
+constexpr unsigned kFull = 0xFFFFFFFFu;
+
+// splitmix64 finalizer, rng.py:23-31 (wrapping u64 arithmetic is native here).
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x ^= x >> 30;
+    x *= kMixA;
+    x ^= x >> 27;
+    x *= kMixB;
+    x ^= x >> 31;
+    return x;
+}
+
+// KeyedRng.hash_counters(a) = mix64((a + G) ^ key), rng.py:64-66
+__host__ __device__ __forceinline__ uint64_t hash_counter(uint64_t key, uint64_t a) {
+    return mix64((a + kGolden) ^ key);
+}
+
+// KeyedRng.hash_pairs(a, b) = mix64((b + G) ^ hash_counters(a)), rng.py:68-72;
+// `ha` is the per-position hash_counter, hoisted out of the per-edge loop.
+__host__ __device__ __forceinline__ uint64_t hash_pair(uint64_t ha, uint64_t b) {
+    return mix64((b + kGolden) ^ ha);
+}
+
+void set_error(const std::string& msg);
+int cuda_status(cudaError_t err, const char* what);
+
+#define GC_CHECK_LAUNCH(what)                                               \
+    do {                                                                    \
+        cudaError_t _e = cudaGetLastError();                                \
+        if (_e != cudaSuccess) return ::gc::cuda_status(_e, what);          \
+    } while (0)
+
+#define GC_TRY(expr, what)                                                  \
+    do {                                                                    \
+        cudaError_t _e = (expr);                                            \
+        if (_e != cudaSuccess) return ::gc::cuda_status(_e, what);          \
+    } while (0)
+
+#define GC_REQUIRE(cond, code, msg)                                         \
+    do {                                                                    \
+        if (!(cond)) {                                                      \
+            ::gc::set_error(msg);                                           \
+            return code;                                                    \
+        }                                                                   \
+    } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// ------------------------------------------------------------------------------
+// Decoupled look-back for segmented single-pass scans. Tile status words pack a
+// 2-bit flag (1 = aggregate available, 2 = inclusive prefix available) over a
+// 62-bit value; an aligned 64-bit store publishes both atomically, so no fence is
+// needed between value and flag. Tiles are claimed in launch order from a
+// counter, so every predecessor a tile waits on is already resident (no deadlock).
+// ------------------------------------------------------------------------------
+constexpr uint64_t kFlagAgg = 1ull << 62;
+constexpr uint64_t kFlagPre = 2ull << 62;
+constexpr uint64_t kValMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ void publish(uint64_t* state, uint64_t word) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(state), "l"(word) : "memory");
+}
+
+__device__ __forceinline__ uint64_t peek(const uint64_t* state) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(state) : "memory");
+    return v;
+}
+
+// Called by one full warp. `first` is the status index of the segment's first tile
+// and `self` this tile's index (first <= self). Returns the exclusive prefix of this
+// tile within its segment and publishes the inclusive prefix.
+__device__ __forceinline__ uint64_t lookback_warp(uint64_t* state, uint64_t first, uint64_t self,
+                                                  uint64_t aggregate) {
+    const int lane = threadIdx.x & 31;
+    if (self == first) {
+        if (lane == 0) publish(state + self, kFlagPre | aggregate);
+        return 0;
+    }
+    uint64_t exclusive = 0;
+    int64_t window_end = (int64_t)self - 1;  // highest predecessor not yet consumed
+    while (true) {
+        int64_t idx = window_end - lane;
+        uint64_t word = 0;
+        bool in_range = idx >= (int64_t)first;
+        if (in_range) {
+            do {
+                word = peek(state + idx);
+            } while ((word >> 62) == 0);
+        }
+        // lanes before the segment start behave as a zero inclusive prefix
+        bool is_pre = !in_range || (word >> 62) == 2;
+        unsigned pre_mask = __ballot_sync(kFull, is_pre);
+        // nearest predecessor holding an inclusive prefix, or 32 if none in this window
+        int stop = pre_mask ? __ffs(pre_mask) - 1 : 32;
+        uint64_t contrib = (lane <= stop && in_range) ? (word & kValMask) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) contrib += __shfl_xor_sync(kFull, contrib, o);
+        exclusive += contrib;
+        if (pre_mask) break;
+        window_end -= 32;
+    }
+    if (lane == 0) publish(state + self, kFlagPre | (exclusive + aggregate));
+    return exclusive;
+}
+
+}  // namespace gc

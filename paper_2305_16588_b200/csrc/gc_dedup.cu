@@ -1,0 +1,204 @@
+// K3 unique + relabel: BatchSample.distinct_vertices (sampling.py:73-75) is np.unique,
+// i.e. the sorted distinct ids. Every emitted vertex marks a per-batch visited bitmap
+// inside hop_expand, so the sorted unique list falls out of one ordered popcount scan
+// of the bitmap (no sort). The per-word exclusive popcount doubles as the relabel map:
+// local(u) = prefix[u >> 5] + popc(word & lanes-below(u)).
+#include <cub/block/block_scan.cuh>
+
+#include "gc_common.cuh"
+
+namespace gc {
+
+constexpr int kUniqThreads = 256;
+constexpr int kWordsPerThread = 4;
+constexpr int kWordsPerTile = kUniqThreads * kWordsPerThread;
+
+struct UniqueParams {
+    uint32_t* bm;
+    uint64_t bwords;
+    uint32_t tiles_per_batch;
+    uint32_t* uniq;
+    uint64_t ustride;
+    uint32_t* ucount;
+    uint32_t* wprefix;
+    uint64_t* feat;
+    int clear;
+    uint64_t* tile_state;
+    uint32_t* tile_counter;
+};
+
+__global__ void __launch_bounds__(kUniqThreads) k_unique(UniqueParams p) {
+    using Scan = cub::BlockScan<uint32_t, kUniqThreads>;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ uint32_t s_vid;
+    __shared__ uint64_t s_prefix;
+    const int tid = threadIdx.x;
+    if (tid == 0) s_vid = atomicAdd(p.tile_counter, 1u);
+    __syncthreads();
+    const uint32_t b = s_vid / p.tiles_per_batch;
+    const uint32_t t = s_vid % p.tiles_per_batch;
+    const uint64_t w0 = (uint64_t)t * kWordsPerTile + (uint64_t)tid * kWordsPerThread;
+    uint32_t* row = p.bm + b * p.bwords;
+    uint4 x = make_uint4(0, 0, 0, 0);
+    if (w0 < p.bwords) x = *reinterpret_cast<const uint4*>(row + w0);  // bwords is a multiple of 4
+    const uint32_t c0 = __popc(x.x), c1 = __popc(x.y), c2 = __popc(x.z), c3 = __popc(x.w);
+    uint32_t excl, total;
+    Scan(scan_tmp).ExclusiveSum(c0 + c1 + c2 + c3, excl, total);
+    const uint64_t sidx = (uint64_t)b * p.tiles_per_batch + t;
+    if (tid == 0 && t != 0) publish(p.tile_state + sidx, kFlagAgg | total);
+    if (tid < 32) {
+        uint64_t pre = lookback_warp(p.tile_state, (uint64_t)b * p.tiles_per_batch, sidx, total);
+        if (tid == 0) s_prefix = pre;
+    }
+    __syncthreads();
+    const uint32_t base = (uint32_t)s_prefix + excl;
+    if (w0 < p.bwords) {
+        if (p.wprefix)
+            *reinterpret_cast<uint4*>(p.wprefix + b * p.bwords + w0) =
+                make_uint4(base, base + c0, base + c0 + c1, base + c0 + c1 + c2);
+        uint32_t* out = p.uniq + b * p.ustride;
+        uint32_t pos = base;
+        const uint32_t words[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            uint32_t w = words[k];
+            const uint32_t vbase = (uint32_t)((w0 + k) * 32);
+            while (w) {
+                const uint32_t u = vbase + (__ffs(w) - 1);
+                out[pos++] = u;
+                if (p.feat) atomicAdd((unsigned long long*)(p.feat + u), 1ull);
+                w &= w - 1;
+            }
+        }
+        if (p.clear && (x.x | x.y | x.z | x.w)) *reinterpret_cast<uint4*>(row + w0) = make_uint4(0, 0, 0, 0);
+    }
+    if (t == p.tiles_per_batch - 1 && tid == kUniqThreads - 1) p.ucount[b] = (uint32_t)s_prefix + excl + c0 + c1 + c2 + c3;
+}
+
+__global__ void k_relabel(const uint32_t* __restrict__ ids, uint64_t stride, const uint32_t* __restrict__ count,
+                          const uint32_t* __restrict__ bm, const uint32_t* __restrict__ wp, uint64_t bwords,
+                          uint32_t* __restrict__ local) {
+    const uint32_t b = blockIdx.y;
+    const uint32_t c = count[b];
+    const uint32_t* row = bm + b * bwords;
+    const uint32_t* pre = wp + b * bwords;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < c; k += gridDim.x * blockDim.x) {
+        const uint32_t u = ids[b * stride + k];
+        const uint32_t w = u >> 5;
+        const uint32_t below = (1u << (u & 31)) - 1u;
+        local[b * stride + k] = __ldg(pre + w) + __popc(__ldg(row + w) & below);
+    }
+}
+
+__global__ void k_bitmap_clear(uint32_t* bm, uint64_t bwords, const uint32_t* __restrict__ uniq, uint64_t ustride,
+                               const uint32_t* __restrict__ ucount) {
+    const uint32_t b = blockIdx.y;
+    const uint32_t c = ucount[b];
+    uint32_t* row = bm + b * bwords;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < c; k += gridDim.x * blockDim.x)
+        row[uniq[b * ustride + k] >> 5] = 0u;
+}
+
+__global__ void k_mark(const uint32_t* __restrict__ ids, uint64_t stride, const uint32_t* __restrict__ count,
+                       uint32_t* bm, uint64_t bwords) {
+    const uint32_t b = blockIdx.y;
+    const uint32_t c = count[b];
+    uint32_t* row = bm + b * bwords;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < c; k += gridDim.x * blockDim.x) {
+        const uint32_t u = ids[b * stride + k];
+        atomicOr(row + (u >> 5), 1u << (u & 31));
+    }
+}
+
+static unsigned uniq_tiles(uint64_t bwords) {
+    uint64_t t = (bwords + kWordsPerTile - 1) / kWordsPerTile;
+    return t ? (unsigned)t : 1u;
+}
+
+static unsigned grid_x(uint32_t max_count, int block) {
+    uint64_t g = ((uint64_t)max_count + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > 1024) g = 1024;
+    return (unsigned)g;
+}
+
+}  // namespace gc
+
+using namespace gc;
+
+extern "C" {
+
+uint64_t gc_bitmap_words(int64_t num_vertices) {
+    uint64_t w = ((uint64_t)(num_vertices > 0 ? num_vertices : 0) + 31) / 32;
+    return (w + 3) / 4 * 4;
+}
+
+size_t gc_unique_temp_bytes(uint32_t num_batches, uint64_t bitmap_words) {
+    return align_up((size_t)num_batches * uniq_tiles(bitmap_words) * sizeof(uint64_t), 256) + 256;
+}
+
+int gc_unique_compact(uint32_t* d_bitmap, uint64_t bitmap_words, uint32_t num_batches, uint32_t* d_unique,
+                      uint64_t unique_stride, uint32_t* d_unique_count, uint32_t* d_word_prefix,
+                      uint64_t* d_feat_lookups, int clear_bitmap, void* d_temp, size_t temp_bytes,
+                      void* stream) {
+    GC_REQUIRE(bitmap_words % 4 == 0, GC_ERR_VALUE, "gc_unique_compact: bitmap_words must be a multiple of 4");
+    if (num_batches == 0) return GC_OK;
+    const size_t need = gc_unique_temp_bytes(num_batches, bitmap_words);
+    GC_REQUIRE(d_temp && temp_bytes >= need, GC_ERR_VALUE, "gc_unique_compact: temp buffer too small");
+    cudaStream_t s = as_stream(stream);
+    const unsigned tiles = uniq_tiles(bitmap_words);
+    const size_t state_bytes = align_up((size_t)num_batches * tiles * sizeof(uint64_t), 256);
+    UniqueParams p{};
+    p.bm = d_bitmap;
+    p.bwords = bitmap_words;
+    p.tiles_per_batch = tiles;
+    p.uniq = d_unique;
+    p.ustride = unique_stride;
+    p.ucount = d_unique_count;
+    p.wprefix = d_word_prefix;
+    p.feat = d_feat_lookups;
+    p.clear = clear_bitmap;
+    p.tile_state = static_cast<uint64_t*>(d_temp);
+    p.tile_counter = reinterpret_cast<uint32_t*>(static_cast<char*>(d_temp) + state_bytes);
+    GC_TRY(cudaMemsetAsync(d_temp, 0, state_bytes + 256, s), "gc_unique_compact memset");
+    const uint64_t grid = (uint64_t)num_batches * tiles;
+    GC_REQUIRE(grid < (1ull << 31), GC_ERR_VALUE, "gc_unique_compact: window too large");
+    k_unique<<<(unsigned)grid, kUniqThreads, 0, s>>>(p);
+    GC_CHECK_LAUNCH("gc_unique_compact");
+    return GC_OK;
+}
+
+int gc_relabel(const uint32_t* d_ids, uint64_t ids_stride, const uint32_t* d_ids_count, uint32_t max_count,
+               uint32_t num_batches, const uint32_t* d_bitmap, const uint32_t* d_word_prefix,
+               uint64_t bitmap_words, uint32_t* d_local, void* stream) {
+    GC_REQUIRE(num_batches < 65536, GC_ERR_VALUE, "gc_relabel: at most 65535 batches per call");
+    if (num_batches == 0 || max_count == 0) return GC_OK;
+    dim3 grid(grid_x(max_count, 256), num_batches);
+    k_relabel<<<grid, 256, 0, as_stream(stream)>>>(d_ids, ids_stride, d_ids_count, d_bitmap, d_word_prefix,
+                                                   bitmap_words, d_local);
+    GC_CHECK_LAUNCH("gc_relabel");
+    return GC_OK;
+}
+
+int gc_mark_visited(const uint32_t* d_ids, uint64_t ids_stride, const uint32_t* d_count, uint32_t max_count,
+                    uint32_t num_batches, uint32_t* d_bitmap, uint64_t bitmap_words, void* stream) {
+    GC_REQUIRE(num_batches < 65536, GC_ERR_VALUE, "gc_mark_visited: at most 65535 batches per call");
+    if (num_batches == 0 || max_count == 0) return GC_OK;
+    dim3 grid(grid_x(max_count, 256), num_batches);
+    k_mark<<<grid, 256, 0, as_stream(stream)>>>(d_ids, ids_stride, d_count, d_bitmap, bitmap_words);
+    GC_CHECK_LAUNCH("gc_mark_visited");
+    return GC_OK;
+}
+
+int gc_bitmap_clear(uint32_t* d_bitmap, uint64_t bitmap_words, uint32_t num_batches, const uint32_t* d_unique,
+                    uint64_t unique_stride, const uint32_t* d_unique_count, uint32_t max_unique, void* stream) {
+    GC_REQUIRE(num_batches < 65536, GC_ERR_VALUE, "gc_bitmap_clear: at most 65535 batches per call");
+    if (num_batches == 0 || max_unique == 0) return GC_OK;
+    dim3 grid(grid_x(max_unique, 256), num_batches);
+    k_bitmap_clear<<<grid, 256, 0, as_stream(stream)>>>(d_bitmap, bitmap_words, d_unique, unique_stride,
+                                                        d_unique_count);
+    GC_CHECK_LAUNCH("gc_bitmap_clear");
+    return GC_OK;
+}
+
+}  // extern "C"

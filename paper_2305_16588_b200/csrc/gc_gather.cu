@@ -1,0 +1,193 @@
+// K4 gather3tier + K5 hotness scatter.
+//
+// gather: every distinct vertex of a batch gets its feature row from the tier that
+// holds it (the serving rule of account_assignment, simulator.py:161-202):
+//   local HBM slab, an NVLink/NVSwitch peer's slab (one-sided loads through a mapped
+//   peer pointer; the owner is the unique holder CSLP assigned, planner.py:54-55), or
+//   the host feature table over PCIe through a UVA pointer to mapped pinned memory.
+// Rows move as 16-byte vectors with one thread per vector, so a warp covers
+// contiguous output and each row's source bytes are read once, fully coalesced.
+#include "gc_common.cuh"
+
+namespace gc {
+
+struct GatherParams {
+    gc_feature_store_t fs;
+    const uint32_t* ids;
+    uint64_t ids_stride;
+    const uint32_t* count;
+    char* out;
+    uint64_t out_stride_rows;
+    uint64_t* tier_rows;
+    uint32_t max_rows;
+};
+
+__device__ __forceinline__ uint4 ld_stream16(const void* ptr) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(ptr));
+    return r;
+}
+
+__device__ __forceinline__ void st_stream16(void* ptr, uint4 v) {
+    asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(ptr), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+// tier: 0 local, 1 peer, 2 host
+__device__ __forceinline__ const char* row_source(const gc_feature_store_t& fs, uint32_t u, int& tier) {
+    if (fs.location == nullptr) {
+        tier = 0;
+        return static_cast<const char*>(fs.slabs[fs.self_rank]) + (uint64_t)u * fs.row_bytes;
+    }
+    const uint32_t loc = __ldg(fs.location + u);
+    if (loc == GC_TIER_HOST) {
+        tier = 2;
+        return static_cast<const char*>(fs.host_rows) + (uint64_t)u * fs.row_bytes;
+    }
+    const uint32_t g = loc >> 28;
+    tier = (g == fs.self_rank) ? 0 : 1;
+    return static_cast<const char*>(fs.slabs[g]) + (uint64_t)(loc & 0x0FFFFFFFu) * fs.row_bytes;
+}
+
+template <int VEC>
+__global__ void __launch_bounds__(256) k_gather(GatherParams p) {
+    __shared__ unsigned long long s_tier[3];
+    const uint32_t b = blockIdx.y;
+    const uint32_t rows = min(p.count[b], p.max_rows);  // capacity clamp; caller checks overflow
+    const uint32_t per_row = p.fs.row_bytes / VEC;
+    const uint64_t total = (uint64_t)rows * per_row;
+    const uint32_t* ids = p.ids + b * p.ids_stride;
+    char* out = p.out + b * p.out_stride_rows * p.fs.row_bytes;
+    if (p.tier_rows && threadIdx.x < 3) s_tier[threadIdx.x] = 0;
+    if (p.tier_rows) __syncthreads();
+    unsigned long long cnt[3] = {0, 0, 0};
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = (uint32_t)(i / per_row);
+        const uint32_t c = (uint32_t)(i - (uint64_t)k * per_row);
+        int tier;
+        const char* src = row_source(p.fs, __ldg(ids + k), tier) + (uint64_t)c * VEC;
+        char* dst = out + (uint64_t)k * p.fs.row_bytes + (uint64_t)c * VEC;
+        if constexpr (VEC == 16) {
+            st_stream16(dst, ld_stream16(src));
+        } else {
+            *reinterpret_cast<uint32_t*>(dst) = __ldg(reinterpret_cast<const uint32_t*>(src));
+        }
+        if (c == 0) cnt[tier] += 1;
+    }
+    if (p.tier_rows) {
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+            unsigned long long v = cnt[t];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+            if ((threadIdx.x & 31) == 0 && v) atomicAdd(&s_tier[t], v);
+        }
+        __syncthreads();
+        if (threadIdx.x < 3 && s_tier[threadIdx.x])
+            atomicAdd((unsigned long long*)(p.tier_rows + threadIdx.x), s_tier[threadIdx.x]);
+    }
+}
+
+// accumulate_hotness bincount (sampling.py:171-173) with warp aggregation for hot ids
+__global__ void k_scatter_add(const uint32_t* __restrict__ ids, const uint32_t* __restrict__ w, int64_t n,
+                              uint64_t* counter) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        const bool valid = i < n;
+        const uint32_t u = valid ? ids[i] : 0u;
+        const uint64_t add = valid ? (w ? (uint64_t)w[i] : 1ull) : 0ull;
+        const unsigned act = __ballot_sync(kFull, valid);
+        if (valid) {
+            const unsigned peers = __match_any_sync(act, u);
+            // segmented sum over the peer group through shuffles
+            uint64_t sum = 0;
+            unsigned rem = peers;
+            while (rem) {
+                const int src = __ffs(rem) - 1;
+                sum += __shfl_sync(peers, add, src);
+                rem &= rem - 1;
+            }
+            if (lane == __ffs(peers) - 1 && sum) atomicAdd((unsigned long long*)(counter + u), (unsigned long long)sum);
+        }
+    }
+}
+
+// Deterministic synthetic feature table (bench/test input, identical to the CPU
+// restatement in oracle/): X[v, d] = (mix64(v*D + d) >> 40) * 2^-24 - 0.5, exact in fp32.
+__global__ void k_synth_features(uint64_t first_row, uint64_t rows, uint32_t dim, float* __restrict__ out) {
+    const uint64_t total = rows * dim;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t v = first_row + i / dim;
+        const uint64_t d = i % dim;
+        out[i] = (float)(mix64(v * dim + d) >> 40) * (1.0f / 16777216.0f) - 0.5f;
+    }
+}
+
+}  // namespace gc
+
+using namespace gc;
+
+extern "C" {
+
+int gc_gather(const gc_feature_store_t* store, const uint32_t* d_ids, uint64_t ids_stride, const uint32_t* d_count,
+              uint32_t max_count, uint32_t num_batches, void* d_out, uint64_t out_stride_rows, uint64_t* d_tier_rows,
+              void* stream) {
+    GC_REQUIRE(store, GC_ERR_VALUE, "gc_gather: store is null");
+    GC_REQUIRE(store->row_bytes > 0 && store->row_bytes % 4 == 0, GC_ERR_VALUE,
+               "gc_gather: row_bytes must be a positive multiple of 4");
+    GC_REQUIRE(store->self_rank < GC_MAX_PEERS, GC_ERR_VALUE, "gc_gather: self_rank out of range");
+    GC_REQUIRE(num_batches < 65536, GC_ERR_VALUE, "gc_gather: at most 65535 batches per call");
+    if (num_batches == 0 || max_count == 0) return GC_OK;
+    GatherParams p{};
+    p.fs = *store;
+    p.ids = d_ids;
+    p.ids_stride = ids_stride;
+    p.count = d_count;
+    p.out = static_cast<char*>(d_out);
+    p.out_stride_rows = out_stride_rows;
+    p.tier_rows = d_tier_rows;
+    p.max_rows = max_count;
+    const bool vec16 = store->row_bytes % 16 == 0 && ((uintptr_t)d_out % 16 == 0);
+    const uint32_t per_row = store->row_bytes / (vec16 ? 16 : 4);
+    uint64_t work = (uint64_t)max_count * per_row;
+    uint64_t gx = (work + 255) / 256;
+    // enough CTAs to fill 148 SMs for the whole window; grid-stride beyond that
+    const uint64_t cap = (uint64_t)148 * 16 / num_batches;
+    if (gx > cap) gx = cap;
+    if (gx < 1) gx = 1;
+    dim3 grid((unsigned)gx, num_batches);
+    if (vec16)
+        k_gather<16><<<grid, 256, 0, as_stream(stream)>>>(p);
+    else
+        k_gather<4><<<grid, 256, 0, as_stream(stream)>>>(p);
+    GC_CHECK_LAUNCH("gc_gather");
+    return GC_OK;
+}
+
+int gc_synth_features(uint64_t first_row, uint64_t rows, uint32_t dim, float* d_out, void* stream) {
+    GC_REQUIRE(dim >= 1, GC_ERR_VALUE, "feature dimension must be >= 1");
+    if (rows == 0) return GC_OK;
+    uint64_t g = (rows * dim + 255) / 256;
+    if (g > 148 * 64) g = 148 * 64;
+    k_synth_features<<<(unsigned)g, 256, 0, as_stream(stream)>>>(first_row, rows, dim, d_out);
+    GC_CHECK_LAUNCH("gc_synth_features");
+    return GC_OK;
+}
+
+int gc_scatter_add(const uint32_t* d_ids, const uint32_t* d_weights, int64_t count, uint64_t* d_counter,
+                   void* stream) {
+    GC_REQUIRE(count >= 0, GC_ERR_VALUE, "gc_scatter_add: count must be >= 0");
+    if (count == 0) return GC_OK;
+    int64_t g = (count + 255) / 256;
+    if (g > 148 * 32) g = 148 * 32;
+    k_scatter_add<<<(unsigned)g, 256, 0, as_stream(stream)>>>(d_ids, d_weights, count, d_counter);
+    GC_CHECK_LAUNCH("gc_scatter_add");
+    return GC_OK;
+}
+
+}  // extern "C"

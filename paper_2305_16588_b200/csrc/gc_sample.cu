@@ -1,0 +1,368 @@
+// K2 hop_expand: one hop of the reference's L-hop sampler (_expand_frontier,
+// sampling.py:84-117) for a window of W independent mini-batches in one launch.
+//
+// Per CTA tile of 256 frontier positions (claimed in order from a counter):
+//   phase 1  thread-per-position: v, row offsets, deg, take = min(deg, fanout);
+//            presampling counters (warp-aggregated), seed marking; CTA scan of take;
+//            the tile aggregate is published for the decoupled look-back.
+//   phase 2a warp-per-position selection into a shared-memory list of source edge
+//            indices (copy path: CSR order; choice path: the `fanout` smallest
+//            (hash_pairs(i, j), j) in ascending order — bit-exact with the lexsort at
+//            sampling.py:108-114 and the scalar oracle tests/helpers.py:95-110).
+//   look-back exclusive prefix of the batch's output (overlaps phase 2a latency).
+//   phase 2b flat, coalesced emission: out[prefix + k] = col[src_edge[k]], marking the
+//            batch's visited bitmap for dedup (K3).
+// Keys depend only on (position, edge index), never on neighbour ids (rng.py:68-72),
+// so only the `take` selected column entries are read from the topology.
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include "gc_common.cuh"
+
+namespace gc {
+
+constexpr int kHopThreads = 256;
+constexpr int kTilePos = 256;
+constexpr int kItemCap = 4096;  // staged output items per round (32 KB of u64 edge indices)
+
+struct HopParams {
+    const uint64_t* ro;
+    const uint32_t* ci;
+    uint64_t n;
+    const uint32_t* frontier;
+    uint64_t fstride;
+    const uint32_t* fcount;
+    uint32_t fanout;
+    uint32_t tiles_per_batch;
+    const uint64_t* hop_keys;
+    uint32_t* out_off;
+    uint64_t ostride;
+    uint32_t* out_nbrs;
+    uint64_t nstride;
+    uint32_t* out_count;
+    uint32_t* bitmap;
+    uint64_t bwords;
+    int mark_frontier;
+    uint64_t* topo_reads;
+    uint64_t* edge_trav;
+    uint64_t* txn_total;
+    uint32_t cls;
+    uint32_t u32b;
+    uint64_t* tile_state;
+    uint32_t* tile_counter;
+};
+
+__device__ __forceinline__ void mark_visited(uint32_t* bm, uint32_t u) {
+    uint32_t* w = bm + (u >> 5);
+    uint32_t bit = 1u << (u & 31);
+    // bits only go 0 -> 1 inside a launch, so a stale cached read can only cost a
+    // redundant atomic, never a missed mark
+    if (!(*w & bit)) atomicOr(w, bit);
+}
+
+__device__ __forceinline__ void stage(uint64_t* s_items, uint32_t item, uint32_t r0, uint32_t r1, uint64_t edge) {
+    if (item >= r0 && item < r1) s_items[item - r0] = edge;
+}
+
+// Exact winner among lanes in `cand` by (lo32 of key, edge index) once the high
+// words tie; all lanes return the same winning edge index.
+__device__ __forceinline__ uint32_t tie_break(unsigned cand, uint64_t key, uint32_t j) {
+    const int lane = threadIdx.x & 31;
+    bool in = (cand >> lane) & 1u;
+    uint32_t lo = in ? (uint32_t)key : 0xFFFFFFFFu;
+    uint32_t jj = in ? j : 0xFFFFFFFFu;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        uint32_t olo = __shfl_xor_sync(kFull, lo, o);
+        uint32_t oj = __shfl_xor_sync(kFull, jj, o);
+        if (olo < lo || (olo == lo && oj < jj)) {
+            lo = olo;
+            jj = oj;
+        }
+    }
+    return jj;
+}
+
+// Choice path with every candidate key resident in registers: lane l holds edges
+// j = l + 32 r for r < R. Extracts the first min(fanout, needed) minima in order.
+template <int R>
+__device__ __forceinline__ void select_registers(uint64_t hc, uint32_t deg, uint32_t fanout, uint64_t o0,
+                                                 uint32_t excl, uint32_t r0, uint32_t r1, uint64_t* s_items) {
+    const int lane = threadIdx.x & 31;
+    uint64_t key[R];
+    unsigned live = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        uint32_t j = lane + 32 * r;
+        key[r] = hash_pair(hc, j);
+        if (j < deg) live |= 1u << r;
+    }
+    // extraction beyond the staged window is not needed
+    uint32_t stop = min(fanout, r1 - excl);
+    for (uint32_t it = 0; it < stop; ++it) {
+        uint64_t lm = ~0ull;
+        int lr = -1;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if (((live >> r) & 1u) && (lr < 0 || key[r] < lm)) {
+                lm = key[r];
+                lr = r;
+            }
+        }
+        uint32_t hi = lr >= 0 ? (uint32_t)(lm >> 32) : 0xFFFFFFFFu;
+        uint32_t m = __reduce_min_sync(kFull, hi);
+        unsigned cand = __ballot_sync(kFull, lr >= 0 && hi == m);
+        int w;
+        if (__popc(cand) == 1) {
+            w = __ffs(cand) - 1;
+        } else {
+            w = (int)(tie_break(cand, lm, lane + 32u * (uint32_t)(lr < 0 ? 0 : lr)) & 31u);
+        }
+        if (lane == w) {
+            stage(s_items, excl + it, r0, r1, o0 + (uint64_t)(lane + 32 * lr));
+            live &= ~(1u << lr);
+        }
+    }
+}
+
+// Choice path for long adjacency lists: keys are recomputed each extraction step
+// above the last emitted (key, j), so any degree is handled exactly.
+__device__ void select_streaming(uint64_t hc, uint32_t deg, uint32_t fanout, uint64_t o0, uint32_t excl, uint32_t r0,
+                                 uint32_t r1, uint64_t* s_items) {
+    const int lane = threadIdx.x & 31;
+    uint64_t lk = 0;
+    uint32_t lj = 0;
+    bool have_last = false;
+    uint32_t stop = min(fanout, r1 - excl);
+    for (uint32_t it = 0; it < stop; ++it) {
+        uint64_t bk = ~0ull;
+        uint32_t bj = 0xFFFFFFFFu;
+        for (uint32_t j = lane; j < deg; j += 32) {
+            uint64_t k = hash_pair(hc, j);
+            if (have_last && (k < lk || (k == lk && j <= lj))) continue;
+            if (bj == 0xFFFFFFFFu || k < bk) {
+                bk = k;
+                bj = j;
+            }
+        }
+        // warp argmin over (key, j)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            uint64_t ok = __shfl_xor_sync(kFull, bk, o);
+            uint32_t oj = __shfl_xor_sync(kFull, bj, o);
+            if (oj != 0xFFFFFFFFu && (bj == 0xFFFFFFFFu || ok < bk || (ok == bk && oj < bj))) {
+                bk = ok;
+                bj = oj;
+            }
+        }
+        if (lane == 0) stage(s_items, excl + it, r0, r1, o0 + bj);
+        lk = bk;
+        lj = bj;
+        have_last = true;
+    }
+}
+
+__global__ void __launch_bounds__(kHopThreads) k_hop_expand(HopParams p) {
+    using Scan = cub::BlockScan<uint32_t, kHopThreads>;
+    using Reduce = cub::BlockReduce<uint64_t, kHopThreads>;
+    __shared__ union {
+        typename Scan::TempStorage scan;
+        typename Reduce::TempStorage reduce;
+    } tmp;
+    __shared__ uint64_t s_off0[kTilePos];
+    __shared__ uint32_t s_deg[kTilePos];
+    __shared__ uint32_t s_excl[kTilePos + 1];
+    __shared__ uint64_t s_items[kItemCap];
+    __shared__ uint32_t s_vid;
+    __shared__ uint64_t s_prefix;
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    if (tid == 0) s_vid = atomicAdd(p.tile_counter, 1u);
+    __syncthreads();
+    const uint32_t vid = s_vid;
+    const uint32_t b = vid / p.tiles_per_batch;
+    const uint32_t t = vid % p.tiles_per_batch;
+    const uint32_t F = p.fcount[b];
+    const uint64_t p0 = (uint64_t)t * kTilePos;
+    if (p0 >= F && t != 0) return;  // past the end of this batch's frontier: no successor needs it
+    const uint32_t npos = p0 < F ? (uint32_t)((F - p0) < (uint64_t)kTilePos ? (F - p0) : (uint64_t)kTilePos) : 0u;
+
+    // ---- phase 1: per-position degree and take
+    const bool valid = tid < (int)npos;
+    uint32_t v = 0, deg = 0, take = 0;
+    uint64_t o0 = 0;
+    if (valid) {
+        v = p.frontier[b * p.fstride + p0 + tid];
+        if (v < p.n) {
+            o0 = p.ro[v];
+            deg = (uint32_t)(p.ro[v + 1] - o0);
+        }
+        take = min(deg, p.fanout);
+        if (p.mark_frontier && p.bitmap) mark_visited(p.bitmap + b * p.bwords, v);
+    }
+    s_off0[tid] = o0;
+    s_deg[tid] = deg;
+    if (p.topo_reads || p.edge_trav) {
+        unsigned act = __ballot_sync(kFull, valid);
+        if (valid) {
+            // vertex 0 of a Zipf graph fills ~1/5 of a frontier: one atomic per
+            // distinct vertex per warp (take depends on v only)
+            unsigned peers = __match_any_sync(act, v);
+            if (lane == __ffs(peers) - 1) {
+                unsigned long long c = __popc(peers);
+                if (p.topo_reads) atomicAdd((unsigned long long*)(p.topo_reads + v), c);
+                if (p.edge_trav && take) atomicAdd((unsigned long long*)(p.edge_trav + v), c * take);
+            }
+        }
+    }
+    if (p.txn_total) {
+        // t(v) = 1 + ceil(nc(v) * uint32_bytes / CLS), sampling.py:177-187
+        uint64_t tv = valid ? 1ull + ((uint64_t)deg * p.u32b + p.cls - 1) / p.cls : 0ull;
+        uint64_t sum = Reduce(tmp.reduce).Sum(tv);
+        if (tid == 0 && sum) atomicAdd((unsigned long long*)p.txn_total, (unsigned long long)sum);
+        __syncthreads();
+    }
+    uint32_t excl, total;
+    Scan(tmp.scan).ExclusiveSum(take, excl, total);
+    s_excl[tid] = excl;
+    if (tid == 0) s_excl[kTilePos] = total;
+    const uint64_t sidx = (uint64_t)b * p.tiles_per_batch + t;
+    const uint64_t sfirst = (uint64_t)b * p.tiles_per_batch;
+    if (tid == 0 && t != 0) publish(p.tile_state + sidx, kFlagAgg | total);
+    __syncthreads();
+
+    const uint64_t hop_key = p.hop_keys[b];
+    uint32_t* out = p.out_nbrs + b * p.nstride;
+    uint32_t* bm = p.bitmap ? p.bitmap + b * p.bwords : nullptr;
+    const uint32_t rounds = (total + kItemCap - 1) / kItemCap;
+
+    for (uint32_t r = 0; r < max(rounds, 1u); ++r) {
+        const uint32_t r0 = r * kItemCap;
+        const uint32_t r1 = min(total, r0 + kItemCap);
+        // ---- phase 2a: stage source edge indices of items [r0, r1)
+        for (uint32_t i = warp; i < npos; i += kHopThreads / 32) {
+            const uint32_t e0 = s_excl[i];
+            const uint32_t e1 = s_excl[i + 1];
+            if (e1 <= r0 || e0 >= r1) continue;
+            const uint32_t d = s_deg[i];
+            const uint64_t base = s_off0[i];
+            if (d <= p.fanout) {
+                for (uint32_t k = lane; k < d; k += 32) stage(s_items, e0 + k, r0, r1, base + k);
+            } else {
+                // hash_counters(position), position = index within this batch's frontier
+                const uint64_t hc = hash_counter(hop_key, p0 + i);
+                if (d <= 32)
+                    select_registers<1>(hc, d, p.fanout, base, e0, r0, r1, s_items);
+                else if (d <= 64)
+                    select_registers<2>(hc, d, p.fanout, base, e0, r0, r1, s_items);
+                else if (d <= 128)
+                    select_registers<4>(hc, d, p.fanout, base, e0, r0, r1, s_items);
+                else
+                    select_streaming(hc, d, p.fanout, base, e0, r0, r1, s_items);
+            }
+        }
+        if (r == 0) {
+            // ---- look-back for the batch-level output prefix of this tile
+            if (warp == 0) {
+                uint64_t pre = lookback_warp(p.tile_state, sfirst, sidx, total);
+                if (lane == 0) s_prefix = pre;
+            }
+            __syncthreads();
+            const uint32_t prefix = (uint32_t)s_prefix;
+            uint32_t* offs = p.out_off + b * p.ostride;
+            if (valid) offs[p0 + tid] = prefix + excl;
+            if (valid && p0 + tid + 1 == F) {
+                offs[F] = prefix + excl + take;
+                p.out_count[b] = prefix + excl + take;
+            }
+            if (F == 0 && tid == 0) {
+                offs[0] = 0;
+                p.out_count[b] = 0;
+            }
+        } else {
+            __syncthreads();
+        }
+        // ---- phase 2b: coalesced emission of the staged items
+        const uint32_t cnt = r1 > r0 ? r1 - r0 : 0;
+        uint32_t* dst = out + (uint32_t)s_prefix + r0;
+#pragma unroll 4
+        for (uint32_t k = tid; k < cnt; k += kHopThreads) {
+            uint32_t u = __ldg(p.ci + s_items[k]);
+            dst[k] = u;
+            if (bm) mark_visited(bm, u);
+        }
+        __syncthreads();
+    }
+}
+
+static unsigned tiles_for(uint32_t max_frontier) {
+    unsigned t = (max_frontier + kTilePos - 1) / kTilePos;
+    return t ? t : 1u;
+}
+
+}  // namespace gc
+
+using namespace gc;
+
+extern "C" {
+
+size_t gc_hop_expand_temp_bytes(uint32_t num_batches, uint32_t max_frontier) {
+    return align_up((size_t)num_batches * tiles_for(max_frontier) * sizeof(uint64_t), 256) + 256;
+}
+
+int gc_hop_expand(const gc_csr_t* graph, const uint32_t* d_frontier, uint64_t frontier_stride,
+                  const uint32_t* d_frontier_count, uint32_t max_frontier, uint32_t fanout,
+                  const uint64_t* d_hop_keys, uint32_t num_batches, uint32_t* d_out_offsets,
+                  uint64_t offsets_stride, uint32_t* d_out_nbrs, uint64_t nbrs_stride, uint32_t* d_out_count,
+                  uint32_t* d_bitmap, uint64_t bitmap_words, int mark_frontier, const gc_hotness_t* hot,
+                  void* d_temp, size_t temp_bytes, void* stream) {
+    GC_REQUIRE(graph && graph->row_offsets, GC_ERR_VALUE, "gc_hop_expand: graph is null");
+    GC_REQUIRE(fanout >= 1, GC_ERR_VALUE, "fanouts must all be >= 1");
+    GC_REQUIRE((uint64_t)max_frontier * fanout < (1ull << 32), GC_ERR_VALUE,
+               "gc_hop_expand: max_frontier * fanout must be < 2^32 per batch");
+    GC_REQUIRE(offsets_stride >= (uint64_t)max_frontier + 1, GC_ERR_VALUE, "gc_hop_expand: offsets stride too small");
+    GC_REQUIRE(graph->num_edges == 0 || graph->col_indices, GC_ERR_VALUE, "gc_hop_expand: graph has no columns");
+    if (num_batches == 0) return GC_OK;
+    const size_t need = gc_hop_expand_temp_bytes(num_batches, max_frontier);
+    GC_REQUIRE(d_temp && temp_bytes >= need, GC_ERR_VALUE, "gc_hop_expand: temp buffer too small");
+    cudaStream_t s = as_stream(stream);
+    const unsigned tiles = tiles_for(max_frontier);
+    HopParams p{};
+    p.ro = graph->row_offsets;
+    p.ci = graph->col_indices;
+    p.n = (uint64_t)graph->num_vertices;
+    p.frontier = d_frontier;
+    p.fstride = frontier_stride;
+    p.fcount = d_frontier_count;
+    p.fanout = fanout;
+    p.tiles_per_batch = tiles;
+    p.hop_keys = d_hop_keys;
+    p.out_off = d_out_offsets;
+    p.ostride = offsets_stride;
+    p.out_nbrs = d_out_nbrs;
+    p.nstride = nbrs_stride;
+    p.out_count = d_out_count;
+    p.bitmap = d_bitmap;
+    p.bwords = bitmap_words;
+    p.mark_frontier = mark_frontier;
+    if (hot) {
+        p.topo_reads = hot->topo_reads;
+        p.edge_trav = hot->edge_traversals;
+        p.txn_total = hot->txn_total;
+        p.cls = hot->cache_line_bytes ? hot->cache_line_bytes : 64;
+        p.u32b = hot->uint32_bytes ? hot->uint32_bytes : 4;
+    }
+    const size_t state_bytes = align_up((size_t)num_batches * tiles * sizeof(uint64_t), 256);
+    p.tile_state = static_cast<uint64_t*>(d_temp);
+    p.tile_counter = reinterpret_cast<uint32_t*>(static_cast<char*>(d_temp) + state_bytes);
+    GC_TRY(cudaMemsetAsync(d_temp, 0, state_bytes + 256, s), "gc_hop_expand memset");
+    const uint64_t grid = (uint64_t)num_batches * tiles;
+    GC_REQUIRE(grid < (1ull << 31), GC_ERR_VALUE, "gc_hop_expand: window too large");
+    k_hop_expand<<<(unsigned)grid, kHopThreads, 0, s>>>(p);
+    GC_CHECK_LAUNCH("gc_hop_expand");
+    return GC_OK;
+}
+
+}  // extern "C"
