@@ -1,0 +1,160 @@
+"""Per-GPU epoch pipeline: local shuffle -> windows of sampled, deduplicated,
+relabelled and gathered mini-batches, all on the device.
+
+This is Legion's batch generator + neighbour sampler + feature extractor for one
+GPU over the reference's exact streams: the shuffle key is
+root.derive(epoch, clique, gpu).derive(ROLE_SHUFFLE) and batch b's hop h key is
+root.derive(epoch, clique, gpu).derive(ROLE_SAMPLE, b).derive(h)
+(sampling.py:215-234). Host work per epoch is the key table (vectorised numpy)
+and the launch sequence; no host round trip happens inside an epoch.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .cache import FeatureStore
+from .graph import CsrGraph
+from .rng import ROLE_SHUFFLE, KeyedRng
+from .sampling import DeviceHotness, SamplingConfig, WindowSampler, batch_hop_keys
+
+# kernels each stage launches (for the bench's gpu_launches count): CUB's onesweep
+# radix sort of 64-bit keys is 1 histogram + 8 digit passes
+LAUNCHES_PERMUTATION = 2 + 9
+
+
+@dataclass
+class EpochPlan:
+    pool: torch.Tensor  # int64 [L] device
+    shuffle_key: int
+    keys: torch.Tensor  # int64 [nb, H] device (uint64 bit patterns)
+    counts: torch.Tensor  # int32 [nb] device
+    num_batches: int
+
+
+class StageTimer:
+    """CUDA events around each stage on the launching stream."""
+
+    def __init__(self):
+        self.events: dict[str, list] = {}
+
+    def start(self, name: str):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        self.events.setdefault(name, []).append((e0, e1))
+        return e1
+
+    def summary(self) -> dict[str, tuple[int, float]]:
+        """name -> (launch count, total ms); call after synchronising."""
+        return {k: (len(v), sum(a.elapsed_time(b) for a, b in v)) for k, v in self.events.items()}
+
+    def reset(self):
+        self.events.clear()
+
+
+class SampleGatherPipeline:
+    """Sampling + dedup + relabel + three-tier gather for one GPU's seed pool."""
+
+    def __init__(self, graph: CsrGraph, cfg: SamplingConfig, store: FeatureStore | None, max_pool: int,
+                 window: int | None = None, relabel: bool = True, feat_rows_cap: int | None = None,
+                 placement: str = "hbm"):
+        self.graph = graph
+        self.cfg = cfg
+        self.store = store
+        B = cfg.batch_size
+        nb = max(1, math.ceil(max_pool / B))
+        self.window = min(nb, window or nb)
+        self.sampler = WindowSampler(graph, cfg.fanouts, B, self.window, placement=placement, relabel=relabel,
+                                     unique_cap=feat_rows_cap)
+        self.feat_cap = self.sampler.ucap
+        self.features = None
+        if store is not None:
+            self.features = torch.empty((self.window, self.feat_cap, store.spec.dimension), dtype=torch.float32,
+                                        device="cuda")
+        self.timer: StageTimer | None = None
+        self.launches = 0
+
+    # ------------------------------------------------------------------ host prep
+    def plan_epoch(self, pool, gpu_stream: KeyedRng) -> EpochPlan:
+        B = self.cfg.batch_size
+        pool_dev = pool if isinstance(pool, torch.Tensor) else torch.from_numpy(np.asarray(pool, np.int64)).cuda()
+        L = pool_dev.numel()
+        nb = math.ceil(L / B)
+        keys = batch_hop_keys(gpu_stream, 0, nb, len(self.cfg.fanouts))
+        counts = np.full(nb, B, dtype=np.int32)
+        if nb:
+            counts[-1] = L - (nb - 1) * B
+        return EpochPlan(
+            pool_dev,
+            gpu_stream.derive(ROLE_SHUFFLE).key,
+            torch.from_numpy(keys.view(np.int64)).cuda(),
+            torch.from_numpy(counts).cuda(),
+            nb,
+        )
+
+    # ------------------------------------------------------------------ device epoch
+    def _stage(self, name):
+        return self.timer.start(name) if self.timer is not None else None
+
+    def run_epoch(self, plan: EpochPlan, on_window=None, hot: DeviceHotness | None = None) -> None:
+        """Shuffle + all windows of one epoch; on_window(pipeline, first_batch, nbatches)
+        is called after each window's device work has been enqueued."""
+        sp = self.sampler
+        B, H = self.cfg.batch_size, len(self.cfg.fanouts)
+        end = self._stage("shuffle")
+        shuffled = KeyedRng(plan.shuffle_key).permutation_device(plan.pool.numel(), plan.pool)
+        self.launches += LAUNCHES_PERMUTATION
+        if end is not None:
+            end.record()
+        for w0 in range(0, plan.num_batches, self.window):
+            w1 = min(plan.num_batches, w0 + self.window)
+            nb = w1 - w0
+            lo, hi = w0 * B, min(plan.pool.numel(), w1 * B)
+            sp.active = nb
+            sp.seeds.view(-1)[: hi - lo].copy_(shuffled[lo:hi])
+            sp.counts[0, :nb].copy_(plan.counts[w0:w1])
+            if H:
+                sp.keys[:, :nb].copy_(plan.keys[w0:w1].t())
+            end = self._stage("hop_expand")
+            sp.expand(hot)
+            self.launches += max(H, 1)
+            if end is not None:
+                end.record()
+            end = self._stage("unique_relabel")
+            sp.dedup(hot, keep_bitmap=self.store is not None and not sp.relabel)
+            self.launches += 1 + (H + 1 if sp.relabel else 0)
+            if end is not None:
+                end.record()
+            if self.store is not None:
+                end = self._stage("gather")
+                self.store.gather(sp.unique, sp.ucount, self.features, num_batches=nb)
+                self.launches += 1
+                if end is not None:
+                    end.record()
+            if sp.relabel or self.store is not None:
+                sp.release_bitmap()
+                self.launches += 1
+            if on_window is not None:
+                on_window(self, w0, nb)
+
+    # ------------------------------------------------------------------ accounting
+    def window_bytes(self, nb: int) -> dict[str, int]:
+        """Algorithmic bytes of the last window, by stage: needs a sync."""
+        sp = self.sampler
+        counts = sp.counts[:, :nb].cpu().numpy().astype(np.int64)  # [H+1, nb]
+        ucount = sp.ucount[:nb].cpu().numpy().astype(np.int64)
+        F = counts[:-1].sum(axis=1)  # per hop frontier positions
+        T = counts[1:].sum(axis=1)  # per hop sampled neighbours
+        sampling = int((4 * F + 16 * F + 4 * T + 4 * T + 4 * (F + nb)).sum())
+        ids = int(counts.sum())
+        dedup = 4 * int(ucount.sum()) + (8 * ids if sp.relabel else 0)
+        row = self.store.spec.row_bytes if self.store is not None else 0
+        gather = 2 * row * int(ucount.sum())
+        return {"sampling": sampling, "dedup": dedup, "gather": gather, "unique_rows": int(ucount.sum()),
+                "sampled": int(T.sum())}
