@@ -1,0 +1,446 @@
+"""Benchmark: sampled+gathered mini-batches/s of Legion's data-preparation path on B200.
+
+Workload (BASELINE.json configs[1], the metric's single-GPU config): ogbn-products-shaped
+synthetic graph — 2.4M vertices, constant out-degree 26 (62.4M edges), Zipf skew 1.2,
+100-d fp32 features fully HBM-resident — GraphSAGE 3-hop fanouts [15,10,5], batch 1024,
+10% training set split into per-GPU tablets. One step = one epoch of the rank's tablet:
+local shuffle (K1), then for every batch 3-hop sampling (K2), dedup + relabel (K3) and
+feature gather (K4), all on the device, with the reference's exact RNG streams.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...        (one process per GPU)
+
+Prints one JSON line (rank 0).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "GraphSAGE epoch time, sampled+gathered batches/s at 1/2/4/8 B200; PCIe GB/batch"
+UNIT = "batches/s"
+CONFIG = {
+    "workload": "C2 ogbn-products-shaped synthetic, fully HBM-cached",
+    "num_vertices": 2_400_000,
+    "avg_degree": 26,
+    "skew": 1.2,
+    "feature_dim": 100,
+    "fanouts": [15, 10, 5],
+    "batch_size": 1024,
+    "training_fraction": 0.1,
+    "master_seed": 7,
+}
+HBM_FALLBACK_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--window", type=int, default=0, help="batches per launch window (0 = whole epoch)")
+    ap.add_argument("--num-vertices", type=int, default=CONFIG["num_vertices"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+def build_inputs(n: int, world: int):
+    from paper_2305_16588_b200 import derive_seed, generate_synthetic, select_training_set
+    from paper_2305_16588_b200.hardware import block_layout
+    from paper_2305_16588_b200.partition import assign_tablets, single_clique_partitioning, split_intra_clique
+
+    seed = CONFIG["master_seed"]
+    g = generate_synthetic(n, CONFIG["avg_degree"], CONFIG["skew"], seed=derive_seed(seed, 1))
+    train = select_training_set(g, CONFIG["training_fraction"], seed=derive_seed(seed, 2))
+    layout = block_layout(world, world)
+    pools = assign_tablets(split_intra_clique(train, single_clique_partitioning(g), layout), layout)
+    return g, pools, layout
+
+
+def peak_hbm():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return HBM_FALLBACK_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = Path(f"/tmp/gc_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if self.proc is None or not self.path.exists():
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.path.read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[2:]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        self.path.unlink(missing_ok=True)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU baseline (oracle port)
+def cpu_batches(g, table, pool, nbatches, seconds, epoch=0):
+    """Time the oracle restatement of the reference path (sample_batch + np.unique +
+    X[ids]) on one host core for about `seconds`; returns (batches, elapsed)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import gnncache_oracle as O
+
+    B, fan = CONFIG["batch_size"], CONFIG["fanouts"]
+    gkey, skey = O.batch_stream_keys(O.derive(CONFIG["master_seed"], 0x10), epoch, 0, 0)
+    shuffled = np.asarray(pool)[O.permutation(skey, len(pool))]
+    t0 = time.perf_counter()
+    done = 0
+    for b in range(nbatches):
+        seeds = shuffled[b * B : (b + 1) * B]
+        hops = O.sample_batch(g.row_offsets, g.col_indices, g.num_vertices, seeds, fan, O.derive(gkey, 2, b))
+        uniq = O.distinct_vertices(seeds, hops)
+        O.gather(table, uniq)
+        done += 1
+        if time.perf_counter() - t0 > seconds:
+            break
+    return done, time.perf_counter() - t0
+
+
+def _ref_worker(args):
+    b0, count, epoch = args
+    g, table, pool = _REF_STATE
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import gnncache_oracle as O
+
+    B, fan = CONFIG["batch_size"], CONFIG["fanouts"]
+    gkey, skey = O.batch_stream_keys(O.derive(CONFIG["master_seed"], 0x10), epoch, 0, 0)
+    shuffled = np.asarray(pool)[O.permutation(skey, len(pool))]
+    for b in range(b0, b0 + count):
+        seeds = shuffled[(b * B) % len(pool) :][:B]
+        hops = O.sample_batch(g.row_offsets, g.col_indices, g.num_vertices, seeds, fan, O.derive(gkey, 2, b))
+        O.gather(table, O.distinct_vertices(seeds, hops))
+    return count
+
+
+_REF_STATE = None
+
+
+def host_table(n, dim):
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import gnncache_oracle as O
+
+    out = np.empty((n, dim), dtype=np.float32)
+    step = 1 << 18
+    for s in range(0, n, step):
+        out[s : s + step] = O.synthetic_features(np.arange(s, min(n, s + step)), dim)
+    return out
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU path (oracle port; the reference itself is
+    pure Python/numpy and is not installed on the box) on all host cores."""
+    global _REF_STATE
+    import multiprocessing as mp
+
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    g, pools, _ = build_inputs(args.num_vertices, 1)
+    table = host_table(g.num_vertices, CONFIG["feature_dim"])
+    _REF_STATE = (g, table, pools[0])
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    nb_epoch = math.ceil(len(pools[0]) / CONFIG["batch_size"])
+    per_step = cores  # one batch per worker per step
+    ctx = mp.get_context("fork")
+    times = []
+    with ctx.Pool(cores) as pool:
+        b = 0
+        for it in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            pool.map(_ref_worker, [((b + i) % nb_epoch, 1, 0) for i in range(per_step)])
+            dt = time.perf_counter() - t0
+            b += per_step
+            if it >= args.warmup:
+                times.append(dt)
+    total = sum(times)
+    value = per_step * len(times) / total
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * total / len(times), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u64", "data": "synthetic (reference generator law, PCG64 draws)", "impl": "reference",
+        "config": {**CONFIG, "num_vertices": args.num_vertices, "parallelism": "host processes"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{per_step} batches per step (one per process) of the epoch, "
+                                   "sample_batch + np.unique + X[ids] per batch"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ B200 arm
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2305_16588_b200 import KeyedRng, SamplingConfig, derive_seed
+    from paper_2305_16588_b200.cache import FeatureStore
+    from paper_2305_16588_b200.graph import synthetic_features_device
+    from paper_2305_16588_b200.pipeline import SampleGatherPipeline, StageTimer
+
+    rank, local, world = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    g, pools, layout = build_inputs(args.num_vertices, world)
+    pool = pools[rank]
+    cfg = SamplingConfig(fanouts=tuple(CONFIG["fanouts"]), batch_size=CONFIG["batch_size"],
+                         seed=derive_seed(CONFIG["master_seed"], 0x10))
+    dim = CONFIG["feature_dim"]
+    table = synthetic_features_device(0, g.num_vertices, dim)  # fully HBM-resident feature table
+    store = FeatureStore.resident(table)
+    nb = math.ceil(len(pool) / cfg.batch_size)
+    window = args.window or nb
+    # per-batch distinct rows stay far below the 938K worst case; 64K keeps the
+    # window's gather buffer small, and the run checks it never overflowed
+    pipe = SampleGatherPipeline(g, cfg, store, len(pool), window=window, feat_rows_cap=65536)
+    root = KeyedRng(cfg.seed)
+    clique, local_idx = layout.gpu_position(rank)
+    plans = [pipe.plan_epoch(pool, root.derive(e, clique, local_idx)) for e in range(args.warmup + args.steps)]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    stats = {"bytes": {"sampling": 0, "dedup": 0, "gather": 0}, "unique_rows": 0, "sampled": 0, "max_unique": 0}
+
+    def account(p, w0, nbw):
+        b = p.window_bytes(nbw)
+        for k in ("sampling", "dedup", "gather"):
+            stats["bytes"][k] += b[k]
+        stats["unique_rows"] += b["unique_rows"]
+        stats["sampled"] += b["sampled"]
+        stats["max_unique"] = max(stats["max_unique"], int(p.sampler.ucount[:nbw].max().item()))
+
+    for e in range(args.warmup):
+        pipe.run_epoch(plans[e])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    timer = StageTimer()
+    pipe.timer = timer
+    pipe.launches = 0
+    step_ms = []
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        for s in range(args.steps):
+            flush.zero_()  # L2 flush outside the timed events
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            pipe.run_epoch(plans[args.warmup + s])
+            e1.record()
+            torch.cuda.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+        if world > 1:
+            dist.barrier()
+    launches = pipe.launches
+    pipe.timer = None
+    # algorithmic bytes of the timed epochs (recomputed, identical streams: untimed)
+    for s in range(args.steps):
+        pipe.run_epoch(plans[args.warmup + s], on_window=account)
+    torch.cuda.synchronize()
+    if stats["max_unique"] > pipe.feat_cap:
+        raise RuntimeError("gather capacity overflow: raise feat_rows_cap")
+
+    total_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        nbt = torch.tensor([nb], dtype=torch.int64, device="cuda")
+        dist.all_reduce(nbt)
+        batches_all = int(nbt.item()) * args.steps
+    else:
+        batches_all = nb * args.steps
+    value = batches_all / (total_ms / 1000.0)
+
+    stage = timer.summary()
+    peak, peak_kind = peak_hbm()
+    stage_bytes = {"hop_expand": stats["bytes"]["sampling"], "unique_relabel": stats["bytes"]["dedup"],
+                   "gather": stats["bytes"]["gather"]}
+    dom = max((k for k in stage if k in stage_bytes), key=lambda k: stage[k][1])
+    dom_launches, dom_ms = stage[dom]
+    achieved = stage_bytes[dom] / (dom_ms / 1000.0) / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / "ncu_traffic.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get(dom)
+        except Exception:
+            traffic = None
+    step_bytes = sum(stats["bytes"].values())
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u64", "data": "synthetic (reference generator law, PCG64 draws; random fp32 features)",
+        "config": {**CONFIG, "num_vertices": args.num_vertices, "batches_per_step_per_gpu": nb,
+                   "window_batches": pipe.window, "parallelism": f"dp{world} (tablet per GPU, no data-path collective)",
+                   "l2": "flushed (256 MB write) between timed steps; graph+features 1.2 GB > L2"},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "launches": dom_launches, "avg_launch_ms": dom_ms / max(dom_launches, 1),
+                     "bytes_per_launch": stage_bytes[dom] / max(dom_launches, 1)},
+        "step_roofline": {"bytes_per_batch": step_bytes / (nb * args.steps),
+                          "t_roof_us_per_batch": step_bytes / (nb * args.steps) / (peak * 1e9) * 1e6,
+                          "measured_us_per_batch": total_ms * 1000 / (nb * args.steps),
+                          "frac": (step_bytes / (peak * 1e9)) / (total_ms / 1000.0)},
+        "stages_ms": {k: v[1] / args.steps for k, v in stage.items()},
+        "pcie_gb_per_batch": 0.0,
+        "sampled_per_batch": stats["sampled"] / (nb * args.steps),
+        "unique_rows_per_batch": stats["unique_rows"] / (nb * args.steps),
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+    }
+
+    if not args.no_e2e:
+        line["e2e"] = e2e_run(args, g, cfg, store, pool, root, clique, local_idx, world)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        host = table.cpu().numpy()
+        done, el = cpu_batches(g, host, pool, nb, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": done / el, "unit": UNIT, "cores": 1, "kind": "port",
+                                "sample": f"first {done} batches of epoch 0 (C2, 1 core): oracle sample_batch + "
+                                          "np.unique + X[ids]"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_run(args, g, cfg, store, pool, root, clique, local_idx, world):
+    """Same metric through the public pipeline API with host buffers: the tablet goes
+    host->device from pinned memory each step, and every batch's result (distinct
+    ids, gathered rows, relabelled hop ids and offsets) comes back to pinned host."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2305_16588_b200.pipeline import SampleGatherPipeline
+
+    nb = math.ceil(len(pool) / cfg.batch_size)
+    pipe = SampleGatherPipeline(g, cfg, store, len(pool), window=args.window or nb, feat_rows_cap=65536)
+    host_pool = torch.from_numpy(np.asarray(pool, dtype=np.int64)).pin_memory()
+    sp = pipe.sampler
+    H = len(cfg.fanouts)
+    pinned = {
+        "feat": torch.empty(pipe.features.shape, dtype=torch.float32).pin_memory(),
+        "uniq": torch.empty(sp.unique.shape, dtype=torch.int32).pin_memory(),
+        "local": [torch.empty(t.shape, dtype=torch.int32).pin_memory() for t in sp.local_nbrs],
+        "offs": [torch.empty(t.shape, dtype=torch.int32).pin_memory() for t in sp.offsets],
+    }
+    moved = {"h2d": 0, "d2h": 0}
+
+    def drain(p, w0, nbw):
+        counts = sp.counts[:, :nbw].cpu()  # sync point: sizes of this window
+        ucnt = sp.ucount[:nbw].cpu()
+        for b in range(nbw):
+            u = int(ucnt[b])
+            pinned["feat"][b, :u].copy_(pipe.features[b, :u], non_blocking=True)
+            pinned["uniq"][b, :u].copy_(sp.unique[b, :u], non_blocking=True)
+            moved["d2h"] += u * (store.spec.row_bytes + 4)
+            for h in range(H):
+                f, t = int(counts[h, b]), int(counts[h + 1, b])
+                pinned["offs"][h][b, : f + 1].copy_(sp.offsets[h][b, : f + 1], non_blocking=True)
+                pinned["local"][h][b, :t].copy_(sp.local_nbrs[h][b, :t], non_blocking=True)
+                moved["d2h"] += 4 * (f + 1 + t)
+        torch.cuda.current_stream().synchronize()
+
+    def step(e):
+        dev_pool = host_pool.to("cuda", non_blocking=True)
+        moved["h2d"] += host_pool.numel() * 8
+        plan = pipe.plan_epoch(dev_pool, root.derive(e, clique, local_idx))
+        moved["h2d"] += plan.keys.numel() * 8 + plan.counts.numel() * 4
+        pipe.run_epoch(plan, on_window=drain)
+
+    steps = max(1, min(args.steps, 3))
+    for e in range(min(args.warmup, 2)):
+        step(e)
+    torch.cuda.synchronize()
+    moved = {"h2d": 0, "d2h": 0}
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for s in range(steps):
+        step(100 + s)
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([el], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t.item())
+    return {"value": nb * world * steps / el, "unit": UNIT, "h2d_bytes_per_step": moved["h2d"] // steps,
+            "d2h_bytes_per_step": moved["d2h"] // steps, "steps": steps,
+            "api": "SampleGatherPipeline.plan_epoch/run_epoch (ctypes -> libgnncache_b200.so)"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()
