@@ -46,6 +46,11 @@ extern "C" {
 #define GC_TIER_HOST 0xFFFFFFFFu /* location-table value for host-resident rows */
 
 int gc_abi_version(void);
+/* Process-wide options. GC_OPT_EXACT_SELECTION=1 makes hop expansion skip the packed
+ * 32-bit REDUX extraction and always use the 64-bit path (a test hook: both paths
+ * must give identical output). */
+#define GC_OPT_EXACT_SELECTION 1
+int gc_set_option(int option, int value);
 const char* gc_last_error(void);
 /* device ordinal of the calling thread's current device; -1 if none */
 int gc_current_device(void);

@@ -23,6 +23,7 @@ GC_ERR_CUDA = -3
 GC_ERR_UNSUPPORTED = -4
 GC_ERR_ASSERT = -5
 GC_MAX_PEERS = 8
+GC_OPT_EXACT_SELECTION = 1
 GC_TIER_HOST = 0xFFFFFFFF
 
 _c_u64p = ctypes.c_void_p  # every device pointer crosses as an opaque address
@@ -73,6 +74,7 @@ SIGNATURES = {
     "gc_abi_version": (ctypes.c_int, []),
     "gc_last_error": (ctypes.c_char_p, []),
     "gc_current_device": (ctypes.c_int, []),
+    "gc_set_option": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
     "gc_mix64": (ctypes.c_int, [V, V, I64, V]),
     "gc_hash_counters": (ctypes.c_int, [U64, V, V, I64, V]),
     "gc_hash_pairs": (ctypes.c_int, [U64, V, V, V, I64, V]),

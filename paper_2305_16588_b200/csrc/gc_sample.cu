@@ -34,6 +34,7 @@ struct HopParams {
     const uint32_t* fcount;
     uint32_t fanout;
     uint32_t tiles_per_batch;
+    uint32_t tile_pos;
     const uint64_t* hop_keys;
     uint32_t* out_off;
     uint64_t ostride;
@@ -50,7 +51,10 @@ struct HopParams {
     uint32_t u32b;
     uint64_t* tile_state;
     uint32_t* tile_counter;
+    int exact_only;  // test hook: always take the 64-bit extraction path
 };
+
+static int g_exact_only = 0;
 
 __device__ __forceinline__ void mark_visited(uint32_t* bm, uint32_t u) {
     uint32_t* w = bm + (u >> 5);
@@ -90,39 +94,111 @@ __device__ __forceinline__ void select_registers(uint64_t hc, uint32_t deg, uint
                                                  uint32_t excl, uint32_t r0, uint32_t r1, uint64_t* s_items) {
     const int lane = threadIdx.x & 31;
     uint64_t key[R];
+    uint32_t rank[R];
     unsigned live = 0;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        uint32_t j = lane + 32 * r;
+        const uint32_t j = lane + 32 * r;
         key[r] = hash_pair(hc, j);
+        rank[r] = 0xFFFFFFFFu;
         if (j < deg) live |= 1u << r;
     }
-    // extraction beyond the staged window is not needed
-    uint32_t stop = min(fanout, r1 - excl);
-    for (uint32_t it = 0; it < stop; ++it) {
-        uint64_t lm = ~0ull;
-        int lr = -1;
+    // lane-local minimum among live candidates (j ascending with r: strict < keeps the
+    // smaller edge index on equal keys)
+    auto local_min = [&](uint64_t& lm, int& lr) {
+        lm = ~0ull;
+        lr = -1;
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
+        for (int r = 0; r < R; ++r)
             if (((live >> r) & 1u) && (lr < 0 || key[r] < lm)) {
                 lm = key[r];
                 lr = r;
             }
+    };
+    uint64_t lm;
+    int lr;
+    local_min(lm, lr);
+    // extraction beyond the staged window is not needed
+    const uint32_t stop = min(fanout, r1 - excl);
+    for (uint32_t it = 0; it < stop; ++it) {
+        const uint32_t hi = lr >= 0 ? (uint32_t)(lm >> 32) : 0xFFFFFFFFu;
+        const uint32_t m = __reduce_min_sync(kFull, hi);
+        bool win = lr >= 0 && hi == m;
+        const unsigned cand = __ballot_sync(kFull, win);
+        if (cand & (cand - 1u)) {
+            // several lanes share the high word: exact (lo32, j) order decides (rare)
+            const uint32_t wj = tie_break(cand, lm, lane + 32u * (uint32_t)(lr < 0 ? 0 : lr));
+            win = (wj & 31u) == (uint32_t)lane;
         }
-        uint32_t hi = lr >= 0 ? (uint32_t)(lm >> 32) : 0xFFFFFFFFu;
-        uint32_t m = __reduce_min_sync(kFull, hi);
-        unsigned cand = __ballot_sync(kFull, lr >= 0 && hi == m);
-        int w;
-        if (__popc(cand) == 1) {
-            w = __ffs(cand) - 1;
-        } else {
-            w = (int)(tie_break(cand, lm, lane + 32u * (uint32_t)(lr < 0 ? 0 : lr)) & 31u);
-        }
-        if (lane == w) {
-            stage(s_items, excl + it, r0, r1, o0 + (uint64_t)(lane + 32 * lr));
+        if (win) {
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (r == lr) rank[r] = it;
             live &= ~(1u << lr);
+            if (R == 1)
+                lr = -1;
+            else
+                local_min(lm, lr);
         }
     }
+    // each lane stages its own winners: item excl + rank <- edge o0 + j
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+        if (rank[r] != 0xFFFFFFFFu) stage(s_items, excl + rank[r], r0, r1, o0 + (uint64_t)(lane + 32 * r));
+}
+
+// Fast choice path: candidate j of lane l is j = l + 32 r (r < R). Each key is
+// packed into 32 bits as (top 32-IB bits of the 64-bit key) << IB | j, which makes
+// every packed value unique, so one REDUX.MIN per extraction names the winner with
+// no ballot. The packed order equals the exact (key, j) order unless two
+// candidates share the packed prefix; such a prefix tie shows up as two equal
+// prefixes among consecutively extracted values (one extra extraction covers the
+// selection boundary), in which case this returns false and the caller reruns the
+// exact 64-bit path. Ties need two of <=128 uniform keys to agree in 25-27 bits.
+template <int R>
+__device__ __forceinline__ bool select_packed(uint64_t hc, uint32_t deg, uint32_t fanout, uint64_t o0, uint32_t excl,
+                                              uint32_t r0, uint32_t r1, uint64_t* s_items) {
+    constexpr int IB = R == 1 ? 5 : (R == 2 ? 6 : 7);
+    constexpr uint32_t kIdx = (1u << IB) - 1u;
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t pk[R];
+    uint32_t rank[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const uint32_t j = lane + 32u * r;
+        const uint64_t key = hash_pair(hc, j);
+        pk[r] = j < deg ? ((uint32_t)(key >> (32 + IB)) << IB) | j : 0xFFFFFFFFu;
+        rank[r] = 0xFFFFFFFFu;
+    }
+    uint32_t lmin = pk[0];
+#pragma unroll
+    for (int r = 1; r < R; ++r) lmin = min(lmin, pk[r]);
+    const uint32_t stop = min(fanout, r1 - excl);  // stop < deg here
+    uint32_t prev = 0xFFFFFFFFu;
+    bool tie = false;
+    for (uint32_t it = 0; it <= stop; ++it) {
+        const uint32_t m = __reduce_min_sync(kFull, lmin);
+        const uint32_t hi = m >> IB;
+        tie |= (it != 0) & (hi == prev);
+        prev = hi;
+        if (it < stop && lane == (m & 31u)) {
+            const uint32_t wr = (m & kIdx) >> 5;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (r == (int)wr) {
+                    rank[r] = it;
+                    pk[r] = 0xFFFFFFFFu;
+                }
+            lmin = pk[0];
+#pragma unroll
+            for (int r = 1; r < R; ++r) lmin = min(lmin, pk[r]);
+        }
+    }
+    if (tie) return false;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+        if (rank[r] != 0xFFFFFFFFu) stage(s_items, excl + rank[r], r0, r1, o0 + (uint64_t)(lane + 32u * r));
+    return true;
 }
 
 // Choice path for long adjacency lists: keys are recomputed each extraction step
@@ -162,6 +238,59 @@ __device__ void select_streaming(uint64_t hc, uint32_t deg, uint32_t fanout, uin
     }
 }
 
+// Thread-per-position choice path for deg <= 64 and fanout < S: the thread streams
+// its deg keys through a branchless S-slot min/max insertion network on packed
+// 32-bit values (26-bit key prefix << 6 | j), which keeps the S smallest in order.
+// Two equal prefixes among ranks 0..fanout mean the packed order may differ from
+// the exact (key, j) order: return false and let a warp redo the position exactly.
+template <int S>
+__device__ __forceinline__ bool select_thread(uint64_t hc, uint32_t deg, uint32_t fanout, uint64_t o0, uint32_t excl,
+                                              uint32_t r0, uint32_t r1, uint64_t* s_items) {
+    constexpr int IB = 6;
+    uint32_t t[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) t[s] = 0xFFFFFFFFu;
+    for (uint32_t j = 0; j < deg; ++j) {
+        const uint32_t x = ((uint32_t)(hash_pair(hc, j) >> (32 + IB)) << IB) | j;
+#pragma unroll
+        for (int s = S - 1; s >= 1; --s) t[s] = max(t[s - 1], min(t[s], x));
+        t[0] = min(t[0], x);
+    }
+    bool tie = false;
+#pragma unroll
+    for (int s = 0; s + 1 < S; ++s) tie |= (s < (int)fanout) & ((t[s] >> IB) == (t[s + 1] >> IB));
+    if (tie) return false;
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+        if (s < (int)fanout) stage(s_items, excl + s, r0, r1, o0 + (t[s] & ((1u << IB) - 1u)));
+    return true;
+}
+
+// Warp-cooperative selection of one position (long lists, wide fanouts, tie redo).
+__device__ __forceinline__ void select_warp(uint64_t hc, uint32_t d, uint32_t fanout, uint64_t base, uint32_t e0,
+                                            uint32_t r0, uint32_t r1, uint64_t* s_items, bool exact) {
+    if (exact && d <= 128) {
+        if (d <= 32)
+            select_registers<1>(hc, d, fanout, base, e0, r0, r1, s_items);
+        else if (d <= 64)
+            select_registers<2>(hc, d, fanout, base, e0, r0, r1, s_items);
+        else
+            select_registers<4>(hc, d, fanout, base, e0, r0, r1, s_items);
+    } else if (d <= 32) {
+        if (!select_packed<1>(hc, d, fanout, base, e0, r0, r1, s_items))
+            select_registers<1>(hc, d, fanout, base, e0, r0, r1, s_items);
+    } else if (d <= 64) {
+        if (!select_packed<2>(hc, d, fanout, base, e0, r0, r1, s_items))
+            select_registers<2>(hc, d, fanout, base, e0, r0, r1, s_items);
+    } else if (d <= 128) {
+        if (!select_packed<4>(hc, d, fanout, base, e0, r0, r1, s_items))
+            select_registers<4>(hc, d, fanout, base, e0, r0, r1, s_items);
+    } else {
+        select_streaming(hc, d, fanout, base, e0, r0, r1, s_items);
+    }
+}
+
+template <int S>
 __global__ void __launch_bounds__(kHopThreads) k_hop_expand(HopParams p) {
     using Scan = cub::BlockScan<uint32_t, kHopThreads>;
     using Reduce = cub::BlockReduce<uint64_t, kHopThreads>;
@@ -169,30 +298,26 @@ __global__ void __launch_bounds__(kHopThreads) k_hop_expand(HopParams p) {
         typename Scan::TempStorage scan;
         typename Reduce::TempStorage reduce;
     } tmp;
-    __shared__ uint64_t s_off0[kTilePos];
-    __shared__ uint32_t s_deg[kTilePos];
-    __shared__ uint32_t s_excl[kTilePos + 1];
     __shared__ uint64_t s_items[kItemCap];
     __shared__ uint32_t s_vid;
     __shared__ uint64_t s_prefix;
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
-    const int warp = tid >> 5;
     if (tid == 0) s_vid = atomicAdd(p.tile_counter, 1u);
     __syncthreads();
     const uint32_t vid = s_vid;
     const uint32_t b = vid / p.tiles_per_batch;
     const uint32_t t = vid % p.tiles_per_batch;
     const uint32_t F = p.fcount[b];
-    const uint64_t p0 = (uint64_t)t * kTilePos;
+    const uint64_t p0 = (uint64_t)t * p.tile_pos;
     if (p0 >= F && t != 0) return;  // past the end of this batch's frontier: no successor needs it
-    const uint32_t npos = p0 < F ? (uint32_t)((F - p0) < (uint64_t)kTilePos ? (F - p0) : (uint64_t)kTilePos) : 0u;
+    const uint32_t npos = p0 < F ? (uint32_t)((F - p0) < (uint64_t)p.tile_pos ? (F - p0) : (uint64_t)p.tile_pos) : 0u;
 
-    // ---- phase 1: per-position degree and take
+    // ---- phase 1: thread-per-position degree, take and position hash
     const bool valid = tid < (int)npos;
     uint32_t v = 0, deg = 0, take = 0;
-    uint64_t o0 = 0;
+    uint64_t o0 = 0, hc = 0;
     if (valid) {
         v = p.frontier[b * p.fstride + p0 + tid];
         if (v < p.n) {
@@ -201,9 +326,9 @@ __global__ void __launch_bounds__(kHopThreads) k_hop_expand(HopParams p) {
         }
         take = min(deg, p.fanout);
         if (p.mark_frontier && p.bitmap) mark_visited(p.bitmap + b * p.bwords, v);
+        // hash_counters(position), position = index in this batch's frontier (rng.py:64-66)
+        if (deg > p.fanout) hc = hash_counter(p.hop_keys[b], p0 + tid);
     }
-    s_off0[tid] = o0;
-    s_deg[tid] = deg;
     if (p.topo_reads || p.edge_trav) {
         unsigned act = __ballot_sync(kFull, valid);
         if (valid) {
@@ -226,46 +351,47 @@ __global__ void __launch_bounds__(kHopThreads) k_hop_expand(HopParams p) {
     }
     uint32_t excl, total;
     Scan(tmp.scan).ExclusiveSum(take, excl, total);
-    s_excl[tid] = excl;
-    if (tid == 0) s_excl[kTilePos] = total;
     const uint64_t sidx = (uint64_t)b * p.tiles_per_batch + t;
     const uint64_t sfirst = (uint64_t)b * p.tiles_per_batch;
     if (tid == 0 && t != 0) publish(p.tile_state + sidx, kFlagAgg | total);
-    __syncthreads();
 
-    const uint64_t hop_key = p.hop_keys[b];
     uint32_t* out = p.out_nbrs + b * p.nstride;
     uint32_t* bm = p.bitmap ? p.bitmap + b * p.bwords : nullptr;
     const uint32_t rounds = (total + kItemCap - 1) / kItemCap;
+    const bool thread_copy = deg <= p.fanout && deg <= 64;
+    const bool thread_choice = S > 0 && !p.exact_only && deg > p.fanout && deg <= 64 && p.fanout < (uint32_t)S;
 
     for (uint32_t r = 0; r < max(rounds, 1u); ++r) {
         const uint32_t r0 = r * kItemCap;
         const uint32_t r1 = min(total, r0 + kItemCap);
-        // ---- phase 2a: stage source edge indices of items [r0, r1)
-        for (uint32_t i = warp; i < npos; i += kHopThreads / 32) {
-            const uint32_t e0 = s_excl[i];
-            const uint32_t e1 = s_excl[i + 1];
-            if (e1 <= r0 || e0 >= r1) continue;
-            const uint32_t d = s_deg[i];
-            const uint64_t base = s_off0[i];
+        // ---- phase 2a: stage the source edge index of every output item in [r0, r1)
+        bool need_warp = false;
+        if (valid && take && excl + take > r0 && excl < r1) {
+            if (thread_copy) {
+                for (uint32_t k = 0; k < deg; ++k) stage(s_items, excl + k, r0, r1, o0 + k);
+            } else if (thread_choice) {
+                need_warp = !select_thread<(S > 0 ? S : 1)>(hc, deg, p.fanout, o0, excl, r0, r1, s_items);
+            } else {
+                need_warp = true;
+            }
+        }
+        unsigned todo = __ballot_sync(kFull, need_warp);
+        while (todo) {
+            const int src = __ffs(todo) - 1;
+            todo &= todo - 1u;
+            const uint32_t d = __shfl_sync(kFull, deg, src);
+            const uint64_t base = __shfl_sync(kFull, o0, src);
+            const uint32_t e0 = __shfl_sync(kFull, excl, src);
+            const uint64_t h = __shfl_sync(kFull, hc, src);
             if (d <= p.fanout) {
                 for (uint32_t k = lane; k < d; k += 32) stage(s_items, e0 + k, r0, r1, base + k);
             } else {
-                // hash_counters(position), position = index within this batch's frontier
-                const uint64_t hc = hash_counter(hop_key, p0 + i);
-                if (d <= 32)
-                    select_registers<1>(hc, d, p.fanout, base, e0, r0, r1, s_items);
-                else if (d <= 64)
-                    select_registers<2>(hc, d, p.fanout, base, e0, r0, r1, s_items);
-                else if (d <= 128)
-                    select_registers<4>(hc, d, p.fanout, base, e0, r0, r1, s_items);
-                else
-                    select_streaming(hc, d, p.fanout, base, e0, r0, r1, s_items);
+                select_warp(h, d, p.fanout, base, e0, r0, r1, s_items, p.exact_only);
             }
         }
         if (r == 0) {
             // ---- look-back for the batch-level output prefix of this tile
-            if (warp == 0) {
+            if (tid < 32) {
                 uint64_t pre = lookback_warp(p.tile_state, sfirst, sidx, total);
                 if (lane == 0) s_prefix = pre;
             }
@@ -297,9 +423,24 @@ __global__ void __launch_bounds__(kHopThreads) k_hop_expand(HopParams p) {
     }
 }
 
-static unsigned tiles_for(uint32_t max_frontier) {
-    unsigned t = (max_frontier + kTilePos - 1) / kTilePos;
+// positions per tile: one staging round whenever fanout <= 128
+static uint32_t tile_positions(uint32_t fanout) {
+    uint32_t tp = kItemCap / (fanout ? fanout : 1);
+    tp = tp >= (uint32_t)kTilePos ? (uint32_t)kTilePos : (tp / 32) * 32;
+    return tp < 32 ? 32 : tp;
+}
+
+static unsigned tiles_for(uint32_t max_frontier, uint32_t tile_pos) {
+    unsigned t = (max_frontier + tile_pos - 1) / tile_pos;
     return t ? t : 1u;
+}
+
+// smallest insertion network holding ranks 0..fanout (0: no thread path)
+static int network_slots(uint32_t fanout) {
+    const int sizes[] = {4, 6, 8, 11, 16, 21, 26, 32};
+    for (int s : sizes)
+        if (fanout < (uint32_t)s) return s;
+    return 0;
 }
 
 }  // namespace gc
@@ -308,8 +449,14 @@ using namespace gc;
 
 extern "C" {
 
+int gc_set_option(int option, int value) {
+    GC_REQUIRE(option == GC_OPT_EXACT_SELECTION, GC_ERR_VALUE, "gc_set_option: unknown option");
+    g_exact_only = value ? 1 : 0;
+    return GC_OK;
+}
+
 size_t gc_hop_expand_temp_bytes(uint32_t num_batches, uint32_t max_frontier) {
-    return align_up((size_t)num_batches * tiles_for(max_frontier) * sizeof(uint64_t), 256) + 256;
+    return align_up((size_t)num_batches * tiles_for(max_frontier, 32) * sizeof(uint64_t), 256) + 256;
 }
 
 int gc_hop_expand(const gc_csr_t* graph, const uint32_t* d_frontier, uint64_t frontier_stride,
@@ -328,8 +475,10 @@ int gc_hop_expand(const gc_csr_t* graph, const uint32_t* d_frontier, uint64_t fr
     const size_t need = gc_hop_expand_temp_bytes(num_batches, max_frontier);
     GC_REQUIRE(d_temp && temp_bytes >= need, GC_ERR_VALUE, "gc_hop_expand: temp buffer too small");
     cudaStream_t s = as_stream(stream);
-    const unsigned tiles = tiles_for(max_frontier);
+    const uint32_t tile_pos = tile_positions(fanout);
+    const unsigned tiles = tiles_for(max_frontier, tile_pos);
     HopParams p{};
+    p.tile_pos = tile_pos;
     p.ro = graph->row_offsets;
     p.ci = graph->col_indices;
     p.n = (uint64_t)graph->num_vertices;
@@ -347,6 +496,7 @@ int gc_hop_expand(const gc_csr_t* graph, const uint32_t* d_frontier, uint64_t fr
     p.bitmap = d_bitmap;
     p.bwords = bitmap_words;
     p.mark_frontier = mark_frontier;
+    p.exact_only = g_exact_only;
     if (hot) {
         p.topo_reads = hot->topo_reads;
         p.edge_trav = hot->edge_traversals;
@@ -360,7 +510,17 @@ int gc_hop_expand(const gc_csr_t* graph, const uint32_t* d_frontier, uint64_t fr
     GC_TRY(cudaMemsetAsync(d_temp, 0, state_bytes + 256, s), "gc_hop_expand memset");
     const uint64_t grid = (uint64_t)num_batches * tiles;
     GC_REQUIRE(grid < (1ull << 31), GC_ERR_VALUE, "gc_hop_expand: window too large");
-    k_hop_expand<<<(unsigned)grid, kHopThreads, 0, s>>>(p);
+    switch (network_slots(fanout)) {
+        case 4: k_hop_expand<4><<<(unsigned)grid, kHopThreads, 0, s>>>(p); break;
+        case 6: k_hop_expand<6><<<(unsigned)grid, kHopThreads, 0, s>>>(p); break;
+        case 8: k_hop_expand<8><<<(unsigned)grid, kHopThreads, 0, s>>>(p); break;
+        case 11: k_hop_expand<11><<<(unsigned)grid, kHopThreads, 0, s>>>(p); break;
+        case 16: k_hop_expand<16><<<(unsigned)grid, kHopThreads, 0, s>>>(p); break;
+        case 21: k_hop_expand<21><<<(unsigned)grid, kHopThreads, 0, s>>>(p); break;
+        case 26: k_hop_expand<26><<<(unsigned)grid, kHopThreads, 0, s>>>(p); break;
+        case 32: k_hop_expand<32><<<(unsigned)grid, kHopThreads, 0, s>>>(p); break;
+        default: k_hop_expand<0><<<(unsigned)grid, kHopThreads, 0, s>>>(p); break;
+    }
     GC_CHECK_LAUNCH("gc_hop_expand");
     return GC_OK;
 }

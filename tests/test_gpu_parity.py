@@ -211,3 +211,27 @@ def test_gather_unaligned_row_width():
     ids = np.array([5, 999, 0, 5, 321])
     got = gather_rows(FeatureStore.resident(table), ids)
     assert np.array_equal(got, O.synthetic_features(ids, 7))
+
+
+@pytest.mark.parametrize("deg,fanouts", [(26, (15, 10, 5)), (55, (25, 10)), (100, (40, 3))])
+def test_packed_and_exact_selection_agree(deg, fanouts):
+    """The packed 32-bit REDUX extraction and the 64-bit path give identical samples."""
+    P = _pkg()
+    from paper_2305_16588_b200 import _lib
+
+    lib = _lib.load_library()
+    gr = P.generate_synthetic(30_000, deg, 1.1, seed=deg)
+    seeds = np.random.default_rng(deg).integers(0, 30_000, 512)
+    cfg = P.SamplingConfig(fanouts=fanouts, batch_size=512)
+    stream = P.KeyedRng(11).derive(deg)
+    fast = P.sample_batch(gr, seeds, cfg, stream)
+    _lib.check(lib.gc_set_option(_lib.GC_OPT_EXACT_SELECTION, 1))
+    try:
+        exact = P.sample_batch(gr, seeds, cfg, stream)
+    finally:
+        _lib.check(lib.gc_set_option(_lib.GC_OPT_EXACT_SELECTION, 0))
+    for a, b in zip(fast.hops, exact.hops):
+        assert np.array_equal(a.neighbors, b.neighbors) and np.array_equal(a.offsets, b.offsets)
+    want = O.sample_batch(gr.row_offsets, gr.col_indices, gr.num_vertices, seeds, fanouts, stream.key)
+    for a, (_, off, nbr) in zip(exact.hops, want):
+        assert np.array_equal(a.neighbors, nbr)
