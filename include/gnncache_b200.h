@@ -124,19 +124,19 @@ int gc_hop_expand(const gc_csr_t* graph, const uint32_t* d_frontier, uint64_t fr
 uint64_t gc_bitmap_words(int64_t num_vertices);
 /* np.unique of seeds ∪ all hop neighbors (sampling.py:73-75) from the visited bitmaps:
  * sorted distinct ids of batch b -> d_unique + b*unique_stride, count -> d_unique_count[b];
- * d_word_prefix (optional) receives the exclusive popcount prefix per word for gc_relabel.
- * feat_lookups (optional) += 1 per distinct id (sampling.py:242). clear_bitmap zeroes the
- * bitmap as it is consumed (only valid if no later gc_relabel reads it). */
+ * d_rank_table (optional, 2*bitmap_words u32 per batch) receives {exclusive popcount
+ * prefix, bitmap word} per word for gc_relabel. feat_lookups (optional) += 1 per
+ * distinct id (sampling.py:242). clear_bitmap zeroes the bitmap as it is consumed. */
 size_t gc_unique_temp_bytes(uint32_t num_batches, uint64_t bitmap_words);
 int gc_unique_compact(uint32_t* d_bitmap, uint64_t bitmap_words, uint32_t num_batches, uint32_t* d_unique,
-                      uint64_t unique_stride, uint32_t* d_unique_count, uint32_t* d_word_prefix,
+                      uint64_t unique_stride, uint32_t* d_unique_count, uint32_t* d_rank_table,
                       uint64_t* d_feat_lookups, int clear_bitmap, void* d_temp, size_t temp_bytes,
                       void* stream);
 /* Relabel (not in the reference; CPU restatement np.searchsorted(unique, ids)):
  * d_local[b*stride + k] = index of d_ids[b*stride + k] in batch b's unique list. */
 int gc_relabel(const uint32_t* d_ids, uint64_t ids_stride, const uint32_t* d_ids_count, uint32_t max_count,
-               uint32_t num_batches, const uint32_t* d_bitmap, const uint32_t* d_word_prefix,
-               uint64_t bitmap_words, uint32_t* d_local, void* stream);
+               uint32_t num_batches, const uint32_t* d_rank_table, uint64_t bitmap_words, uint32_t* d_local,
+               void* stream);
 /* Mark ids in the per-batch visited bitmaps (seeds of a zero-hop config). */
 int gc_mark_visited(const uint32_t* d_ids, uint64_t ids_stride, const uint32_t* d_count, uint32_t max_count,
                     uint32_t num_batches, uint32_t* d_bitmap, uint64_t bitmap_words, void* stream);

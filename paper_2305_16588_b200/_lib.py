@@ -89,7 +89,7 @@ SIGNATURES = {
     "gc_bitmap_words": (U64, [I64]),
     "gc_unique_temp_bytes": (SZ, [U32, U64]),
     "gc_unique_compact": (ctypes.c_int, [V, U64, U32, V, U64, V, V, V, ctypes.c_int, V, SZ, V]),
-    "gc_relabel": (ctypes.c_int, [V, U64, V, U32, U32, V, V, U64, V, V]),
+    "gc_relabel": (ctypes.c_int, [V, U64, V, U32, U32, V, U64, V, V]),
     "gc_mark_visited": (ctypes.c_int, [V, U64, V, U32, U32, V, U64, V]),
     "gc_synth_features": (ctypes.c_int, [U64, U64, U32, V, V]),
     "gc_bitmap_clear": (ctypes.c_int, [V, U64, U32, V, U64, V, U32, V]),

@@ -33,10 +33,25 @@ __host__ __device__ __forceinline__ uint64_t hash_counter(uint64_t key, uint64_t
     return mix64((a + kGolden) ^ key);
 }
 
+// Bits 63..33 of mix64(x): the final `x ^= x >> 31` (rng.py:30) only changes bits
+// 32..0, so selection that compares key prefixes of <= 31 bits can skip it.
+__host__ __device__ __forceinline__ uint64_t mix64_high(uint64_t x) {
+    x ^= x >> 30;
+    x *= kMixA;
+    x ^= x >> 27;
+    x *= kMixB;
+    return x;
+}
+
 // KeyedRng.hash_pairs(a, b) = mix64((b + G) ^ hash_counters(a)), rng.py:68-72;
 // `ha` is the per-position hash_counter, hoisted out of the per-edge loop.
 __host__ __device__ __forceinline__ uint64_t hash_pair(uint64_t ha, uint64_t b) {
     return mix64((b + kGolden) ^ ha);
+}
+
+// hash_pair with only bits 63..33 exact (see mix64_high)
+__host__ __device__ __forceinline__ uint64_t hash_pair_high(uint64_t ha, uint64_t b) {
+    return mix64_high((b + kGolden) ^ ha);
 }
 
 void set_error(const std::string& msg);

@@ -1,8 +1,9 @@
 // K3 unique + relabel: BatchSample.distinct_vertices (sampling.py:73-75) is np.unique,
 // i.e. the sorted distinct ids. Every emitted vertex marks a per-batch visited bitmap
 // inside hop_expand, so the sorted unique list falls out of one ordered popcount scan
-// of the bitmap (no sort). The per-word exclusive popcount doubles as the relabel map:
-// local(u) = prefix[u >> 5] + popc(word & lanes-below(u)).
+// of the bitmap (no sort). The per-word exclusive popcount, stored interleaved with
+// the word itself as a rank table {prefix, bits}, is the relabel map:
+// local(u) = prefix[u >> 5] + popc(bits[u >> 5] & lanes-below(u)) — one 8-byte load.
 #include <cub/block/block_scan.cuh>
 
 #include "gc_common.cuh"
@@ -20,7 +21,7 @@ struct UniqueParams {
     uint32_t* uniq;
     uint64_t ustride;
     uint32_t* ucount;
-    uint32_t* wprefix;
+    uint2* rank;
     uint64_t* feat;
     int clear;
     uint64_t* tile_state;
@@ -53,9 +54,11 @@ __global__ void __launch_bounds__(kUniqThreads) k_unique(UniqueParams p) {
     __syncthreads();
     const uint32_t base = (uint32_t)s_prefix + excl;
     if (w0 < p.bwords) {
-        if (p.wprefix)
-            *reinterpret_cast<uint4*>(p.wprefix + b * p.bwords + w0) =
-                make_uint4(base, base + c0, base + c0 + c1, base + c0 + c1 + c2);
+        if (p.rank) {
+            uint4* rt = reinterpret_cast<uint4*>(p.rank + b * p.bwords + w0);
+            rt[0] = make_uint4(base, x.x, base + c0, x.y);
+            rt[1] = make_uint4(base + c0 + c1, x.z, base + c0 + c1 + c2, x.w);
+        }
         uint32_t* out = p.uniq + b * p.ustride;
         uint32_t pos = base;
         const uint32_t words[4] = {x.x, x.y, x.z, x.w};
@@ -76,17 +79,16 @@ __global__ void __launch_bounds__(kUniqThreads) k_unique(UniqueParams p) {
 }
 
 __global__ void k_relabel(const uint32_t* __restrict__ ids, uint64_t stride, const uint32_t* __restrict__ count,
-                          const uint32_t* __restrict__ bm, const uint32_t* __restrict__ wp, uint64_t bwords,
-                          uint32_t* __restrict__ local) {
+                          const uint2* __restrict__ rank, uint64_t bwords, uint32_t* __restrict__ local) {
     const uint32_t b = blockIdx.y;
     const uint32_t c = count[b];
-    const uint32_t* row = bm + b * bwords;
-    const uint32_t* pre = wp + b * bwords;
+    const uint2* rt = rank + b * bwords;
+    const uint32_t* in = ids + b * stride;
+    uint32_t* out = local + b * stride;
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < c; k += gridDim.x * blockDim.x) {
-        const uint32_t u = ids[b * stride + k];
-        const uint32_t w = u >> 5;
-        const uint32_t below = (1u << (u & 31)) - 1u;
-        local[b * stride + k] = __ldg(pre + w) + __popc(__ldg(row + w) & below);
+        const uint32_t u = __ldcs(in + k);
+        const uint2 e = __ldg(rt + (u >> 5));
+        __stcs(out + k, e.x + __popc(e.y & ((1u << (u & 31)) - 1u)));
     }
 }
 
@@ -138,7 +140,7 @@ size_t gc_unique_temp_bytes(uint32_t num_batches, uint64_t bitmap_words) {
 }
 
 int gc_unique_compact(uint32_t* d_bitmap, uint64_t bitmap_words, uint32_t num_batches, uint32_t* d_unique,
-                      uint64_t unique_stride, uint32_t* d_unique_count, uint32_t* d_word_prefix,
+                      uint64_t unique_stride, uint32_t* d_unique_count, uint32_t* d_rank_table,
                       uint64_t* d_feat_lookups, int clear_bitmap, void* d_temp, size_t temp_bytes,
                       void* stream) {
     GC_REQUIRE(bitmap_words % 4 == 0, GC_ERR_VALUE, "gc_unique_compact: bitmap_words must be a multiple of 4");
@@ -155,7 +157,7 @@ int gc_unique_compact(uint32_t* d_bitmap, uint64_t bitmap_words, uint32_t num_ba
     p.uniq = d_unique;
     p.ustride = unique_stride;
     p.ucount = d_unique_count;
-    p.wprefix = d_word_prefix;
+    p.rank = reinterpret_cast<uint2*>(d_rank_table);
     p.feat = d_feat_lookups;
     p.clear = clear_bitmap;
     p.tile_state = static_cast<uint64_t*>(d_temp);
@@ -169,13 +171,14 @@ int gc_unique_compact(uint32_t* d_bitmap, uint64_t bitmap_words, uint32_t num_ba
 }
 
 int gc_relabel(const uint32_t* d_ids, uint64_t ids_stride, const uint32_t* d_ids_count, uint32_t max_count,
-               uint32_t num_batches, const uint32_t* d_bitmap, const uint32_t* d_word_prefix,
-               uint64_t bitmap_words, uint32_t* d_local, void* stream) {
+               uint32_t num_batches, const uint32_t* d_rank_table, uint64_t bitmap_words, uint32_t* d_local,
+               void* stream) {
     GC_REQUIRE(num_batches < 65536, GC_ERR_VALUE, "gc_relabel: at most 65535 batches per call");
     if (num_batches == 0 || max_count == 0) return GC_OK;
     dim3 grid(grid_x(max_count, 256), num_batches);
-    k_relabel<<<grid, 256, 0, as_stream(stream)>>>(d_ids, ids_stride, d_ids_count, d_bitmap, d_word_prefix,
-                                                   bitmap_words, d_local);
+    k_relabel<<<grid, 256, 0, as_stream(stream)>>>(d_ids, ids_stride, d_ids_count,
+                                                   reinterpret_cast<const uint2*>(d_rank_table), bitmap_words,
+                                                   d_local);
     GC_CHECK_LAUNCH("gc_relabel");
     return GC_OK;
 }

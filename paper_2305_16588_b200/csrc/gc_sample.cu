@@ -166,7 +166,7 @@ __device__ __forceinline__ bool select_packed(uint64_t hc, uint32_t deg, uint32_
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const uint32_t j = lane + 32u * r;
-        const uint64_t key = hash_pair(hc, j);
+        const uint64_t key = hash_pair_high(hc, j);  // only bits >= 37 are used
         pk[r] = j < deg ? ((uint32_t)(key >> (32 + IB)) << IB) | j : 0xFFFFFFFFu;
         rank[r] = 0xFFFFFFFFu;
     }
@@ -251,7 +251,7 @@ __device__ __forceinline__ bool select_thread(uint64_t hc, uint32_t deg, uint32_
 #pragma unroll
     for (int s = 0; s < S; ++s) t[s] = 0xFFFFFFFFu;
     for (uint32_t j = 0; j < deg; ++j) {
-        const uint32_t x = ((uint32_t)(hash_pair(hc, j) >> (32 + IB)) << IB) | j;
+        const uint32_t x = ((uint32_t)(hash_pair_high(hc, j) >> (32 + IB)) << IB) | j;
 #pragma unroll
         for (int s = S - 1; s >= 1; --s) t[s] = max(t[s - 1], min(t[s], x));
         t[0] = min(t[0], x);
@@ -291,7 +291,7 @@ __device__ __forceinline__ void select_warp(uint64_t hc, uint32_t d, uint32_t fa
 }
 
 template <int S>
-__global__ void __launch_bounds__(kHopThreads) k_hop_expand(HopParams p) {
+__global__ void __launch_bounds__(kHopThreads, (S > 0 && S <= 16) ? 5 : 1) k_hop_expand(HopParams p) {
     using Scan = cub::BlockScan<uint32_t, kHopThreads>;
     using Reduce = cub::BlockReduce<uint64_t, kHopThreads>;
     __shared__ union {

@@ -127,7 +127,7 @@ class SampleGatherPipeline:
             if end is not None:
                 end.record()
             end = self._stage("unique_relabel")
-            sp.dedup(hot, keep_bitmap=self.store is not None and not sp.relabel)
+            sp.dedup(hot)
             self.launches += 1 + (H + 1 if sp.relabel else 0)
             if end is not None:
                 end.record()
@@ -137,9 +137,6 @@ class SampleGatherPipeline:
                 self.launches += 1
                 if end is not None:
                     end.record()
-            if sp.relabel or self.store is not None:
-                sp.release_bitmap()
-                self.launches += 1
             if on_window is not None:
                 on_window(self, w0, nb)
 

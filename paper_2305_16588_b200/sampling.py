@@ -185,7 +185,8 @@ class WindowSampler:
         self.ucap = max(1, bound if unique_cap is None else min(bound, int(unique_cap)))
         self.unique = torch.empty((W, self.ucap), dtype=i32, device=dev)
         self.ucount = torch.zeros(W, dtype=i32, device=dev)
-        self.wprefix = torch.empty((W, self.words), dtype=i32, device=dev) if relabel else None
+        # relabel rank table: {exclusive popcount prefix, bitmap word} per word
+        self.rank = torch.empty((W, 2 * self.words), dtype=i32, device=dev) if relabel else None
         self.local_seeds = torch.empty((W, self.B), dtype=i32, device=dev) if relabel else None
         self.local_nbrs = [torch.empty_like(t) for t in self.nbrs] if relabel else None
         hop_tmp = max([self.lib.gc_hop_expand_temp_bytes(W, caps[h]) for h in range(self.H)] + [256])
@@ -235,14 +236,15 @@ class WindowSampler:
                 "mark_visited",
             )
 
-    def dedup(self, hot: DeviceHotness | None = None, keep_bitmap: bool = False, stream=None) -> None:
+    def dedup(self, hot: DeviceHotness | None = None, stream=None) -> None:
+        """Sorted unique ids per batch; the visited bitmap is cleared as it is consumed
+        (relabel reads the interleaved rank table instead)."""
         s = _lib.stream_handle(stream)
-        keep = keep_bitmap or self.relabel
         _lib.check(
             self.lib.gc_unique_compact(
                 self.bitmap.data_ptr(), self.words, self.active, self.unique.data_ptr(), self.ucap,
-                self.ucount.data_ptr(), _lib.ptr(self.wprefix), hot.feat_lookups.data_ptr() if hot else None,
-                0 if keep else 1, self.uq_tmp.data_ptr(), self.uq_tmp.numel(), s,
+                self.ucount.data_ptr(), _lib.ptr(self.rank), hot.feat_lookups.data_ptr() if hot else None,
+                1, self.uq_tmp.data_ptr(), self.uq_tmp.numel(), s,
             ),
             "unique_compact",
         )
@@ -253,24 +255,13 @@ class WindowSampler:
             for ids, cnt, loc, cap in arrays:
                 _lib.check(
                     self.lib.gc_relabel(ids.data_ptr(), ids.shape[1], cnt.data_ptr(), cap, self.active,
-                                        self.bitmap.data_ptr(), self.wprefix.data_ptr(), self.words,
-                                        loc.data_ptr(), s),
+                                        self.rank.data_ptr(), self.words, loc.data_ptr(), s),
                     "relabel",
                 )
-
-    def release_bitmap(self, stream=None) -> None:
-        """Zero the words the window touched (after relabel/keep_bitmap)."""
-        _lib.check(
-            self.lib.gc_bitmap_clear(self.bitmap.data_ptr(), self.words, self.active, self.unique.data_ptr(),
-                                     self.ucap, self.ucount.data_ptr(), self.ucap, _lib.stream_handle(stream)),
-            "bitmap_clear",
-        )
 
     def run(self, hot: DeviceHotness | None = None, stream=None) -> None:
         self.expand(hot, stream)
         self.dedup(hot, stream=stream)
-        if self.relabel:
-            self.release_bitmap(stream)
 
     # ---- host views (API drivers / tests)
     def batch_to_host(self, b: int) -> BatchSample:
