@@ -54,10 +54,11 @@ __global__ void __launch_bounds__(kUniqThreads) k_unique(UniqueParams p) {
     __syncthreads();
     const uint32_t base = (uint32_t)s_prefix + excl;
     if (w0 < p.bwords) {
-        if (p.rank) {
+        // relabel only looks up words holding a present id: empty words need no entry
+        if (p.rank && (x.x | x.y | x.z | x.w)) {
             uint4* rt = reinterpret_cast<uint4*>(p.rank + b * p.bwords + w0);
-            rt[0] = make_uint4(base, x.x, base + c0, x.y);
-            rt[1] = make_uint4(base + c0 + c1, x.z, base + c0 + c1 + c2, x.w);
+            if (x.x | x.y) rt[0] = make_uint4(base, x.x, base + c0, x.y);
+            if (x.z | x.w) rt[1] = make_uint4(base + c0 + c1, x.z, base + c0 + c1 + c2, x.w);
         }
         uint32_t* out = p.uniq + b * p.ustride;
         uint32_t pos = base;
@@ -78,6 +79,14 @@ __global__ void __launch_bounds__(kUniqThreads) k_unique(UniqueParams p) {
     if (t == p.tiles_per_batch - 1 && tid == kUniqThreads - 1) p.ucount[b] = (uint32_t)s_prefix + excl + c0 + c1 + c2 + c3;
 }
 
+__device__ __forceinline__ uint32_t rank_of(const uint2* __restrict__ rt, uint32_t u) {
+    const uint2 e = __ldg(rt + (u >> 5));
+    return e.x + __popc(e.y & ((1u << (u & 31)) - 1u));
+}
+
+// VEC ids per thread per step (16-byte streaming loads/stores when the batch stride
+// keeps rows 16-byte aligned), so VEC independent rank-table loads are in flight
+template <int VEC>
 __global__ void k_relabel(const uint32_t* __restrict__ ids, uint64_t stride, const uint32_t* __restrict__ count,
                           const uint2* __restrict__ rank, uint64_t bwords, uint32_t* __restrict__ local) {
     const uint32_t b = blockIdx.y;
@@ -85,10 +94,22 @@ __global__ void k_relabel(const uint32_t* __restrict__ ids, uint64_t stride, con
     const uint2* rt = rank + b * bwords;
     const uint32_t* in = ids + b * stride;
     uint32_t* out = local + b * stride;
-    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < c; k += gridDim.x * blockDim.x) {
-        const uint32_t u = __ldcs(in + k);
-        const uint2 e = __ldg(rt + (u >> 5));
-        __stcs(out + k, e.x + __popc(e.y & ((1u << (u & 31)) - 1u)));
+    if constexpr (VEC == 4) {
+        const uint32_t c4 = c / 4;
+        for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < c4; k += gridDim.x * blockDim.x) {
+            const uint4 u = __ldcs(reinterpret_cast<const uint4*>(in) + k);
+            uint4 r;
+            r.x = rank_of(rt, u.x);
+            r.y = rank_of(rt, u.y);
+            r.z = rank_of(rt, u.z);
+            r.w = rank_of(rt, u.w);
+            __stcs(reinterpret_cast<uint4*>(out) + k, r);
+        }
+        const uint32_t k = c4 * 4 + blockIdx.x * blockDim.x + threadIdx.x;
+        if (k < c) out[k] = rank_of(rt, in[k]);
+    } else {
+        for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < c; k += gridDim.x * blockDim.x)
+            out[k] = rank_of(rt, __ldcs(in + k));
     }
 }
 
@@ -175,10 +196,15 @@ int gc_relabel(const uint32_t* d_ids, uint64_t ids_stride, const uint32_t* d_ids
                void* stream) {
     GC_REQUIRE(num_batches < 65536, GC_ERR_VALUE, "gc_relabel: at most 65535 batches per call");
     if (num_batches == 0 || max_count == 0) return GC_OK;
-    dim3 grid(grid_x(max_count, 256), num_batches);
-    k_relabel<<<grid, 256, 0, as_stream(stream)>>>(d_ids, ids_stride, d_ids_count,
-                                                   reinterpret_cast<const uint2*>(d_rank_table), bitmap_words,
-                                                   d_local);
+    const auto* rt = reinterpret_cast<const uint2*>(d_rank_table);
+    const bool vec = ids_stride % 4 == 0 && (uintptr_t)d_ids % 16 == 0 && (uintptr_t)d_local % 16 == 0;
+    if (vec) {
+        dim3 grid(grid_x((max_count + 3) / 4, 256), num_batches);
+        k_relabel<4><<<grid, 256, 0, as_stream(stream)>>>(d_ids, ids_stride, d_ids_count, rt, bitmap_words, d_local);
+    } else {
+        dim3 grid(grid_x(max_count, 256), num_batches);
+        k_relabel<1><<<grid, 256, 0, as_stream(stream)>>>(d_ids, ids_stride, d_ids_count, rt, bitmap_words, d_local);
+    }
     GC_CHECK_LAUNCH("gc_relabel");
     return GC_OK;
 }

@@ -1,0 +1,87 @@
+"""Windowed epoch pipeline (shuffle -> sample -> dedup -> relabel -> gather) vs the oracle."""
+
+import math
+
+import numpy as np
+import pytest
+
+import gnncache_oracle as O
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _device():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    torch.cuda.set_device(0)
+
+
+@pytest.mark.parametrize("window,batch,fanouts,deg", [(0, 256, (15, 10, 5), 26), (3, 100, (25, 10), 14),
+                                                       (2, 77, (4, 4), 40), (5, 64, (3,), 200)])
+def test_epoch_windows_match_oracle(window, batch, fanouts, deg):
+    import paper_2305_16588_b200 as P
+    from paper_2305_16588_b200.cache import FeatureStore
+    from paper_2305_16588_b200.graph import synthetic_features_device
+    from paper_2305_16588_b200.pipeline import SampleGatherPipeline
+
+    n, dim = 40_000, 100
+    g = P.generate_synthetic(n, deg, 1.2, seed=3)
+    pool = np.sort(np.random.default_rng(1).choice(n, 1500, replace=False)).astype(np.int64)
+    cfg = P.SamplingConfig(fanouts=fanouts, batch_size=batch)
+    store = FeatureStore.resident(synthetic_features_device(0, n, dim))
+    pipe = SampleGatherPipeline(g, cfg, store, len(pool), window=window or None)
+    gs = P.KeyedRng(9).derive(2, 0, 0)
+    plan = pipe.plan_epoch(pool, gs)
+    table = O.synthetic_features(np.arange(n), dim)
+    shuffled = pool[O.permutation(gs.derive(1).key, len(pool))]
+    seen = []
+
+    def check(p, w0, nbw):
+        sp = p.sampler
+        torch.cuda.synchronize()
+        counts = sp.counts[:, :nbw].cpu().numpy()
+        for bi in range(nbw):
+            b = w0 + bi
+            seeds = shuffled[b * batch : (b + 1) * batch]
+            hops = O.sample_batch(g.row_offsets, g.col_indices, n, seeds, fanouts, gs.derive(2, b).key)
+            got_seeds = sp.seeds[bi, : counts[0, bi]].cpu().numpy().view(np.uint32)
+            assert np.array_equal(got_seeds, seeds)
+            uniq = O.distinct_vertices(seeds, hops)
+            u = int(sp.ucount[bi])
+            assert np.array_equal(sp.unique[bi, :u].cpu().numpy().view(np.uint32), uniq)
+            assert np.array_equal(sp.local_seeds[bi, : len(seeds)].cpu().numpy(), O.relabel(uniq, seeds))
+            for h, (_, off, nbr) in enumerate(hops):
+                t = int(counts[h + 1, bi])
+                assert t == len(nbr)
+                assert np.array_equal(sp.nbrs[h][bi, :t].cpu().numpy().view(np.uint32), nbr)
+                assert np.array_equal(sp.offsets[h][bi, : len(off)].cpu().numpy(), off)
+                assert np.array_equal(sp.local_nbrs[h][bi, :t].cpu().numpy(), O.relabel(uniq, nbr))
+            assert np.array_equal(p.features[bi, :u].cpu().numpy(), table[uniq])
+            seen.append(b)
+
+    pipe.run_epoch(plan, on_window=check)
+    assert seen == list(range(math.ceil(len(pool) / batch)))
+
+
+def test_epoch_presampling_counters_match_reference_semantics():
+    """Hotness fused into the window pipeline equals the oracle epoch trace."""
+    import paper_2305_16588_b200 as P
+    from paper_2305_16588_b200.pipeline import SampleGatherPipeline
+    from paper_2305_16588_b200.sampling import DeviceHotness
+
+    n = 20_000
+    g = P.generate_synthetic(n, 12, 1.2, seed=8)
+    pool = np.arange(0, n, 13, dtype=np.int64)
+    cfg = P.SamplingConfig(fanouts=(10, 5), batch_size=128)
+    pipe = SampleGatherPipeline(g, cfg, None, len(pool), window=4)
+    hot = DeviceHotness(n)
+    seed = 77
+    pipe.run_epoch(pipe.plan_epoch(pool, P.KeyedRng(seed).derive(0, 0, 0)), hot=hot)
+    reads, looks, trav, nb = O.sampling_epoch(g.row_offsets, g.col_indices, n, [pool], [(0,)], [10, 5], 128, seed, 0)[0]
+    assert np.array_equal(hot.topo_reads.cpu().numpy(), reads)
+    assert np.array_equal(hot.feat_lookups.cpu().numpy(), looks)
+    assert np.array_equal(hot.edge_traversals.cpu().numpy(), trav)
+    t = O.transaction_cost_table(g.row_offsets)
+    assert int(hot.txn_total.item()) == int((reads * t).sum())
