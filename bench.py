@@ -19,7 +19,6 @@ import argparse
 import json
 import math
 import os
-import subprocess
 import sys
 import time
 from pathlib import Path
@@ -87,50 +86,60 @@ def peak_hbm():
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons during the timed region."""
+    """SM clock and throttle reasons sampled through NVML every ~2 ms in a thread while
+    the timed region runs (nvidia-smi's 100 ms period is longer than a C2 step)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.path = Path(f"/tmp/gc_clocks_{os.getpid()}.csv")
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = None
+        self._thread = None
+        self.error = None
 
     def __enter__(self):
+        import threading
+
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-        except (FileNotFoundError, OSError):
-            self.proc = None
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+        except Exception as exc:  # no NVML: report why instead of clocks
+            self.error = f"nvml unavailable: {exc}"
+            return self
+        self._stop = threading.Event()
+
+        def poll():
+            while not self._stop.is_set():
+                try:
+                    self.samples.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                    bits = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    for name, mask in self.REASONS.items():
+                        if bits & mask:
+                            self.reasons.add(name)
+                except Exception as exc:
+                    self.error = str(exc)
+                    return
+                self._stop.wait(0.002)
+
+        self._thread = threading.Thread(target=poll, daemon=True)
+        self._thread.start()
         return self
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            self.proc.wait()
+        if self._thread is not None:
+            self._stop.set()
+            self._thread.join()
 
     def summary(self):
-        if self.proc is None or not self.path.exists():
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.path.read_text().splitlines():
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) != 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                smax = float(parts[1])
-            except ValueError:
-                continue
-            for name, val in zip(names, parts[2:]):
-                if val.lower() == "active":
-                    reasons.add(name)
-        self.path.unlink(missing_ok=True)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        out = {"sm_mhz": float(np.median(self.samples)) if self.samples else None, "sm_max_mhz": self.max_mhz,
+               "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "nvml"}
+        if self.error:
+            out["error"] = self.error
+        return out
 
 
 # ------------------------------------------------------------------ CPU baseline (oracle port)
@@ -261,11 +270,14 @@ def run_b200(args):
     plans = [pipe.plan_epoch(pool, root.derive(e, clique, local_idx)) for e in range(args.warmup + args.steps)]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
-    stats = {"bytes": {"sampling": 0, "dedup": 0, "gather": 0}, "unique_rows": 0, "sampled": 0, "max_unique": 0}
+    H = len(cfg.fanouts)
+    hop_keys = [f"hop_expand.h{h}" for h in range(H)]
+    stats = {"bytes": {k: 0 for k in ["sampling", "dedup", "gather"] + hop_keys}, "unique_rows": 0, "sampled": 0,
+             "max_unique": 0}
 
     def account(p, w0, nbw):
         b = p.window_bytes(nbw)
-        for k in ("sampling", "dedup", "gather"):
+        for k in stats["bytes"]:
             stats["bytes"][k] += b[k]
         stats["unique_rows"] += b["unique_rows"]
         stats["sampled"] += b["sampled"]
@@ -318,8 +330,10 @@ def run_b200(args):
 
     stage = timer.summary()
     peak, peak_kind = peak_hbm()
-    stage_bytes = {"hop_expand": stats["bytes"]["sampling"], "unique_relabel": stats["bytes"]["dedup"],
-                   "gather": stats["bytes"]["gather"]}
+    stage_bytes = {"unique_relabel": stats["bytes"]["dedup"], "gather": stats["bytes"]["gather"]}
+    for k in hop_keys:
+        stage_bytes[k] = stats["bytes"][k]
+    # dominant single kernel = the stage with the most device time (one launch per window)
     dom = max((k for k in stage if k in stage_bytes), key=lambda k: stage[k][1])
     dom_launches, dom_ms = stage[dom]
     achieved = stage_bytes[dom] / (dom_ms / 1000.0) / 1e9
@@ -328,9 +342,10 @@ def run_b200(args):
     if prof.exists():
         try:
             traffic = json.loads(prof.read_text()).get(dom)
+            traffic = float(traffic) if traffic is not None else None
         except Exception:
             traffic = None
-    step_bytes = sum(stats["bytes"].values())
+    step_bytes = stats["bytes"]["sampling"] + stats["bytes"]["dedup"] + stats["bytes"]["gather"]
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -348,6 +363,7 @@ def run_b200(args):
                           "measured_us_per_batch": total_ms * 1000 / (nb * args.steps),
                           "frac": (step_bytes / (peak * 1e9)) / (total_ms / 1000.0)},
         "stages_ms": {k: v[1] / args.steps for k, v in stage.items()},
+        "stage_bytes_per_step": {k: v / args.steps for k, v in stage_bytes.items()},
         "pcie_gb_per_batch": 0.0,
         "sampled_per_batch": stats["sampled"] / (nb * args.steps),
         "unique_rows_per_batch": stats["unique_rows"] / (nb * args.steps),

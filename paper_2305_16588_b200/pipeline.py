@@ -24,8 +24,8 @@ from .rng import ROLE_SHUFFLE, KeyedRng
 from .sampling import DeviceHotness, SamplingConfig, WindowSampler, batch_hop_keys
 
 # kernels each stage launches (for the bench's gpu_launches count): CUB's onesweep
-# radix sort of 64-bit keys is 1 histogram + 8 digit passes
-LAUNCHES_PERMUTATION = 2 + 9
+# radix sort of 64-bit keys is 1 histogram + 1 scan + 8 digit passes (ncu launch list)
+LAUNCHES_PERMUTATION = 2 + 10
 
 
 @dataclass
@@ -121,11 +121,8 @@ class SampleGatherPipeline:
             sp.counts[0, :nb].copy_(plan.counts[w0:w1])
             if H:
                 sp.keys[:, :nb].copy_(plan.keys[w0:w1].t())
-            end = self._stage("hop_expand")
-            sp.expand(hot)
+            sp.expand(hot, timer=self.timer)
             self.launches += max(H, 1)
-            if end is not None:
-                end.record()
             end = self._stage("unique_relabel")
             sp.dedup(hot)
             self.launches += 1 + (H + 1 if sp.relabel else 0)
@@ -142,16 +139,25 @@ class SampleGatherPipeline:
 
     # ------------------------------------------------------------------ accounting
     def window_bytes(self, nb: int) -> dict[str, int]:
-        """Algorithmic bytes of the last window, by stage: needs a sync."""
+        """Algorithmic bytes of the last window by kernel stage; syncs.
+
+        hop h: frontier ids 4F + row-offset pair 16F + selected columns 4T read,
+               neighbours 4T + offsets 4(F+1) written
+        unique+relabel: distinct ids 4U written; every sampled id read 4 B and its
+               local index written 4 B
+        gather: U rows read from their tier and U rows written"""
         sp = self.sampler
         counts = sp.counts[:, :nb].cpu().numpy().astype(np.int64)  # [H+1, nb]
         ucount = sp.ucount[:nb].cpu().numpy().astype(np.int64)
         F = counts[:-1].sum(axis=1)  # per hop frontier positions
         T = counts[1:].sum(axis=1)  # per hop sampled neighbours
-        sampling = int((4 * F + 16 * F + 4 * T + 4 * T + 4 * (F + nb)).sum())
+        hop = 4 * F + 16 * F + 4 * T + 4 * T + 4 * (F + nb)
         ids = int(counts.sum())
         dedup = 4 * int(ucount.sum()) + (8 * ids if sp.relabel else 0)
         row = self.store.spec.row_bytes if self.store is not None else 0
         gather = 2 * row * int(ucount.sum())
-        return {"sampling": sampling, "dedup": dedup, "gather": gather, "unique_rows": int(ucount.sum()),
-                "sampled": int(T.sum())}
+        out = {"sampling": int(hop.sum()), "dedup": dedup, "gather": gather, "unique_rows": int(ucount.sum()),
+               "sampled": int(T.sum())}
+        for h in range(len(hop)):
+            out[f"hop_expand.h{h}"] = int(hop[h])
+        return out

@@ -213,11 +213,12 @@ class WindowSampler:
             self.keys[:, :nb].copy_(kt, non_blocking=True)
 
     # ---- stages
-    def expand(self, hot: DeviceHotness | None = None, stream=None) -> None:
+    def expand(self, hot: DeviceHotness | None = None, stream=None, timer=None) -> None:
         nb = self.active
         s = _lib.stream_handle(stream)
         hp = hot.c_struct if hot is not None else None
         for h, f in enumerate(self.fanouts):
+            end = timer.start(f"hop_expand.h{h}") if timer is not None else None
             front = self.seeds if h == 0 else self.nbrs[h - 1]
             _lib.check(
                 self.lib.gc_hop_expand(
@@ -229,6 +230,8 @@ class WindowSampler:
                 ),
                 "hop_expand",
             )
+            if end is not None:
+                end.record()
         if self.H == 0:
             _lib.check(
                 self.lib.gc_mark_visited(self.seeds.data_ptr(), self.B, self.counts[0].data_ptr(), self.B, nb,
