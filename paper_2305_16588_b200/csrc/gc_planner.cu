@@ -139,7 +139,7 @@ __global__ void k_split_place(const int64_t* __restrict__ order, int64_t len, co
 }
 
 // exclusive offsets in (owner-major, tile-minor) order + per-owner totals; one CTA
-__global__ void k_split_scan(const int64_t* __restrict__ tile_counts, int64_t tiles, uint32_t k,
+__global__ void __launch_bounds__(1024, 1) k_split_scan(const int64_t* __restrict__ tile_counts, int64_t tiles, uint32_t k,
                              int64_t* __restrict__ tile_offsets, int64_t* __restrict__ counts) {
     using Scan = cub::BlockScan<int64_t, 1024>;
     __shared__ typename Scan::TempStorage tmp;

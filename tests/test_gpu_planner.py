@@ -1,0 +1,106 @@
+"""Cost-model kernels (K6/K7) vs the reference's golden plan and the CPU oracle."""
+
+import numpy as np
+import pytest
+
+import gnncache_oracle as O
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _device():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _golden_setup(golden):
+    import paper_2305_16588_b200 as P
+
+    g = golden("planner")
+    graph = P.CsrGraph(len(g["graph_ro"]) - 1, len(g["graph_ci"]), g["graph_ro"], g["graph_ci"])
+    layout = P.block_layout(4, 4)
+    spec = P.HardwareSpec(layout, clique_budget_bytes=int(g["budget"][0]))
+    hot = P.HotnessMatrices(0, g["HT"].copy(), g["HF"].copy(), int(g["txn"][0]))
+    return P, g, graph, layout, spec, hot
+
+
+def test_candidate_orders_plan_and_assignment_match_reference(golden):
+    P, g, graph, layout, spec, hot = _golden_setup(golden)
+    from paper_2305_16588_b200 import planner as PL
+
+    orders = PL.build_candidate_orders(hot)
+    for k in ("topo_totals", "feat_totals", "topo_order", "feat_order", "topo_owner", "feat_owner"):
+        assert np.array_equal(getattr(orders, k), g[k]), k
+    for gi in range(4):
+        assert np.array_equal(orders.gpu_topo_queues[gi], g["topo_order"][g["topo_owner"][g["topo_order"]] == gi])
+        assert np.array_equal(orders.gpu_feat_queues[gi], g["feat_order"][g["feat_owner"][g["feat_order"]] == gi])
+    feat = P.FeatureSpec(100)
+    plan, est = PL.search_optimal_plan(orders, int(g["budget"][0]), 0.01, graph, feat, spec, hot.sampling_txn_total)
+    assert plan.alpha == g["alpha"][0]
+    assert [est.sampling_txns, est.feature_txns, est.total_txns, est.topo_prefix_len, est.feat_prefix_len] == \
+        [float(x) for x in g["est"]]
+    again = PL.estimate_traffic(orders, plan, graph, feat, spec, hot.sampling_txn_total)
+    assert again == est
+    asg = PL.materialize_assignment([orders], [plan], layout, graph, feat, spec)
+    for gi in range(4):
+        assert np.array_equal(asg.topo_vertices[gi], g[f"asg_topo{gi}"])
+        assert np.array_equal(asg.feat_vertices[gi], g[f"asg_feat{gi}"])
+        assert [asg.topo_bytes[gi], asg.feat_bytes[gi]] == list(g[f"asg_bytes{gi}"])
+
+
+def test_boundaries_match_linear_scan(golden):
+    P, g, graph, layout, spec, hot = _golden_setup(golden)
+    from paper_2305_16588_b200 import planner as PL
+
+    orders = PL.build_candidate_orders(hot)
+    deg = graph.out_degrees[orders.topo_order]
+    costs = deg * 4 + 8
+    feat = P.FeatureSpec(100)
+    for budget in (0.0, 7.5, 8.0, 1000.0, 12345.6, float(costs.sum()), float(costs.sum()) + 1):
+        total, want = 0, len(costs)
+        for i, c in enumerate(costs):
+            total += int(c)
+            if total > budget:
+                want = i
+                break
+        assert PL.boundary_topology(orders, budget, graph, spec) == want
+        assert PL.boundary_feature(orders, budget, feat) == min(len(orders.feat_order), int(budget // 400))
+    with pytest.raises(ValueError):
+        PL.boundary_topology(orders, -1.0, graph, spec)
+
+
+@pytest.mark.parametrize("n,k,hi", [(2_000_003, 8, 5), (300_000, 3, 1000), (100_000, 1, 2**40)])
+def test_ranking_with_heavy_ties_matches_lexsort(n, k, hi):
+    """Stable descending sort: ties (many, with small hi) must stay in ascending-id order."""
+    from paper_2305_16588_b200 import planner as PL
+
+    rng = np.random.default_rng(n)
+    rows = rng.integers(0, hi, size=(k, n)).astype(np.int64)
+    hot = PL.HotnessMatrices(0, rows, rows[::-1].copy(), 0)
+    orders = PL.build_candidate_orders(hot)
+    want = O.candidate_orders(rows, rows[::-1].copy())
+    for key in ("topo_totals", "topo_order", "topo_owner", "feat_order", "feat_owner"):
+        assert np.array_equal(getattr(orders, key), want[key]), key
+
+
+def test_plan_search_matches_oracle_on_generated_hotness():
+    import paper_2305_16588_b200 as P
+    from paper_2305_16588_b200 import planner as PL
+
+    g = P.generate_synthetic(50_000, 14, 1.1, seed=5)
+    layout = P.block_layout(2, 2)
+    rng = np.random.default_rng(2)
+    ht = rng.zipf(1.5, size=(2, g.num_vertices)).astype(np.int64) % 1000
+    hf = rng.zipf(1.3, size=(2, g.num_vertices)).astype(np.int64) % 1000
+    hot = P.HotnessMatrices(0, ht, hf, 123_456_789)
+    feat = P.FeatureSpec(128)
+    for budget in (1_000_000, 20_000_000, 10**12):
+        spec = P.HardwareSpec(layout, clique_budget_bytes=budget)
+        orders = PL.build_candidate_orders(hot)
+        plan, est = PL.search_optimal_plan(orders, budget, 0.01, g, feat, spec, hot.sampling_txn_total)
+        o = O.candidate_orders(ht, hf)
+        alpha, total, bt, bf, samp, fe = O.plan_search(o, g.row_offsets, budget, 0.01, 512, hot.sampling_txn_total)
+        assert (plan.alpha, est.total_txns, est.topo_prefix_len, est.feat_prefix_len) == (alpha, total, bt, bf)
