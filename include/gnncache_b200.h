@@ -205,6 +205,21 @@ size_t gc_distribute_prefix_temp_bytes(int64_t len, uint32_t k_rows);
 int gc_distribute_prefix(const int64_t* d_order, int64_t len, const int32_t* d_owner, uint32_t k_rows,
                          int64_t* d_out, int64_t* d_counts, void* d_temp, size_t temp_bytes, void* stream);
 
+/* ---------------------------------- K9: tier accounting (simulator.py:132-203) */
+
+/* holders[v] |= 1 << local_gpu for v in ids (clique membership masks, simulator.py:125-129);
+ * holders is u8[n] padded to a multiple of 4 bytes. */
+int gc_mark_holders(const int64_t* d_ids, int64_t count, uint32_t local_gpu, uint8_t* d_holders, void* stream);
+/* One GPU's TrafficReport row from its epoch trace: out u64[10 + 2k] =
+ * {topo_reads, topo_local_hits, topo_peer_hits, sampling_cpu_txn, sampling_peer_txn,
+ *  feat_lookups, feat_local_hits, feat_peer_hits, feature_cpu_txn, feature_peer_txn,
+ *  topology peer txn by serving GPU [k], feature peer txn by serving GPU [k]};
+ * the serving peer is the lowest-index holder (simulator.py:168-169). */
+int gc_tier_account(const uint64_t* d_row_offsets, int64_t n, const uint64_t* d_topo_reads,
+                    const uint64_t* d_feat_lookups, const uint8_t* d_topo_holders, const uint8_t* d_feat_holders,
+                    uint32_t local_gpu, uint32_t clique_size, uint32_t cache_line_bytes, uint32_t uint32_bytes,
+                    uint32_t row_txns, uint64_t* d_out, void* stream);
+
 /* --------------------------------------- host tier + peer mapping (plumbing) */
 
 /* Register host memory as mapped, read-only pinned memory (UVA host tier). */

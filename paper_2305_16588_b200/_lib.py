@@ -104,6 +104,8 @@ SIGNATURES = {
     "gc_searchsorted_right": (ctypes.c_int, [V, I64, V, I32, V, V]),
     "gc_distribute_prefix_temp_bytes": (SZ, [I64, U32]),
     "gc_distribute_prefix": (ctypes.c_int, [V, I64, V, U32, V, V, V, SZ, V]),
+    "gc_mark_holders": (ctypes.c_int, [V, I64, U32, V, V]),
+    "gc_tier_account": (ctypes.c_int, [V, I64, V, V, V, V, U32, U32, U32, U32, U32, V, V]),
     "gc_host_register": (ctypes.c_int, [V, SZ, ctypes.POINTER(ctypes.c_void_p)]),
     "gc_host_unregister": (ctypes.c_int, [V]),
     "gc_ipc_export": (ctypes.c_int, [V, ctypes.c_char_p]),

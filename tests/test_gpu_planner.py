@@ -104,3 +104,27 @@ def test_plan_search_matches_oracle_on_generated_hotness():
         o = O.candidate_orders(ht, hf)
         alpha, total, bt, bf, samp, fe = O.plan_search(o, g.row_offsets, budget, 0.01, 512, hot.sampling_txn_total)
         assert (plan.alpha, est.total_txns, est.topo_prefix_len, est.feat_prefix_len) == (alpha, total, bt, bf)
+
+
+def test_account_assignment_matches_reference_report(golden):
+    """Device tier accounting of the reference's golden epoch equals its TrafficReport."""
+    P, g, graph, layout, spec, hot = _golden_setup(golden)
+    from paper_2305_16588_b200 import planner as PL
+    from paper_2305_16588_b200.simulator import account_assignment, hit_rate_summary, simulate_epoch
+
+    feat = P.FeatureSpec(100)
+    asg = PL.CacheAssignment(
+        4, [g[f"asg_topo{i}"] for i in range(4)], [g[f"asg_feat{i}"] for i in range(4)],
+        [int(g[f"asg_bytes{i}"][0]) for i in range(4)], [int(g[f"asg_bytes{i}"][1]) for i in range(4)])
+    pools = [g[f"pool{i}"] for i in range(4)]
+    cfg = P.SamplingConfig(fanouts=(10, 5), batch_size=64, presample_epochs=1, seed=P.derive_seed(7, 4))
+    rep = simulate_epoch(graph, pools, cfg, asg, layout, spec, feat, seed=P.derive_seed(7, 5))
+    for k in ("sampling_cpu_txn", "sampling_peer_txn", "feature_cpu_txn", "feature_peer_txn", "topo_reads",
+              "topo_local_hits", "topo_peer_hits", "feat_lookups", "feat_local_hits", "feat_peer_hits",
+              "traffic_matrix"):
+        assert np.array_equal(getattr(rep, k), g[f"rep_{k}"]), k
+    s = hit_rate_summary(rep)
+    assert 0.0 <= s.aggregate_feat <= 1.0 and 0.0 <= s.aggregate_topo <= 1.0
+    traces = P.run_sampling_epoch(graph, pools, layout, cfg, P.derive_seed(7, 5), 0)
+    assert np.array_equal(account_assignment(traces, asg, layout, graph, spec, feat).traffic_matrix,
+                          g["rep_traffic_matrix"])
