@@ -83,6 +83,29 @@ typedef struct gc_csr {
     const uint32_t* col_indices;
 } gc_csr_t;
 
+/* Tiered topology (Legion's topology cache): the neighbour list of v is read from
+ *  - `full` when location == NULL (whole CSR in HBM, or UVA-mapped pinned host memory);
+ *  - otherwise location[v] == GC_TIER_HOST -> `full` (the host tier, over PCIe), or
+ *    location[v] == (g<<28)|slot -> clique GPU g's compact CSR slab
+ *    (slab_offsets[g][slot..slot+1] into slab_cols[g]; g == self_rank is local HBM,
+ *    any other g is read one-sided over NVLink through a mapped peer pointer).
+ * tier_reads (optional, u64[6]) += {positions, sampled edges} served {local, peer, host}. */
+typedef struct gc_topology {
+    gc_csr_t full;
+    const uint32_t* location;
+    const uint64_t* slab_offsets[GC_MAX_PEERS];
+    const uint32_t* slab_cols[GC_MAX_PEERS];
+    uint32_t self_rank;
+    uint32_t full_on_host; /* 1: `full` is pinned host memory (reads of it count as the host tier) */
+    uint64_t* tier_reads;
+} gc_topology_t;
+
+/* K8 cache fill: copy the neighbour lists of ids[0..count) from `src` (HBM or mapped
+ * host CSR) into a compact slab whose offsets d_slab_offsets[0..count] the caller has
+ * already laid out (exclusive scan of the degrees, planner.py:310 byte accounting). */
+int gc_csr_extract(const gc_csr_t* src, const int64_t* d_ids, int64_t count, const uint64_t* d_slab_offsets,
+                   uint32_t* d_slab_cols, void* stream);
+
 /* ------------------------------------------------- hotness (sampling.py:146-289) */
 
 /* Device hotness counters of one GPU (GpuTrace, sampling.py:190-197). Any pointer may
@@ -107,11 +130,12 @@ typedef struct gc_hotness {
  *  d_bitmap (optional): per-batch visited bitmap (bitmap_words u32 words per batch); every
  *                       emitted neighbor is marked, and the frontier too if mark_frontier.
  *  hot (optional)     : presampling counters of the sampling GPU.
+ * Neighbour lists come from the topology tier that holds them (gc_topology_t).
  * Selection is bit-exact with the reference: deg<=fanout copies the CSR slice in order,
  * otherwise the fanout smallest (hash_pairs(i,j), j) are emitted in ascending order.
  * Requires max_frontier*fanout < 2^32. */
 size_t gc_hop_expand_temp_bytes(uint32_t num_batches, uint32_t max_frontier);
-int gc_hop_expand(const gc_csr_t* graph, const uint32_t* d_frontier, uint64_t frontier_stride,
+int gc_hop_expand(const gc_topology_t* topo, const uint32_t* d_frontier, uint64_t frontier_stride,
                   const uint32_t* d_frontier_count, uint32_t max_frontier, uint32_t fanout,
                   const uint64_t* d_hop_keys, uint32_t num_batches, uint32_t* d_out_offsets,
                   uint64_t offsets_stride, uint32_t* d_out_nbrs, uint64_t nbrs_stride, uint32_t* d_out_count,

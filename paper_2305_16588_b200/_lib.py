@@ -38,6 +38,18 @@ class GcCsr(ctypes.Structure):
     ]
 
 
+class GcTopology(ctypes.Structure):
+    _fields_ = [
+        ("full", GcCsr),
+        ("location", ctypes.c_void_p),
+        ("slab_offsets", ctypes.c_void_p * 8),
+        ("slab_cols", ctypes.c_void_p * 8),
+        ("self_rank", ctypes.c_uint32),
+        ("full_on_host", ctypes.c_uint32),
+        ("tier_reads", ctypes.c_void_p),
+    ]
+
+
 class GcHotness(ctypes.Structure):
     _fields_ = [
         ("topo_reads", ctypes.c_void_p),
@@ -83,9 +95,10 @@ SIGNATURES = {
     "gc_hop_expand_temp_bytes": (SZ, [U32, U32]),
     "gc_hop_expand": (
         ctypes.c_int,
-        [ctypes.POINTER(GcCsr), V, U64, V, U32, U32, V, U32, V, U64, V, U64, V, V, U64, ctypes.c_int,
+        [ctypes.POINTER(GcTopology), V, U64, V, U32, U32, V, U32, V, U64, V, U64, V, V, U64, ctypes.c_int,
          ctypes.POINTER(GcHotness), V, SZ, V],
     ),
+    "gc_csr_extract": (ctypes.c_int, [ctypes.POINTER(GcCsr), V, I64, V, V, V]),
     "gc_bitmap_words": (U64, [I64]),
     "gc_unique_temp_bytes": (SZ, [U32, U64]),
     "gc_unique_compact": (ctypes.c_int, [V, U64, U32, V, U64, V, V, V, ctypes.c_int, V, SZ, V]),

@@ -23,9 +23,76 @@ import numpy as np
 import torch
 
 from . import _lib
-from .graph import FeatureSpec
+from .graph import CsrGraph, FeatureSpec
 
 TIER_NAMES = ("local", "peer", "host")
+
+
+class TopologyStore:
+    """Tiered neighbour lists of one GPU (Legion's topology cache).
+
+    CacheAssignment.topo_vertices of the clique decide the slabs: GPU g's compact CSR
+    holds the lists CSLP placed on g (in priority order); everything else is read
+    from the full CSR in pinned, mapped host memory over PCIe (or from an HBM copy
+    when host_full=False). Slabs are filled by the K8 copy kernel from the full CSR.
+    With peer_slabs=None every slab of the clique is built in this process on the
+    current device; otherwise peer_slabs[g] = (offsets address, cols address) mapped
+    from GPU g."""
+
+    def __init__(self, graph: CsrGraph, topo_vertices: list[np.ndarray], self_rank: int, host_full: bool = True,
+                 peer_slabs: list | None = None):
+        lib = _lib.lib()
+        n = graph.num_vertices
+        k = len(topo_vertices)
+        if not 0 <= self_rank < k or k > _lib.GC_MAX_PEERS:
+            raise ValueError("self_rank must index the clique (at most 8 GPUs)")
+        self.full = graph.device("host" if host_full else "hbm")
+        loc = np.full(n, _lib.GC_TIER_HOST, dtype=np.uint32)
+        deg = graph.out_degrees
+        self.slabs: list = []
+        for g, verts in enumerate(topo_vertices):
+            verts = np.asarray(verts, dtype=np.int64)
+            if len(verts) >= 1 << 28:
+                raise ValueError("at most 2^28 cached neighbour lists per GPU")
+            if len(verts) and (loc[verts] != _lib.GC_TIER_HOST).any():
+                raise ValueError("a vertex's topology is cached on two GPUs; the clique cache is partitioned")
+            loc[verts] = (np.uint32(g) << np.uint32(28)) | np.arange(len(verts), dtype=np.uint32)
+            if peer_slabs is not None and g != self_rank:
+                self.slabs.append(peer_slabs[g])
+                continue
+            offs = np.zeros(len(verts) + 1, dtype=np.uint64)
+            np.cumsum(deg[verts], out=offs[1:])
+            d_offs = torch.from_numpy(offs.view(np.int64)).cuda()
+            d_cols = torch.empty(max(int(offs[-1]), 1), dtype=torch.int32, device="cuda")
+            d_ids = torch.from_numpy(verts).cuda()
+            _lib.check(lib.gc_csr_extract(self.full.c_struct, d_ids.data_ptr(), len(verts), d_offs.data_ptr(),
+                                          d_cols.data_ptr(), _lib.stream_handle()), "csr_extract")
+            self.slabs.append((d_offs, d_cols))
+        self.location = torch.from_numpy(loc.view(np.int32)).cuda()
+        self.tier_reads = torch.zeros(6, dtype=torch.int64, device="cuda")
+        t = _lib.GcTopology()
+        t.full = self.full.c_struct
+        t.location = self.location.data_ptr()
+        for g, slab in enumerate(self.slabs):
+            o, c = slab
+            t.slab_offsets[g] = o if isinstance(o, int) else o.data_ptr()
+            t.slab_cols[g] = c if isinstance(c, int) else c.data_ptr()
+        t.self_rank = self_rank
+        t.full_on_host = 1 if host_full else 0
+        t.tier_reads = self.tier_reads.data_ptr()
+        self.c_struct = t
+        self.self_rank = self_rank
+
+    def tier_counts(self) -> dict:
+        v = self.tier_reads.cpu().numpy()
+        return {f"{what}_{tier}": int(v[i * 3 + j]) for i, what in enumerate(("reads", "edges"))
+                for j, tier in enumerate(TIER_NAMES)}
+
+    def host_bytes(self) -> int:
+        """PCIe payload of host-tier list reads so far: a 16-byte row-offset pair per read
+        plus 4 bytes per sampled column."""
+        v = self.tier_reads.cpu().numpy()
+        return int(16 * v[2] + 4 * v[5])
 
 
 @dataclass

@@ -25,10 +25,19 @@ constexpr int kHopThreads = 256;
 constexpr int kTilePos = 256;
 constexpr int kItemCap = 4096;  // staged output items per round (32 KB of u64 edge indices)
 
+constexpr int kTierShift = 56;  // staged edge index = (tier code << 56) | edge within that tier's CSR
+constexpr uint64_t kEdgeMask = (1ull << kTierShift) - 1;
+
 struct HopParams {
     const uint64_t* ro;
     const uint32_t* ci;
     uint64_t n;
+    const uint32_t* loc;
+    const uint64_t* soff[GC_MAX_PEERS];
+    const uint32_t* scols[GC_MAX_PEERS];
+    uint32_t self_rank;
+    uint32_t full_on_host;
+    uint64_t* tier_reads;
     const uint32_t* frontier;
     uint64_t fstride;
     const uint32_t* fcount;
@@ -318,11 +327,23 @@ __global__ void __launch_bounds__(kHopThreads, (S > 0 && S <= 16) ? 5 : 1) k_hop
     const bool valid = tid < (int)npos;
     uint32_t v = 0, deg = 0, take = 0;
     uint64_t o0 = 0, hc = 0;
+    // 0 local, 1 peer slab, 2 host; the full CSR is local unless it lives in host memory
+    int tier = (p.loc || p.full_on_host) ? 2 : 0;
     if (valid) {
         v = p.frontier[b * p.fstride + p0 + tid];
         if (v < p.n) {
-            o0 = p.ro[v];
-            deg = (uint32_t)(p.ro[v + 1] - o0);
+            const uint32_t L = p.loc ? __ldg(p.loc + v) : GC_TIER_HOST;
+            if (L == GC_TIER_HOST) {
+                o0 = p.ro[v];
+                deg = (uint32_t)(p.ro[v + 1] - o0);
+            } else {
+                const uint32_t g = L >> 28, slot = L & 0x0FFFFFFFu;
+                const uint64_t* so = p.soff[g];
+                o0 = so[slot];
+                deg = (uint32_t)(so[slot + 1] - o0);
+                o0 |= (uint64_t)(g + 1) << kTierShift;  // tag: read the columns from slab g
+                tier = g == p.self_rank ? 0 : 1;
+            }
         }
         take = min(deg, p.fanout);
         if (p.mark_frontier && p.bitmap) mark_visited(p.bitmap + b * p.bwords, v);
@@ -339,6 +360,20 @@ __global__ void __launch_bounds__(kHopThreads, (S > 0 && S <= 16) ? 5 : 1) k_hop
                 unsigned long long c = __popc(peers);
                 if (p.topo_reads) atomicAdd((unsigned long long*)(p.topo_reads + v), c);
                 if (p.edge_trav && take) atomicAdd((unsigned long long*)(p.edge_trav + v), c * take);
+            }
+        }
+    }
+    if (p.tier_reads) {
+        // topology reads by tier: positions and sampled edges (PCIe bytes for the host tier)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const unsigned m = __ballot_sync(kFull, valid && tier == c);
+            uint32_t e = (valid && tier == c) ? take : 0u;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(kFull, e, o);
+            if (lane == 0 && m) {
+                atomicAdd((unsigned long long*)(p.tier_reads + c), (unsigned long long)__popc(m));
+                atomicAdd((unsigned long long*)(p.tier_reads + 3 + c), (unsigned long long)e);
             }
         }
     }
@@ -415,7 +450,10 @@ __global__ void __launch_bounds__(kHopThreads, (S > 0 && S <= 16) ? 5 : 1) k_hop
         uint32_t* dst = out + (uint32_t)s_prefix + r0;
 #pragma unroll 4
         for (uint32_t k = tid; k < cnt; k += kHopThreads) {
-            uint32_t u = __ldg(p.ci + s_items[k]);
+            const uint64_t it = s_items[k];
+            const uint32_t code = (uint32_t)(it >> kTierShift);
+            const uint32_t* cols = code ? p.scols[code - 1] : p.ci;
+            uint32_t u = __ldg(cols + (it & kEdgeMask));
             dst[k] = u;
             if (bm) mark_visited(bm, u);
         }
@@ -459,13 +497,14 @@ size_t gc_hop_expand_temp_bytes(uint32_t num_batches, uint32_t max_frontier) {
     return align_up((size_t)num_batches * tiles_for(max_frontier, 32) * sizeof(uint64_t), 256) + 256;
 }
 
-int gc_hop_expand(const gc_csr_t* graph, const uint32_t* d_frontier, uint64_t frontier_stride,
+int gc_hop_expand(const gc_topology_t* topo, const uint32_t* d_frontier, uint64_t frontier_stride,
                   const uint32_t* d_frontier_count, uint32_t max_frontier, uint32_t fanout,
                   const uint64_t* d_hop_keys, uint32_t num_batches, uint32_t* d_out_offsets,
                   uint64_t offsets_stride, uint32_t* d_out_nbrs, uint64_t nbrs_stride, uint32_t* d_out_count,
                   uint32_t* d_bitmap, uint64_t bitmap_words, int mark_frontier, const gc_hotness_t* hot,
                   void* d_temp, size_t temp_bytes, void* stream) {
-    GC_REQUIRE(graph && graph->row_offsets, GC_ERR_VALUE, "gc_hop_expand: graph is null");
+    GC_REQUIRE(topo && topo->full.row_offsets, GC_ERR_VALUE, "gc_hop_expand: topology is null");
+    const gc_csr_t* graph = &topo->full;
     GC_REQUIRE(fanout >= 1, GC_ERR_VALUE, "fanouts must all be >= 1");
     GC_REQUIRE((uint64_t)max_frontier * fanout < (1ull << 32), GC_ERR_VALUE,
                "gc_hop_expand: max_frontier * fanout must be < 2^32 per batch");
@@ -481,6 +520,14 @@ int gc_hop_expand(const gc_csr_t* graph, const uint32_t* d_frontier, uint64_t fr
     p.tile_pos = tile_pos;
     p.ro = graph->row_offsets;
     p.ci = graph->col_indices;
+    p.loc = topo->location;
+    for (int g = 0; g < GC_MAX_PEERS; ++g) {
+        p.soff[g] = topo->slab_offsets[g];
+        p.scols[g] = topo->slab_cols[g];
+    }
+    p.self_rank = topo->self_rank;
+    p.full_on_host = topo->full_on_host;
+    p.tier_reads = topo->tier_reads;
     p.n = (uint64_t)graph->num_vertices;
     p.frontier = d_frontier;
     p.fstride = frontier_stride;

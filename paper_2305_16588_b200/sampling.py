@@ -156,10 +156,12 @@ class WindowSampler:
     """
 
     def __init__(self, graph: CsrGraph, fanouts, batch_size: int, window: int, *, placement: str = "hbm",
-                 relabel: bool = False, unique_cap: int | None = None):
+                 relabel: bool = False, unique_cap: int | None = None, topology=None):
         self.lib = _lib.lib()
         self.graph = graph
-        self.dcsr = graph.device(placement)
+        # topology: a cache.TopologyStore (tiered lists) or the plain CSR in `placement`
+        self.topology = topology
+        self.topo_struct = topology.c_struct if topology is not None else graph.device(placement).topology
         self.n = graph.num_vertices
         self.fanouts = tuple(int(f) for f in fanouts)
         self.H = len(self.fanouts)
@@ -222,7 +224,7 @@ class WindowSampler:
             front = self.seeds if h == 0 else self.nbrs[h - 1]
             _lib.check(
                 self.lib.gc_hop_expand(
-                    self.dcsr.c_struct, front.data_ptr(), front.shape[1], self.counts[h].data_ptr(), self.caps[h], f,
+                    self.topo_struct, front.data_ptr(), front.shape[1], self.counts[h].data_ptr(), self.caps[h], f,
                     self.keys[h].data_ptr(), nb, self.offsets[h].data_ptr(), self.offsets[h].shape[1],
                     self.nbrs[h].data_ptr(), self.nbrs[h].shape[1], self.counts[h + 1].data_ptr(),
                     self.bitmap.data_ptr(), self.words, 1 if h == 0 else 0, hp,

@@ -85,3 +85,38 @@ def test_epoch_presampling_counters_match_reference_semantics():
     assert np.array_equal(hot.edge_traversals.cpu().numpy(), trav)
     t = O.transaction_cost_table(g.row_offsets)
     assert int(hot.txn_total.item()) == int((reads * t).sum())
+
+
+@pytest.mark.parametrize("host_full", [True, False])
+def test_tiered_topology_sampling_matches_oracle(host_full):
+    """Neighbour lists read from local slab / peer slabs / host CSR give the reference
+    sample, and the per-tier read counters match the tier rule (simulator.py:161-202)."""
+    import paper_2305_16588_b200 as P
+    from paper_2305_16588_b200.cache import TopologyStore
+    from paper_2305_16588_b200.sampling import WindowSampler
+
+    n = 60_000
+    g = P.generate_synthetic(n, 26, 1.2, seed=21)
+    rng = np.random.default_rng(4)
+    perm = rng.permutation(n)
+    parts = [np.sort(perm[i * 9000 : (i + 1) * 9000]) for i in range(4)]  # 60% cached across 4 GPUs, 40% host
+    store = TopologyStore(g, parts, self_rank=1, host_full=host_full)
+    fanouts = (15, 10, 5)
+    sp = WindowSampler(g, fanouts, 512, 2, topology=store)
+    seeds = rng.integers(0, n, (2, 512))
+    keys = np.array([[P.KeyedRng(5).derive(b).derive(h).key for h in range(3)] for b in range(2)], dtype=np.uint64)
+    sp.load(torch.from_numpy(seeds.astype(np.int32).reshape(-1)).cuda(), np.array([512, 512]), keys)
+    sp.run()
+    tier, _ = O.tier_of(parts, n, 1)
+    reads, edges = np.zeros(3, np.int64), np.zeros(3, np.int64)
+    for b in range(2):
+        got = sp.batch_to_host(b)
+        want = O.sample_batch(g.row_offsets, g.col_indices, n, seeds[b], fanouts, P.KeyedRng(5).derive(b).key)
+        for hop, (src, off, nbr) in zip(got.hops, want):
+            assert np.array_equal(hop.neighbors, nbr) and np.array_equal(hop.offsets, off)
+            np.add.at(reads, tier[src], 1)
+            np.add.at(edges, tier[src], np.diff(off))
+    c = store.tier_counts()
+    assert [c["reads_local"], c["reads_peer"], c["reads_host"]] == list(reads)
+    assert [c["edges_local"], c["edges_peer"], c["edges_host"]] == list(edges)
+    assert store.host_bytes() == 16 * reads[2] + 4 * edges[2]
