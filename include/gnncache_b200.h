@@ -89,7 +89,9 @@ typedef struct gc_csr {
  *    location[v] == (g<<28)|slot -> clique GPU g's compact CSR slab
  *    (slab_offsets[g][slot..slot+1] into slab_cols[g]; g == self_rank is local HBM,
  *    any other g is read one-sided over NVLink through a mapped peer pointer).
- * tier_reads (optional, u64[6]) += {positions, sampled edges} served {local, peer, host}. */
+ * tier_reads (optional, u64[7]) += {positions, sampled edges} served {local, peer, host},
+ * and [6] += sum of t(v) = 1 + ceil(deg*4/CLS) over host-tier reads (PCIe transactions,
+ * sampling.py:177-187; CLS and the id width come from `hot` when given, else 64 and 4). */
 typedef struct gc_topology {
     gc_csr_t full;
     const uint32_t* location;

@@ -69,7 +69,7 @@ class TopologyStore:
                                           d_cols.data_ptr(), _lib.stream_handle()), "csr_extract")
             self.slabs.append((d_offs, d_cols))
         self.location = torch.from_numpy(loc.view(np.int32)).cuda()
-        self.tier_reads = torch.zeros(6, dtype=torch.int64, device="cuda")
+        self.tier_reads = torch.zeros(7, dtype=torch.int64, device="cuda")
         t = _lib.GcTopology()
         t.full = self.full.c_struct
         t.location = self.location.data_ptr()
@@ -85,8 +85,13 @@ class TopologyStore:
 
     def tier_counts(self) -> dict:
         v = self.tier_reads.cpu().numpy()
-        return {f"{what}_{tier}": int(v[i * 3 + j]) for i, what in enumerate(("reads", "edges"))
-                for j, tier in enumerate(TIER_NAMES)}
+        out = {f"{what}_{tier}": int(v[i * 3 + j]) for i, what in enumerate(("reads", "edges"))
+               for j, tier in enumerate(TIER_NAMES)}
+        out["host_txn"] = int(v[6])  # PCIe transactions, the unit of TrafficReport.sampling_cpu_txn
+        return out
+
+    def reset_counters(self) -> None:
+        self.tier_reads.zero_()
 
     def host_bytes(self) -> int:
         """PCIe payload of host-tier list reads so far: a 16-byte row-offset pair per read
@@ -186,6 +191,9 @@ class FeatureStore:
     def tier_counts(self) -> dict:
         v = self.tier_rows.cpu().numpy()
         return {name: int(x) for name, x in zip(TIER_NAMES, v)}
+
+    def reset_counters(self) -> None:
+        self.tier_rows.zero_()
 
 
 def gather_rows(store: FeatureStore, ids: np.ndarray) -> np.ndarray:

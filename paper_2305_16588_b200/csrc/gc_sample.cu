@@ -376,6 +376,11 @@ __global__ void __launch_bounds__(kHopThreads, (S > 0 && S <= 16) ? 5 : 1) k_hop
                 atomicAdd((unsigned long long*)(p.tier_reads + 3 + c), (unsigned long long)e);
             }
         }
+        // PCIe transactions of host-tier reads, t(v) = 1 + ceil(deg * 4 / CLS)
+        uint32_t tx = (valid && tier == 2) ? 1u + (uint32_t)(((uint64_t)deg * p.u32b + p.cls - 1) / p.cls) : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tx += __shfl_xor_sync(kFull, tx, o);
+        if (lane == 0 && tx) atomicAdd((unsigned long long*)(p.tier_reads + 6), (unsigned long long)tx);
     }
     if (p.txn_total) {
         // t(v) = 1 + ceil(nc(v) * uint32_bytes / CLS), sampling.py:177-187
@@ -544,6 +549,8 @@ int gc_hop_expand(const gc_topology_t* topo, const uint32_t* d_frontier, uint64_
     p.bwords = bitmap_words;
     p.mark_frontier = mark_frontier;
     p.exact_only = g_exact_only;
+    p.cls = 64;
+    p.u32b = 4;
     if (hot) {
         p.topo_reads = hot->topo_reads;
         p.edge_trav = hot->edge_traversals;

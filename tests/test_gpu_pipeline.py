@@ -120,3 +120,47 @@ def test_tiered_topology_sampling_matches_oracle(host_full):
     assert [c["reads_local"], c["reads_peer"], c["reads_host"]] == list(reads)
     assert [c["edges_local"], c["edges_peer"], c["edges_host"]] == list(edges)
     assert store.host_bytes() == 16 * reads[2] + 4 * edges[2]
+
+
+def test_plan_built_cache_traffic_equals_reference_report():
+    """Presample -> CSLP plan -> materialize -> three-tier cache -> one validation epoch:
+    the device's measured local/peer/host traffic equals the reference simulator's
+    TrafficReport for the same epoch and plan (simulator.py:132-228)."""
+    import paper_2305_16588_b200 as P
+    from paper_2305_16588_b200 import planner as PL
+    from paper_2305_16588_b200.cache import FeatureStore, TopologyStore
+    from paper_2305_16588_b200.graph import synthetic_features_device
+    from paper_2305_16588_b200.partition import single_clique_partitioning
+    from paper_2305_16588_b200.pipeline import SampleGatherPipeline
+    from paper_2305_16588_b200.simulator import simulate_epoch
+
+    n, dim, k = 150_000, 128, 4
+    g = P.generate_synthetic(n, 14, 1.2, seed=P.derive_seed(3, 1))
+    train = P.select_training_set(g, 0.1, seed=P.derive_seed(3, 2))
+    layout = P.block_layout(k, k)
+    pools = P.assign_tablets(P.split_intra_clique(train, single_clique_partitioning(g), layout), layout)
+    feat = P.FeatureSpec(dim)
+    budget = int(0.15 * (g.num_edges * 4 + 8 * n + n * feat.row_bytes))
+    spec = P.HardwareSpec(layout, clique_budget_bytes=budget)
+    cfg = P.SamplingConfig(fanouts=(25, 10), batch_size=1024, presample_epochs=1, seed=P.derive_seed(3, 4))
+    hot = P.run_presampling(g, pools, layout, cfg, spec)[0]
+    orders = PL.build_candidate_orders(hot)
+    plan, est = PL.search_optimal_plan(orders, budget, 0.01, g, feat, spec, hot.sampling_txn_total)
+    asg = PL.materialize_assignment([orders], [plan], layout, g, feat, spec)
+    assert 0 < sum(map(len, asg.feat_vertices)) < n and sum(map(len, asg.topo_vertices)) > 0
+    val_seed = P.derive_seed(3, 5)
+    rep = simulate_epoch(g, pools, cfg, asg, layout, spec, feat, seed=val_seed)
+    host_table = synthetic_features_device(0, n, dim).cpu()
+    row_txns = PL.feature_row_transactions(feat, spec)
+    for gpu in (0, 2):
+        topo = TopologyStore(g, asg.topo_vertices, gpu)
+        fstore = FeatureStore.from_assignment(host_table, asg.feat_vertices, gpu)
+        pipe = SampleGatherPipeline(g, cfg, fstore, len(pools[gpu]), window=8, topology=topo)
+        pipe.run_epoch(pipe.plan_epoch(pools[gpu], P.KeyedRng(val_seed).derive(0, 0, gpu)))
+        t, f = topo.tier_counts(), fstore.tier_counts()
+        assert t["reads_local"] == rep.topo_local_hits[gpu]
+        assert t["reads_peer"] == rep.topo_peer_hits[gpu]
+        assert t["reads_local"] + t["reads_peer"] + t["reads_host"] == rep.topo_reads[gpu]
+        assert t["host_txn"] == rep.sampling_cpu_txn[gpu]
+        assert f["local"] == rep.feat_local_hits[gpu] and f["peer"] == rep.feat_peer_hits[gpu]
+        assert f["host"] * row_txns == rep.feature_cpu_txn[gpu]
