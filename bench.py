@@ -246,12 +246,20 @@ def run_b200(args):
     from paper_2305_16588_b200.graph import synthetic_features_device
     from paper_2305_16588_b200.pipeline import SampleGatherPipeline, StageTimer
 
+    from paper_2305_16588_b200.distributed import max_over_ranks, sum_over_ranks
+
     rank, local, world = dist_env()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
+    # one process per GPU; GC_DIST_BACKEND=gloo lets a test run several ranks on one GPU
+    device = local % torch.cuda.device_count()
+    torch.cuda.set_device(device)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("GC_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+        else:
+            dist.init_process_group(backend)
 
     g, pools, layout = build_inputs(args.num_vertices, world)
     pool = pools[rank]
@@ -293,7 +301,7 @@ def run_b200(args):
     pipe.timer = timer
     pipe.launches = 0
     step_ms = []
-    with ClockSampler(local) as clocks:
+    with ClockSampler(device) as clocks:
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -318,12 +326,8 @@ def run_b200(args):
 
     total_ms = float(sum(step_ms))
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-        nbt = torch.tensor([nb], dtype=torch.int64, device="cuda")
-        dist.all_reduce(nbt)
-        batches_all = int(nbt.item()) * args.steps
+        total_ms = max_over_ranks(total_ms)  # device-timed, max over ranks
+        batches_all = sum_over_ranks(nb) * args.steps
     else:
         batches_all = nb * args.steps
     value = batches_all / (total_ms / 1000.0)
@@ -373,6 +377,8 @@ def run_b200(args):
 
     if not args.no_e2e:
         line["e2e"] = e2e_run(args, g, cfg, store, pool, root, clique, local_idx, world)
+    if world > 1:
+        line["config"]["dist_backend"] = dist.get_backend()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         host = table.cpu().numpy()
         done, el = cpu_batches(g, host, pool, nb, args.cpu_seconds)
@@ -436,15 +442,18 @@ def e2e_run(args, g, cfg, store, pool, root, clique, local_idx, world):
     moved = {"h2d": 0, "d2h": 0}
     if world > 1:
         dist.barrier()
-    t0 = time.perf_counter()
+    # device events on the launching stream; the drains' host syncs sit inside them
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
     for s in range(steps):
         step(100 + s)
+    e1.record()
     torch.cuda.synchronize()
-    el = time.perf_counter() - t0
+    el = e0.elapsed_time(e1) / 1000.0
     if world > 1:
-        t = torch.tensor([el], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        el = float(t.item())
+        from paper_2305_16588_b200.distributed import max_over_ranks
+
+        el = max_over_ranks(el)
     return {"value": nb * world * steps / el, "unit": UNIT, "h2d_bytes_per_step": moved["h2d"] // steps,
             "d2h_bytes_per_step": moved["d2h"] // steps, "steps": steps,
             "api": "SampleGatherPipeline.plan_epoch/run_epoch (ctypes -> libgnncache_b200.so)"}
