@@ -54,6 +54,35 @@ __host__ __device__ __forceinline__ uint64_t hash_pair_high(uint64_t ha, uint64_
     return mix64_high((b + kGolden) ^ ha);
 }
 
+// High word of hash_pair_high(hc, j) for edge indices j < 235, specialised per
+// position. (j + G) differs from G only in its low byte while j + (G & 0xFF) < 256,
+// so x = (j + G) ^ hc has a position-constant high part H; x >> 30 depends on H
+// only, making x ^ (x >> 30) = A + c_j with A constant and c_j < 256, hence
+// (x ^ (x >> 30)) * MixA = P + c_j * MixA with P = A * MixA per position. Of the
+// second multiply only the high word is needed (selection compares bits >= 38).
+// Exact: equals (uint32_t)(hash_pair_high(hc, j) >> 32); checked against mix64 in
+// tests through every selection path.
+struct PairHashHigh {
+    uint64_t P;
+    uint32_t m;
+    __device__ __forceinline__ explicit PairHashHigh(uint64_t hc) {
+        const uint64_t H = (kGolden ^ hc) & ~0xFFull;
+        const uint64_t K = H >> 30;
+        m = (uint32_t)((hc ^ K) & 0xFFu);
+        const uint64_t p = ((H ^ K) & ~0xFFull) * kMixA;
+        // opaque copy: otherwise the compiler folds P + c*MixA back into (A + c)*MixA,
+        // a full 64x64 multiply per candidate instead of an 8x64 multiply-add
+        asm("mov.b64 %0, %1;" : "=l"(P) : "l"(p));
+    }
+    __device__ __forceinline__ uint32_t hi(uint32_t j) const {
+        const uint32_t c = ((uint32_t)(kGolden & 0xFFu) + j) ^ m;
+        uint64_t x = P + (uint64_t)c * kMixA;
+        x ^= x >> 27;
+        const uint32_t lo = (uint32_t)x, h = (uint32_t)(x >> 32);
+        return __umulhi(lo, (uint32_t)kMixB) + lo * (uint32_t)(kMixB >> 32) + h * (uint32_t)kMixB;
+    }
+};
+
 void set_error(const std::string& msg);
 int cuda_status(cudaError_t err, const char* what);
 

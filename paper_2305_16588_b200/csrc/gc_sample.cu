@@ -172,11 +172,11 @@ __device__ __forceinline__ bool select_packed(uint64_t hc, uint32_t deg, uint32_
     const uint32_t lane = threadIdx.x & 31;
     uint32_t pk[R];
     uint32_t rank[R];
+    const PairHashHigh hh(hc);  // j < 128: only key bits >= 37 are used
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const uint32_t j = lane + 32u * r;
-        const uint64_t key = hash_pair_high(hc, j);  // only bits >= 37 are used
-        pk[r] = j < deg ? ((uint32_t)(key >> (32 + IB)) << IB) | j : 0xFFFFFFFFu;
+        pk[r] = j < deg ? (hh.hi(j) & ~kIdx) | j : 0xFFFFFFFFu;
         rank[r] = 0xFFFFFFFFu;
     }
     uint32_t lmin = pk[0];
@@ -259,8 +259,9 @@ __device__ __forceinline__ bool select_thread(uint64_t hc, uint32_t deg, uint32_
     uint32_t t[S];
 #pragma unroll
     for (int s = 0; s < S; ++s) t[s] = 0xFFFFFFFFu;
+    const PairHashHigh hh(hc);  // deg <= 64: key bits 63..38 from the specialised hash
     for (uint32_t j = 0; j < deg; ++j) {
-        const uint32_t x = ((uint32_t)(hash_pair_high(hc, j) >> (32 + IB)) << IB) | j;
+        const uint32_t x = (hh.hi(j) & ~((1u << IB) - 1u)) | j;
 #pragma unroll
         for (int s = S - 1; s >= 1; --s) t[s] = max(t[s - 1], min(t[s], x));
         t[0] = min(t[0], x);
