@@ -1,0 +1,125 @@
+"""GraphSAGE training over the device-prepared mini-batches.
+
+The reference has no trainer; Legion's backend is a PyTorch GraphSAGE/GCN
+fed by the sampling server. The data-preparation kernels produce,
+per batch, the sampled position tree (frontiers are not deduplicated between hops,
+sampling.py:123-125): level 0 = seeds, level h+1 = hop h's neighbours with offsets
+into level h. Relabel maps every position to a row of the batch's gathered feature
+matrix, so the model never touches global ids:
+
+    h0[level]  = X_batch[local_ids[level]]
+    layer l    : h[level] = act(W_self h[level] + W_neigh mean(children of level+1))
+                 for levels 0 .. L-1-l
+    loss       = cross_entropy(classifier(h[0]), labels[seeds])
+
+Layer GEMMs run in PyTorch (north star: tensor cores are not part of this product);
+the mean aggregation is a segment reduce over the tree offsets.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.nn as nn
+import torch.nn.functional as F
+
+
+@dataclass
+class TreeBatch:
+    """One mini-batch as the model consumes it (all tensors on one device)."""
+
+    features: torch.Tensor  # float32 [U, D] gathered rows (U distinct vertices)
+    local: list  # per level: int64 [P_level] row index into `features`
+    offsets: list  # per hop: int64 [P_level + 1] children offsets into the next level
+    labels: torch.Tensor  # int64 [B]
+
+
+def synthetic_labels(ids, num_classes: int) -> np.ndarray:
+    """Deterministic class of a vertex: splitmix64(v) mod C (bench/test input)."""
+    v = np.asarray(ids, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        v = v ^ (v >> np.uint64(30))
+        v = v * np.uint64(0xBF58476D1CE4E5B9)
+        v = v ^ (v >> np.uint64(27))
+        v = v * np.uint64(0x94D049BB133111EB)
+        v = v ^ (v >> np.uint64(31))
+    return (v % np.uint64(num_classes)).astype(np.int64)
+
+
+def segment_mean(x: torch.Tensor, offsets: torch.Tensor) -> torch.Tensor:
+    """Mean of x over consecutive segments [offsets[i], offsets[i+1]); empty -> 0."""
+    lengths = offsets[1:] - offsets[:-1]
+    if x.shape[0] == 0:
+        return x.new_zeros((lengths.shape[0], x.shape[1]))
+    return torch.segment_reduce(x, "mean", lengths=lengths, unsafe=True, initial=0.0)
+
+
+class SAGELayer(nn.Module):
+    def __init__(self, d_in: int, d_out: int):
+        super().__init__()
+        self.lin_self = nn.Linear(d_in, d_out)
+        self.lin_neigh = nn.Linear(d_in, d_out, bias=False)
+
+    def forward(self, h_self, h_children, offsets):
+        return self.lin_self(h_self) + self.lin_neigh(segment_mean(h_children, offsets))
+
+
+class GraphSAGE(nn.Module):
+    """L-layer mean-aggregator GraphSAGE on sampled position trees."""
+
+    def __init__(self, d_in: int, hidden: int, num_classes: int, num_layers: int):
+        super().__init__()
+        dims = [d_in] + [hidden] * num_layers
+        self.layers = nn.ModuleList(SAGELayer(dims[i], dims[i + 1]) for i in range(num_layers))
+        self.classifier = nn.Linear(hidden, num_classes)
+
+    def forward(self, batch: TreeBatch) -> torch.Tensor:
+        L = len(self.layers)
+        h = [batch.features[idx] for idx in batch.local[: L + 1]]
+        for li, layer in enumerate(self.layers):
+            h = [F.relu(layer(h[lvl], h[lvl + 1], batch.offsets[lvl])) for lvl in range(L - li)]
+        return self.classifier(h[0])
+
+
+def tree_batch_from_window(pipe, b: int, labels: torch.Tensor, counts=None, ucount=None) -> TreeBatch:
+    """View batch b of the pipeline's current window as a TreeBatch (device tensors;
+    u32 ids widen to int64 for indexing). labels: int64 [n] class per vertex;
+    counts/ucount: the window's host copies of the per-batch sizes (else read here)."""
+    sp = pipe.sampler
+    counts = sp.counts[:, b].tolist() if counts is None else [int(c) for c in counts[:, b]]
+    u = int(sp.ucount[b].item()) if ucount is None else int(ucount[b])
+    feats = pipe.features[b, :u]
+    local = [sp.local_seeds[b, : counts[0]].long()]
+    offsets = []
+    for h in range(sp.H):
+        local.append(sp.local_nbrs[h][b, : counts[h + 1]].long())
+        offsets.append(sp.offsets[h][b, : counts[h] + 1].long())
+    seeds = sp.seeds[b, : counts[0]].long() & 0xFFFFFFFF
+    return TreeBatch(feats, local, offsets, labels[seeds])
+
+
+def train_step(model: GraphSAGE, opt: torch.optim.Optimizer, batch: TreeBatch) -> torch.Tensor:
+    opt.zero_grad(set_to_none=True)
+    loss = F.cross_entropy(model(batch), batch.labels)
+    loss.backward()
+    opt.step()
+    return loss.detach()
+
+
+def train_epoch(pipe, plan, model: GraphSAGE, opt, labels: torch.Tensor, max_batches: int | None = None) -> list:
+    """Sample the epoch window by window on the device and train on every batch in
+    order; returns the per-batch losses (device scalars)."""
+    losses = []
+
+    def consume(p, w0, nbw):
+        counts = p.sampler.counts[:, :nbw].cpu().numpy()  # one sync per window for the sizes
+        ucount = p.sampler.ucount[:nbw].cpu().numpy()
+        for b in range(nbw):
+            if max_batches is not None and len(losses) >= max_batches:
+                return
+            losses.append(train_step(model, opt, tree_batch_from_window(p, b, labels, counts, ucount)))
+
+    pipe.run_epoch(plan, on_window=consume)
+    return losses
