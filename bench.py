@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--train-epochs", type=int, default=1, help="GraphSAGE epochs timed after the data-path bench")
     return ap.parse_args()
 
 
@@ -375,6 +376,8 @@ def run_b200(args):
         "clocks": clocks.summary(),
     }
 
+    if args.train_epochs > 0:
+        line["graphsage_epoch"] = train_run(args, g, cfg, pipe, pool, root, clique, local_idx, world)
     if not args.no_e2e:
         line["e2e"] = e2e_run(args, g, cfg, store, pool, root, clique, local_idx, world)
     if world > 1:
@@ -389,6 +392,37 @@ def run_b200(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def train_run(args, g, cfg, pipe, pool, root, clique, local_idx, world):
+    """Full GraphSAGE epochs (hidden 256, 47 classes, SGD) on the device-prepared batches:
+    epoch time = sampling + gather + forward/backward/step of every batch (CUDA events)."""
+    import torch
+
+    from paper_2305_16588_b200.distributed import max_over_ranks
+    from paper_2305_16588_b200.train import GraphSAGE, synthetic_labels, train_epoch
+
+    classes = 47
+    torch.manual_seed(0)
+    model = GraphSAGE(CONFIG["feature_dim"], 256, classes, len(cfg.fanouts)).cuda()
+    opt = torch.optim.SGD(model.parameters(), lr=0.1)
+    labels = torch.from_numpy(synthetic_labels(np.arange(g.num_vertices), classes)).cuda()
+    plans = [pipe.plan_epoch(pool, root.derive(1000 + e, clique, local_idx)) for e in range(args.train_epochs + 1)]
+    train_epoch(pipe, plans[0], model, opt, labels, max_batches=8)  # warm-up (allocator, kernels)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    losses = []
+    for e in range(args.train_epochs):
+        losses += train_epoch(pipe, plans[1 + e], model, opt, labels)
+    e1.record()
+    torch.cuda.synchronize()
+    sec = e0.elapsed_time(e1) / 1000.0 / args.train_epochs
+    if world > 1:
+        sec = max_over_ranks(sec)
+    return {"seconds": sec, "batches_per_gpu": len(losses) // args.train_epochs, "epochs": args.train_epochs,
+            "model": "GraphSAGE mean, 3 layers, hidden 256, 47 classes, fp32, SGD",
+            "first_loss": float(losses[0]), "last_loss": float(losses[-1])}
 
 
 def e2e_run(args, g, cfg, store, pool, root, clique, local_idx, world):
