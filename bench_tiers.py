@@ -1,0 +1,140 @@
+"""Three-tier bench: Legion's full flow on a papers100M-shaped graph with a host tier.
+
+BASELINE configs[2] shape (ogbn-papers100M: 111M vertices, degree ~14, 128-d fp32,
+fanouts [25,10], batch 1024, 10% training set), scaled by --scale (default 0.1 so the
+host tables fit a desk-size box; --scale 1 is the full shape). On the device:
+
+  1. presampling epoch (K1/K2/K3/K5)         -> HotnessMatrices, N_TSUM
+  2. CSLP ranking + alpha search (K6/K7)      -> plan, predicted PCIe transactions
+  3. materialize + cache fill (K8)            -> topology slab + feature slab in HBM;
+                                                 everything else stays in pinned host
+                                                 memory, read over PCIe through UVA
+  4. validation epochs through the three tiers (K2 tiered topology, K4 gather)
+
+Reports batches/s through the tiers and measured PCIe bytes per batch next to the
+reference cost model's prediction N_total x CLS / batches (planner.py:142-169).
+
+    python bench_tiers.py [--scale 0.1] [--budget-frac 0.1] [--steps 3]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--scale", type=float, default=0.1)
+    ap.add_argument("--budget-frac", type=float, default=0.1, help="cache budget / (topology + feature bytes)")
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=1)
+    ap.add_argument("--window", type=int, default=256)
+    a = ap.parse_args()
+
+    import torch
+
+    import paper_2305_16588_b200 as P
+    from paper_2305_16588_b200 import planner as PL
+    from paper_2305_16588_b200.cache import FeatureStore, TopologyStore
+    from paper_2305_16588_b200.graph import synthetic_features_device
+    from paper_2305_16588_b200.partition import single_clique_partitioning
+    from paper_2305_16588_b200.pipeline import SampleGatherPipeline, StageTimer
+
+    torch.cuda.set_device(0)
+    t_setup = time.perf_counter()
+    n = int(round(111_000_000 * a.scale))
+    deg, dim, fanouts, bs = 14, 128, (25, 10), 1024
+    g = P.generate_synthetic(n, deg, 1.2, seed=P.derive_seed(7, 1))
+    train = P.select_training_set(g, 0.1, seed=P.derive_seed(7, 2))
+    layout = P.block_layout(1, 1)
+    pools = P.assign_tablets(P.split_intra_clique(train, single_clique_partitioning(g), layout), layout)
+    feat = P.FeatureSpec(dim)
+    total_bytes = g.num_edges * 4 + 8 * n + n * feat.row_bytes
+    budget = int(a.budget_frac * total_bytes)
+    spec = P.HardwareSpec(layout, clique_budget_bytes=budget)
+    cfg = P.SamplingConfig(fanouts=fanouts, batch_size=bs, presample_epochs=1, seed=P.derive_seed(7, 4))
+
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    hot = P.run_presampling(g, pools, layout, cfg, spec)[0]
+    t_pre = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    orders = PL.build_candidate_orders(hot)
+    plan, est = PL.search_optimal_plan(orders, budget, 0.01, g, feat, spec, hot.sampling_txn_total)
+    asg = PL.materialize_assignment([orders], [plan], layout, g, feat, spec)
+    torch.cuda.synchronize()
+    t_plan = time.perf_counter() - t0
+
+    host_table = synthetic_features_device(0, n, dim).cpu().pin_memory()
+    t0 = time.perf_counter()
+    topo = TopologyStore(g, asg.topo_vertices, 0, host_full=True)
+    fstore = FeatureStore.from_assignment(host_table, asg.feat_vertices, 0)
+    torch.cuda.synchronize()
+    t_fill = time.perf_counter() - t0
+    pool = pools[0]
+    nb = math.ceil(len(pool) / bs)
+    pipe = SampleGatherPipeline(g, cfg, fstore, len(pool), window=min(a.window, nb), feat_rows_cap=60_000,
+                                topology=topo)
+    root = P.KeyedRng(P.derive_seed(7, 5))
+    plans = [pipe.plan_epoch(pool, root.derive(e, 0, 0)) for e in range(a.warmup + a.steps)]
+    setup_s = time.perf_counter() - t_setup
+    for e in range(a.warmup):
+        pipe.run_epoch(plans[e])
+    torch.cuda.synchronize()
+    topo.reset_counters()
+    fstore.reset_counters()
+    timer = StageTimer()
+    pipe.timer = timer
+    ms = []
+    for s in range(a.steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        pipe.run_epoch(plans[a.warmup + s])
+        e1.record()
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    t, f = topo.tier_counts(), fstore.tier_counts()
+    batches = nb * a.steps
+    row_txns = PL.feature_row_transactions(feat, spec)
+    cls = spec.cache_line_bytes
+    measured_txn = t["host_txn"] + f["host"] * row_txns
+    pred_txn = est.total_txns
+    stages = {k: v[1] / a.steps for k, v in timer.summary().items()}
+    out = {
+        "metric": "three-tier sampled+gathered batches/s; PCIe GB/batch vs plan prediction",
+        "value": batches / (sum(ms) / 1000.0),
+        "unit": "batches/s",
+        "n_gpus": 1,
+        "steps": a.steps,
+        "config": {"workload": f"C3 ogbn-papers100M-shaped synthetic x{a.scale}", "num_vertices": n,
+                   "num_edges": g.num_edges, "feature_dim": dim, "fanouts": list(fanouts), "batch_size": bs,
+                   "budget_bytes": budget, "budget_frac": a.budget_frac, "batches_per_epoch": nb},
+        "plan": {"alpha": plan.alpha, "topo_prefix_len": est.topo_prefix_len, "feat_prefix_len": est.feat_prefix_len,
+                 "predicted_txn_per_epoch": pred_txn, "presample_txn_total": hot.sampling_txn_total},
+        "pcie": {
+            "measured_gb_per_batch": measured_txn * cls / batches / 1e9,
+            "predicted_gb_per_batch": pred_txn * cls / nb / 1e9,
+            "measured_over_predicted": (measured_txn / batches) / (pred_txn / nb) if pred_txn else None,
+            "payload_gb_per_batch": (t["reads_host"] * 16 + t["edges_host"] * 4 + f["host"] * feat.row_bytes)
+            / batches / 1e9,
+            "unit_note": "transactions x 64 B cache lines, the reference's PCIe unit (SPEC.md:403)",
+        },
+        "tiers_per_batch": {**{k: v / batches for k, v in t.items()}, **{f"rows_{k}": v / batches for k, v in f.items()}},
+        "stages_ms_per_epoch": stages,
+        "setup_s": {"total": setup_s, "presampling": t_pre, "plan": t_plan, "cache_fill": t_fill},
+    }
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()
