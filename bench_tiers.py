@@ -75,7 +75,12 @@ def main():
     torch.cuda.synchronize()
     t_plan = time.perf_counter() - t0
 
-    host_table = synthetic_features_device(0, n, dim).cpu().pin_memory()
+    # host tier: the whole fp32 table in pinned, mapped memory (filled from the device)
+    host_table = torch.empty((n, dim), dtype=torch.float32, pin_memory=True)
+    step = 1 << 24
+    for r0 in range(0, n, step):
+        rows = min(step, n - r0)
+        host_table[r0 : r0 + rows].copy_(synthetic_features_device(r0, rows, dim))
     t0 = time.perf_counter()
     topo = TopologyStore(g, asg.topo_vertices, 0, host_full=True)
     fstore = FeatureStore.from_assignment(host_table, asg.feat_vertices, 0)
