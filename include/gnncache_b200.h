@@ -122,6 +122,18 @@ typedef struct gc_hotness {
     uint32_t uint32_bytes;     /* HardwareSpec.uint32_bytes (hardware.py:168) */
 } gc_hotness_t;
 
+/* Per-batch visited sets of a window (the dedup state, K3). `bitmap` holds one bit per
+ * vertex, `words` u32 per batch (gc_bitmap_words). The optional `summary` holds one bit
+ * per 32-word block (1024 vertices), set when a block's first bit is set, so
+ * compaction touches only non-empty blocks: O(distinct + n/1024) per batch instead of
+ * O(n/32) — what makes 100M-vertex graphs cheap. summary_words = gc_summary_words(n). */
+typedef struct gc_visited {
+    uint32_t* bitmap;
+    uint64_t words;
+    uint32_t* summary;
+    uint64_t summary_words;
+} gc_visited_t;
+
 /* ------------------------------------------- K2: hop expansion (sampling.py:84-143) */
 
 /* One hop of _expand_frontier (sampling.py:84-117) for W batches at once.
@@ -129,8 +141,8 @@ typedef struct gc_hotness {
  *  hop key of batch b : d_hop_keys[b] = stream.derive(h).key (sampling.py:135)
  *  output offsets     : d_out_offsets + b*offsets_stride, count+1 entries (u32, exclusive scan of take)
  *  output neighbors   : d_out_nbrs + b*nbrs_stride, d_out_count[b] entries
- *  d_bitmap (optional): per-batch visited bitmap (bitmap_words u32 words per batch); every
- *                       emitted neighbor is marked, and the frontier too if mark_frontier.
+ *  visited (optional)  : per-batch visited sets; every emitted neighbour is marked, and
+ *                       the frontier too if mark_frontier.
  *  hot (optional)     : presampling counters of the sampling GPU.
  * Neighbour lists come from the topology tier that holds them (gc_topology_t).
  * Selection is bit-exact with the reference: deg<=fanout copies the CSR slice in order,
@@ -141,20 +153,22 @@ int gc_hop_expand(const gc_topology_t* topo, const uint32_t* d_frontier, uint64_
                   const uint32_t* d_frontier_count, uint32_t max_frontier, uint32_t fanout,
                   const uint64_t* d_hop_keys, uint32_t num_batches, uint32_t* d_out_offsets,
                   uint64_t offsets_stride, uint32_t* d_out_nbrs, uint64_t nbrs_stride, uint32_t* d_out_count,
-                  uint32_t* d_bitmap, uint64_t bitmap_words, int mark_frontier, const gc_hotness_t* hot,
+                  const gc_visited_t* visited, int mark_frontier, const gc_hotness_t* hot,
                   void* d_temp, size_t temp_bytes, void* stream);
 
 /* ------------------------------- K3: dedup + relabel (BatchSample.distinct_vertices) */
 
 /* Words per batch bitmap for n vertices (padded for 16-byte vector access). */
 uint64_t gc_bitmap_words(int64_t num_vertices);
+/* Words per batch of the block summary (one bit per 32 bitmap words). */
+uint64_t gc_summary_words(int64_t num_vertices);
 /* np.unique of seeds ∪ all hop neighbors (sampling.py:73-75) from the visited bitmaps:
  * sorted distinct ids of batch b -> d_unique + b*unique_stride, count -> d_unique_count[b];
  * d_rank_table (optional, 2*bitmap_words u32 per batch) receives {exclusive popcount
  * prefix, bitmap word} per word for gc_relabel. feat_lookups (optional) += 1 per
  * distinct id (sampling.py:242). clear_bitmap zeroes the bitmap as it is consumed. */
-size_t gc_unique_temp_bytes(uint32_t num_batches, uint64_t bitmap_words);
-int gc_unique_compact(uint32_t* d_bitmap, uint64_t bitmap_words, uint32_t num_batches, uint32_t* d_unique,
+size_t gc_unique_temp_bytes(uint32_t num_batches, const gc_visited_t* visited);
+int gc_unique_compact(const gc_visited_t* visited, uint32_t num_batches, uint32_t* d_unique,
                       uint64_t unique_stride, uint32_t* d_unique_count, uint32_t* d_rank_table,
                       uint64_t* d_feat_lookups, int clear_bitmap, void* d_temp, size_t temp_bytes,
                       void* stream);
@@ -163,11 +177,11 @@ int gc_unique_compact(uint32_t* d_bitmap, uint64_t bitmap_words, uint32_t num_ba
 int gc_relabel(const uint32_t* d_ids, uint64_t ids_stride, const uint32_t* d_ids_count, uint32_t max_count,
                uint32_t num_batches, const uint32_t* d_rank_table, uint64_t bitmap_words, uint32_t* d_local,
                void* stream);
-/* Mark ids in the per-batch visited bitmaps (seeds of a zero-hop config). */
+/* Mark ids in the per-batch visited sets (seeds of a zero-hop config). */
 int gc_mark_visited(const uint32_t* d_ids, uint64_t ids_stride, const uint32_t* d_count, uint32_t max_count,
-                    uint32_t num_batches, uint32_t* d_bitmap, uint64_t bitmap_words, void* stream);
-/* Zero the bitmap words touched by batch b's unique ids (cheap reset for the next window). */
-int gc_bitmap_clear(uint32_t* d_bitmap, uint64_t bitmap_words, uint32_t num_batches, const uint32_t* d_unique,
+                    uint32_t num_batches, const gc_visited_t* visited, void* stream);
+/* Zero the visited words touched by batch b's unique ids (reset after clear_bitmap=0). */
+int gc_bitmap_clear(const gc_visited_t* visited, uint32_t num_batches, const uint32_t* d_unique,
                     uint64_t unique_stride, const uint32_t* d_unique_count, uint32_t max_unique, void* stream);
 
 /* ------------------------------------------------ K4: three-tier feature gather */

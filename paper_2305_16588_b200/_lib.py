@@ -50,6 +50,15 @@ class GcTopology(ctypes.Structure):
     ]
 
 
+class GcVisited(ctypes.Structure):
+    _fields_ = [
+        ("bitmap", ctypes.c_void_p),
+        ("words", ctypes.c_uint64),
+        ("summary", ctypes.c_void_p),
+        ("summary_words", ctypes.c_uint64),
+    ]
+
+
 class GcHotness(ctypes.Structure):
     _fields_ = [
         ("topo_reads", ctypes.c_void_p),
@@ -95,17 +104,18 @@ SIGNATURES = {
     "gc_hop_expand_temp_bytes": (SZ, [U32, U32]),
     "gc_hop_expand": (
         ctypes.c_int,
-        [ctypes.POINTER(GcTopology), V, U64, V, U32, U32, V, U32, V, U64, V, U64, V, V, U64, ctypes.c_int,
-         ctypes.POINTER(GcHotness), V, SZ, V],
+        [ctypes.POINTER(GcTopology), V, U64, V, U32, U32, V, U32, V, U64, V, U64, V, ctypes.POINTER(GcVisited),
+         ctypes.c_int, ctypes.POINTER(GcHotness), V, SZ, V],
     ),
     "gc_csr_extract": (ctypes.c_int, [ctypes.POINTER(GcCsr), V, I64, V, V, V]),
     "gc_bitmap_words": (U64, [I64]),
-    "gc_unique_temp_bytes": (SZ, [U32, U64]),
-    "gc_unique_compact": (ctypes.c_int, [V, U64, U32, V, U64, V, V, V, ctypes.c_int, V, SZ, V]),
+    "gc_summary_words": (U64, [I64]),
+    "gc_unique_temp_bytes": (SZ, [U32, ctypes.POINTER(GcVisited)]),
+    "gc_unique_compact": (ctypes.c_int, [ctypes.POINTER(GcVisited), U32, V, U64, V, V, V, ctypes.c_int, V, SZ, V]),
     "gc_relabel": (ctypes.c_int, [V, U64, V, U32, U32, V, U64, V, V]),
-    "gc_mark_visited": (ctypes.c_int, [V, U64, V, U32, U32, V, U64, V]),
+    "gc_mark_visited": (ctypes.c_int, [V, U64, V, U32, U32, ctypes.POINTER(GcVisited), V]),
     "gc_synth_features": (ctypes.c_int, [U64, U64, U32, V, V]),
-    "gc_bitmap_clear": (ctypes.c_int, [V, U64, U32, V, U64, V, U32, V]),
+    "gc_bitmap_clear": (ctypes.c_int, [ctypes.POINTER(GcVisited), U32, V, U64, V, U32, V]),
     "gc_gather": (ctypes.c_int, [ctypes.POINTER(GcFeatureStore), V, U64, V, U32, U32, V, U64, V, V]),
     "gc_scatter_add": (ctypes.c_int, [V, V, I64, V, V]),
     "gc_colsum_argmax": (ctypes.c_int, [V, U32, I64, V, V, V]),

@@ -83,6 +83,24 @@ struct PairHashHigh {
     }
 };
 
+// Mark vertex u in one batch's visited set. Bits only go 0 -> 1 inside a launch, so
+// a stale cached read costs at most a redundant atomic, never a missed mark. With a
+// block summary, the one thread whose atomic turns a word non-zero flags the word's
+// 32-word block (1024 vertices) for the sparse compaction.
+__device__ __forceinline__ void mark_visited(uint32_t* bm, uint32_t* sm, uint32_t u) {
+    uint32_t* w = bm + (u >> 5);
+    const uint32_t bit = 1u << (u & 31);
+    if (*w & bit) return;
+    if (sm == nullptr) {
+        atomicOr(w, bit);
+        return;
+    }
+    if (atomicOr(w, bit) == 0u) {
+        const uint32_t blk = u >> 10;
+        atomicOr(sm + (blk >> 5), 1u << (blk & 31));
+    }
+}
+
 void set_error(const std::string& msg);
 int cuda_status(cudaError_t err, const char* what);
 

@@ -17,6 +17,8 @@ constexpr int kWordsPerTile = kUniqThreads * kWordsPerThread;
 struct UniqueParams {
     uint32_t* bm;
     uint64_t bwords;
+    uint32_t* sm;
+    uint64_t swords;
     uint32_t tiles_per_batch;
     uint32_t* uniq;
     uint64_t ustride;
@@ -79,6 +81,91 @@ __global__ void __launch_bounds__(kUniqThreads) k_unique(UniqueParams p) {
     if (t == p.tiles_per_batch - 1 && tid == kUniqThreads - 1) p.ucount[b] = (uint32_t)s_prefix + excl + c0 + c1 + c2 + c3;
 }
 
+// Sparse compaction: one warp per summary word (32 blocks of 32 bitmap words); lane i
+// tallies block i. Pass 1 counts the set bits of each non-empty block (one coalesced
+// 128-byte load per block), a CTA scan + decoupled look-back give the batch-level
+// offset of the tile, pass 2 reloads the blocks and emits ids in ascending order,
+// rank-table entries for non-empty words, and clears what it consumed.
+constexpr int kSparseWarps = kUniqThreads / 32;  // summary words per tile
+
+__device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, uint32_t& total) {
+    const int lane = threadIdx.x & 31;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+    }
+    total = __shfl_sync(kFull, x, 31);
+    return x - v;
+}
+
+__global__ void __launch_bounds__(kUniqThreads) k_unique_sparse(UniqueParams p) {
+    __shared__ uint32_t s_vid;
+    __shared__ uint32_t s_warp[kSparseWarps];
+    __shared__ uint64_t s_prefix;
+    __shared__ uint32_t s_total;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_vid = atomicAdd(p.tile_counter, 1u);
+    __syncthreads();
+    const uint32_t b = s_vid / p.tiles_per_batch;
+    const uint32_t t = s_vid % p.tiles_per_batch;
+    const uint64_t sw = (uint64_t)t * kSparseWarps + warp;
+    uint32_t* row = p.bm + b * p.bwords;
+    uint32_t* srow = p.sm + b * p.swords;
+    const uint32_t s = sw < p.swords ? srow[sw] : 0u;
+    // pass 1: lane i holds the population of block i of this summary word
+    uint32_t my_cnt = 0;
+    for (uint32_t m = s; m; m &= m - 1u) {
+        const int i = __ffs(m) - 1;
+        const uint64_t wi = (sw * 32 + i) * 32 + lane;
+        const uint32_t x = wi < p.bwords ? row[wi] : 0u;
+        const uint32_t c = __reduce_add_sync(kFull, (uint32_t)__popc(x));
+        if (lane == i) my_cnt = c;
+    }
+    uint32_t warp_total;
+    const uint32_t blk_excl = warp_excl_scan(my_cnt, warp_total);
+    if (lane == 0) s_warp[warp] = warp_total;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t v = lane < kSparseWarps ? s_warp[lane] : 0u;
+        uint32_t tile_total;
+        const uint32_t ex = warp_excl_scan(v, tile_total);
+        if (lane < kSparseWarps) s_warp[lane] = ex;
+        const uint64_t sidx = (uint64_t)b * p.tiles_per_batch + t;
+        if (lane == 0 && t != 0) publish(p.tile_state + sidx, kFlagAgg | tile_total);
+        const uint64_t pre = lookback_warp(p.tile_state, (uint64_t)b * p.tiles_per_batch, sidx, tile_total);
+        if (lane == 0) {
+            s_prefix = pre;
+            s_total = tile_total;
+        }
+    }
+    __syncthreads();
+    const uint32_t warp_base = (uint32_t)s_prefix + s_warp[warp];
+    uint32_t* out = p.uniq + b * p.ustride;
+    // pass 2: emission in ascending vertex order
+    for (uint32_t m = s; m; m &= m - 1u) {
+        const int i = __ffs(m) - 1;
+        const uint32_t blk_base = warp_base + __shfl_sync(kFull, blk_excl, i);
+        const uint64_t wi = (sw * 32 + i) * 32 + lane;
+        const uint32_t x = wi < p.bwords ? row[wi] : 0u;
+        uint32_t dummy;
+        uint32_t pos = blk_base + warp_excl_scan((uint32_t)__popc(x), dummy);
+        if (x) {
+            if (p.rank) p.rank[b * p.bwords + wi] = make_uint2(pos, x);
+            const uint32_t vbase = (uint32_t)(wi * 32);
+            for (uint32_t w = x; w; w &= w - 1u) {
+                const uint32_t u = vbase + (__ffs(w) - 1);
+                out[pos++] = u;
+                if (p.feat) atomicAdd((unsigned long long*)(p.feat + u), 1ull);
+            }
+            if (p.clear) row[wi] = 0u;
+        }
+    }
+    if (p.clear && lane == 0 && s) srow[sw] = 0u;
+    if (t == p.tiles_per_batch - 1 && tid == 0) p.ucount[b] = (uint32_t)s_prefix + s_total;
+}
+
 __device__ __forceinline__ uint32_t rank_of(const uint2* __restrict__ rt, uint32_t u) {
     const uint2 e = __ldg(rt + (u >> 5));
     return e.x + __popc(e.y & ((1u << (u & 31)) - 1u));
@@ -113,28 +200,31 @@ __global__ void k_relabel(const uint32_t* __restrict__ ids, uint64_t stride, con
     }
 }
 
-__global__ void k_bitmap_clear(uint32_t* bm, uint64_t bwords, const uint32_t* __restrict__ uniq, uint64_t ustride,
-                               const uint32_t* __restrict__ ucount) {
+__global__ void k_bitmap_clear(uint32_t* bm, uint64_t bwords, uint32_t* sm, uint64_t swords,
+                               const uint32_t* __restrict__ uniq, uint64_t ustride, const uint32_t* __restrict__ ucount) {
     const uint32_t b = blockIdx.y;
     const uint32_t c = ucount[b];
     uint32_t* row = bm + b * bwords;
-    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < c; k += gridDim.x * blockDim.x)
-        row[uniq[b * ustride + k] >> 5] = 0u;
-}
-
-__global__ void k_mark(const uint32_t* __restrict__ ids, uint64_t stride, const uint32_t* __restrict__ count,
-                       uint32_t* bm, uint64_t bwords) {
-    const uint32_t b = blockIdx.y;
-    const uint32_t c = count[b];
-    uint32_t* row = bm + b * bwords;
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < c; k += gridDim.x * blockDim.x) {
-        const uint32_t u = ids[b * stride + k];
-        atomicOr(row + (u >> 5), 1u << (u & 31));
+        const uint32_t u = uniq[b * ustride + k];
+        row[u >> 5] = 0u;
+        if (sm) sm[b * swords + (u >> 15)] = 0u;
     }
 }
 
-static unsigned uniq_tiles(uint64_t bwords) {
-    uint64_t t = (bwords + kWordsPerTile - 1) / kWordsPerTile;
+__global__ void k_mark(const uint32_t* __restrict__ ids, uint64_t stride, const uint32_t* __restrict__ count,
+                       uint32_t* bm, uint64_t bwords, uint32_t* sm, uint64_t swords) {
+    const uint32_t b = blockIdx.y;
+    const uint32_t c = count[b];
+    uint32_t* row = bm + b * bwords;
+    uint32_t* srow = sm ? sm + b * swords : nullptr;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < c; k += gridDim.x * blockDim.x)
+        mark_visited(row, srow, ids[b * stride + k]);
+}
+
+static unsigned uniq_tiles(const gc_visited_t* v) {
+    uint64_t t = v->summary ? (v->summary_words + kSparseWarps - 1) / kSparseWarps
+                            : (v->words + kWordsPerTile - 1) / kWordsPerTile;
     return t ? (unsigned)t : 1u;
 }
 
@@ -156,24 +246,35 @@ uint64_t gc_bitmap_words(int64_t num_vertices) {
     return (w + 3) / 4 * 4;
 }
 
-size_t gc_unique_temp_bytes(uint32_t num_batches, uint64_t bitmap_words) {
-    return align_up((size_t)num_batches * uniq_tiles(bitmap_words) * sizeof(uint64_t), 256) + 256;
+uint64_t gc_summary_words(int64_t num_vertices) {
+    const uint64_t blocks = (gc_bitmap_words(num_vertices) + 31) / 32;
+    return ((blocks + 31) / 32 + 3) / 4 * 4;
 }
 
-int gc_unique_compact(uint32_t* d_bitmap, uint64_t bitmap_words, uint32_t num_batches, uint32_t* d_unique,
+size_t gc_unique_temp_bytes(uint32_t num_batches, const gc_visited_t* visited) {
+    if (!visited) return 0;
+    return align_up((size_t)num_batches * uniq_tiles(visited) * sizeof(uint64_t), 256) + 256;
+}
+
+int gc_unique_compact(const gc_visited_t* visited, uint32_t num_batches, uint32_t* d_unique,
                       uint64_t unique_stride, uint32_t* d_unique_count, uint32_t* d_rank_table,
                       uint64_t* d_feat_lookups, int clear_bitmap, void* d_temp, size_t temp_bytes,
                       void* stream) {
-    GC_REQUIRE(bitmap_words % 4 == 0, GC_ERR_VALUE, "gc_unique_compact: bitmap_words must be a multiple of 4");
+    GC_REQUIRE(visited && visited->bitmap, GC_ERR_VALUE, "gc_unique_compact: visited set is null");
+    GC_REQUIRE(visited->words % 4 == 0, GC_ERR_VALUE, "gc_unique_compact: bitmap words must be a multiple of 4");
+    GC_REQUIRE(!visited->summary || visited->summary_words * 32 * 32 >= visited->words, GC_ERR_VALUE,
+               "gc_unique_compact: summary too small for the bitmap");
     if (num_batches == 0) return GC_OK;
-    const size_t need = gc_unique_temp_bytes(num_batches, bitmap_words);
+    const size_t need = gc_unique_temp_bytes(num_batches, visited);
     GC_REQUIRE(d_temp && temp_bytes >= need, GC_ERR_VALUE, "gc_unique_compact: temp buffer too small");
     cudaStream_t s = as_stream(stream);
-    const unsigned tiles = uniq_tiles(bitmap_words);
+    const unsigned tiles = uniq_tiles(visited);
     const size_t state_bytes = align_up((size_t)num_batches * tiles * sizeof(uint64_t), 256);
     UniqueParams p{};
-    p.bm = d_bitmap;
-    p.bwords = bitmap_words;
+    p.bm = visited->bitmap;
+    p.bwords = visited->words;
+    p.sm = visited->summary;
+    p.swords = visited->summary_words;
     p.tiles_per_batch = tiles;
     p.uniq = d_unique;
     p.ustride = unique_stride;
@@ -186,7 +287,10 @@ int gc_unique_compact(uint32_t* d_bitmap, uint64_t bitmap_words, uint32_t num_ba
     GC_TRY(cudaMemsetAsync(d_temp, 0, state_bytes + 256, s), "gc_unique_compact memset");
     const uint64_t grid = (uint64_t)num_batches * tiles;
     GC_REQUIRE(grid < (1ull << 31), GC_ERR_VALUE, "gc_unique_compact: window too large");
-    k_unique<<<(unsigned)grid, kUniqThreads, 0, s>>>(p);
+    if (p.sm)
+        k_unique_sparse<<<(unsigned)grid, kUniqThreads, 0, s>>>(p);
+    else
+        k_unique<<<(unsigned)grid, kUniqThreads, 0, s>>>(p);
     GC_CHECK_LAUNCH("gc_unique_compact");
     return GC_OK;
 }
@@ -210,21 +314,25 @@ int gc_relabel(const uint32_t* d_ids, uint64_t ids_stride, const uint32_t* d_ids
 }
 
 int gc_mark_visited(const uint32_t* d_ids, uint64_t ids_stride, const uint32_t* d_count, uint32_t max_count,
-                    uint32_t num_batches, uint32_t* d_bitmap, uint64_t bitmap_words, void* stream) {
+                    uint32_t num_batches, const gc_visited_t* visited, void* stream) {
+    GC_REQUIRE(visited && visited->bitmap, GC_ERR_VALUE, "gc_mark_visited: visited set is null");
     GC_REQUIRE(num_batches < 65536, GC_ERR_VALUE, "gc_mark_visited: at most 65535 batches per call");
     if (num_batches == 0 || max_count == 0) return GC_OK;
     dim3 grid(grid_x(max_count, 256), num_batches);
-    k_mark<<<grid, 256, 0, as_stream(stream)>>>(d_ids, ids_stride, d_count, d_bitmap, bitmap_words);
+    k_mark<<<grid, 256, 0, as_stream(stream)>>>(d_ids, ids_stride, d_count, visited->bitmap, visited->words,
+                                                visited->summary, visited->summary_words);
     GC_CHECK_LAUNCH("gc_mark_visited");
     return GC_OK;
 }
 
-int gc_bitmap_clear(uint32_t* d_bitmap, uint64_t bitmap_words, uint32_t num_batches, const uint32_t* d_unique,
+int gc_bitmap_clear(const gc_visited_t* visited, uint32_t num_batches, const uint32_t* d_unique,
                     uint64_t unique_stride, const uint32_t* d_unique_count, uint32_t max_unique, void* stream) {
+    GC_REQUIRE(visited && visited->bitmap, GC_ERR_VALUE, "gc_bitmap_clear: visited set is null");
     GC_REQUIRE(num_batches < 65536, GC_ERR_VALUE, "gc_bitmap_clear: at most 65535 batches per call");
     if (num_batches == 0 || max_unique == 0) return GC_OK;
     dim3 grid(grid_x(max_unique, 256), num_batches);
-    k_bitmap_clear<<<grid, 256, 0, as_stream(stream)>>>(d_bitmap, bitmap_words, d_unique, unique_stride,
+    k_bitmap_clear<<<grid, 256, 0, as_stream(stream)>>>(visited->bitmap, visited->words, visited->summary,
+                                                        visited->summary_words, d_unique, unique_stride,
                                                         d_unique_count);
     GC_CHECK_LAUNCH("gc_bitmap_clear");
     return GC_OK;

@@ -52,6 +52,8 @@ struct HopParams {
     uint32_t* out_count;
     uint32_t* bitmap;
     uint64_t bwords;
+    uint32_t* summary;
+    uint64_t swords;
     int mark_frontier;
     uint64_t* topo_reads;
     uint64_t* edge_trav;
@@ -64,14 +66,6 @@ struct HopParams {
 };
 
 static int g_exact_only = 0;
-
-__device__ __forceinline__ void mark_visited(uint32_t* bm, uint32_t u) {
-    uint32_t* w = bm + (u >> 5);
-    uint32_t bit = 1u << (u & 31);
-    // bits only go 0 -> 1 inside a launch, so a stale cached read can only cost a
-    // redundant atomic, never a missed mark
-    if (!(*w & bit)) atomicOr(w, bit);
-}
 
 __device__ __forceinline__ void stage(uint64_t* s_items, uint32_t item, uint32_t r0, uint32_t r1, uint64_t edge) {
     if (item >= r0 && item < r1) s_items[item - r0] = edge;
@@ -347,7 +341,8 @@ __global__ void __launch_bounds__(kHopThreads, (S > 0 && S <= 16) ? 5 : 1) k_hop
             }
         }
         take = min(deg, p.fanout);
-        if (p.mark_frontier && p.bitmap) mark_visited(p.bitmap + b * p.bwords, v);
+        if (p.mark_frontier && p.bitmap)
+            mark_visited(p.bitmap + b * p.bwords, p.summary ? p.summary + b * p.swords : nullptr, v);
         // hash_counters(position), position = index in this batch's frontier (rng.py:64-66)
         if (deg > p.fanout) hc = hash_counter(p.hop_keys[b], p0 + tid);
     }
@@ -398,6 +393,7 @@ __global__ void __launch_bounds__(kHopThreads, (S > 0 && S <= 16) ? 5 : 1) k_hop
 
     uint32_t* out = p.out_nbrs + b * p.nstride;
     uint32_t* bm = p.bitmap ? p.bitmap + b * p.bwords : nullptr;
+    uint32_t* sm = p.summary ? p.summary + b * p.swords : nullptr;
     const uint32_t rounds = (total + kItemCap - 1) / kItemCap;
     const bool thread_copy = deg <= p.fanout && deg <= 64;
     const bool thread_choice = S > 0 && !p.exact_only && deg > p.fanout && deg <= 64 && p.fanout < (uint32_t)S;
@@ -461,7 +457,7 @@ __global__ void __launch_bounds__(kHopThreads, (S > 0 && S <= 16) ? 5 : 1) k_hop
             const uint32_t* cols = code ? p.scols[code - 1] : p.ci;
             uint32_t u = __ldg(cols + (it & kEdgeMask));
             dst[k] = u;
-            if (bm) mark_visited(bm, u);
+            if (bm) mark_visited(bm, sm, u);
         }
         __syncthreads();
     }
@@ -507,7 +503,7 @@ int gc_hop_expand(const gc_topology_t* topo, const uint32_t* d_frontier, uint64_
                   const uint32_t* d_frontier_count, uint32_t max_frontier, uint32_t fanout,
                   const uint64_t* d_hop_keys, uint32_t num_batches, uint32_t* d_out_offsets,
                   uint64_t offsets_stride, uint32_t* d_out_nbrs, uint64_t nbrs_stride, uint32_t* d_out_count,
-                  uint32_t* d_bitmap, uint64_t bitmap_words, int mark_frontier, const gc_hotness_t* hot,
+                  const gc_visited_t* visited, int mark_frontier, const gc_hotness_t* hot,
                   void* d_temp, size_t temp_bytes, void* stream) {
     GC_REQUIRE(topo && topo->full.row_offsets, GC_ERR_VALUE, "gc_hop_expand: topology is null");
     const gc_csr_t* graph = &topo->full;
@@ -546,8 +542,12 @@ int gc_hop_expand(const gc_topology_t* topo, const uint32_t* d_frontier, uint64_
     p.out_nbrs = d_out_nbrs;
     p.nstride = nbrs_stride;
     p.out_count = d_out_count;
-    p.bitmap = d_bitmap;
-    p.bwords = bitmap_words;
+    if (visited) {
+        p.bitmap = visited->bitmap;
+        p.bwords = visited->words;
+        p.summary = visited->summary;
+        p.swords = visited->summary_words;
+    }
     p.mark_frontier = mark_frontier;
     p.exact_only = g_exact_only;
     p.cls = 64;

@@ -63,7 +63,7 @@ class SampleGatherPipeline:
 
     def __init__(self, graph: CsrGraph, cfg: SamplingConfig, store: FeatureStore | None, max_pool: int,
                  window: int | None = None, relabel: bool = True, feat_rows_cap: int | None = None,
-                 placement: str = "hbm", topology=None):
+                 placement: str = "hbm", topology=None, sparse_visited: bool | None = None):
         self.graph = graph
         self.cfg = cfg
         self.store = store
@@ -71,7 +71,7 @@ class SampleGatherPipeline:
         nb = max(1, math.ceil(max_pool / B))
         self.window = min(nb, window or nb)
         self.sampler = WindowSampler(graph, cfg.fanouts, B, self.window, placement=placement, relabel=relabel,
-                                     unique_cap=feat_rows_cap, topology=topology)
+                                     unique_cap=feat_rows_cap, topology=topology, sparse_visited=sparse_visited)
         self.feat_cap = self.sampler.ucap
         self.features = None
         if store is not None:

@@ -155,8 +155,12 @@ class WindowSampler:
     between hops, sampling.py:123-125).
     """
 
+    # above this many vertices the visited sets carry a block summary (sparse compaction)
+    SPARSE_VISITED_MIN_VERTICES = 1 << 22
+
     def __init__(self, graph: CsrGraph, fanouts, batch_size: int, window: int, *, placement: str = "hbm",
-                 relabel: bool = False, unique_cap: int | None = None, topology=None):
+                 relabel: bool = False, unique_cap: int | None = None, topology=None,
+                 sparse_visited: bool | None = None):
         self.lib = _lib.lib()
         self.graph = graph
         # topology: a cache.TopologyStore (tiered lists) or the plain CSR in `placement`
@@ -183,6 +187,11 @@ class WindowSampler:
         self.keys = torch.zeros((self.H, W), dtype=torch.int64, device=dev)
         self.words = int(self.lib.gc_bitmap_words(self.n))
         self.bitmap = torch.zeros((W, self.words), dtype=i32, device=dev)
+        if sparse_visited is None:
+            sparse_visited = self.n >= self.SPARSE_VISITED_MIN_VERTICES
+        self.swords = int(self.lib.gc_summary_words(self.n)) if sparse_visited else 0
+        self.summary = torch.zeros((W, self.swords), dtype=i32, device=dev) if sparse_visited else None
+        self.visited = _lib.GcVisited(self.bitmap.data_ptr(), self.words, _lib.ptr(self.summary), self.swords)
         bound = min(self.n, sum(caps))
         self.ucap = max(1, bound if unique_cap is None else min(bound, int(unique_cap)))
         self.unique = torch.empty((W, self.ucap), dtype=i32, device=dev)
@@ -193,7 +202,7 @@ class WindowSampler:
         self.local_nbrs = [torch.empty_like(t) for t in self.nbrs] if relabel else None
         hop_tmp = max([self.lib.gc_hop_expand_temp_bytes(W, caps[h]) for h in range(self.H)] + [256])
         self.hop_tmp = torch.empty(hop_tmp, dtype=torch.uint8, device=dev)
-        uq_tmp = self.lib.gc_unique_temp_bytes(W, self.words)
+        uq_tmp = self.lib.gc_unique_temp_bytes(W, self.visited)
         self.uq_tmp = torch.empty(uq_tmp, dtype=torch.uint8, device=dev)
         self.active = 0
 
@@ -227,7 +236,7 @@ class WindowSampler:
                     self.topo_struct, front.data_ptr(), front.shape[1], self.counts[h].data_ptr(), self.caps[h], f,
                     self.keys[h].data_ptr(), nb, self.offsets[h].data_ptr(), self.offsets[h].shape[1],
                     self.nbrs[h].data_ptr(), self.nbrs[h].shape[1], self.counts[h + 1].data_ptr(),
-                    self.bitmap.data_ptr(), self.words, 1 if h == 0 else 0, hp,
+                    self.visited, 1 if h == 0 else 0, hp,
                     self.hop_tmp.data_ptr(), self.hop_tmp.numel(), s,
                 ),
                 "hop_expand",
@@ -237,7 +246,7 @@ class WindowSampler:
         if self.H == 0:
             _lib.check(
                 self.lib.gc_mark_visited(self.seeds.data_ptr(), self.B, self.counts[0].data_ptr(), self.B, nb,
-                                         self.bitmap.data_ptr(), self.words, s),
+                                         self.visited, s),
                 "mark_visited",
             )
 
@@ -247,7 +256,7 @@ class WindowSampler:
         s = _lib.stream_handle(stream)
         _lib.check(
             self.lib.gc_unique_compact(
-                self.bitmap.data_ptr(), self.words, self.active, self.unique.data_ptr(), self.ucap,
+                self.visited, self.active, self.unique.data_ptr(), self.ucap,
                 self.ucount.data_ptr(), _lib.ptr(self.rank), hot.feat_lookups.data_ptr() if hot else None,
                 1, self.uq_tmp.data_ptr(), self.uq_tmp.numel(), s,
             ),
@@ -294,16 +303,19 @@ def device_unique(ids: np.ndarray, n: int) -> np.ndarray:
     """np.unique of one id list through the bitmap dedup kernels."""
     lib = _lib.lib()
     words = int(lib.gc_bitmap_words(n))
+    swords = int(lib.gc_summary_words(n))
     d_ids = torch.from_numpy(ids.astype(np.uint32).view(np.int32)).cuda()
     cnt = torch.tensor([len(ids)], dtype=torch.int32, device="cuda")
     bm = torch.zeros(words, dtype=torch.int32, device="cuda")
+    sm = torch.zeros(swords, dtype=torch.int32, device="cuda")
+    vis = _lib.GcVisited(bm.data_ptr(), words, sm.data_ptr(), swords)
     s = _lib.stream_handle()
-    _lib.check(lib.gc_mark_visited(d_ids.data_ptr(), len(ids), cnt.data_ptr(), len(ids), 1, bm.data_ptr(), words, s))
+    _lib.check(lib.gc_mark_visited(d_ids.data_ptr(), len(ids), cnt.data_ptr(), len(ids), 1, vis, s))
     cap = min(n, len(ids))
     uniq = torch.empty(max(cap, 1), dtype=torch.int32, device="cuda")
     ucnt = torch.zeros(1, dtype=torch.int32, device="cuda")
-    tmp = torch.empty(lib.gc_unique_temp_bytes(1, words), dtype=torch.uint8, device="cuda")
-    _lib.check(lib.gc_unique_compact(bm.data_ptr(), words, 1, uniq.data_ptr(), cap, ucnt.data_ptr(), None, None, 1,
+    tmp = torch.empty(lib.gc_unique_temp_bytes(1, vis), dtype=torch.uint8, device="cuda")
+    _lib.check(lib.gc_unique_compact(vis, 1, uniq.data_ptr(), cap, ucnt.data_ptr(), None, None, 1,
                                      tmp.data_ptr(), tmp.numel(), s))
     return uniq[: int(ucnt.item())].cpu().numpy().view(np.uint32).astype(np.int64)
 
@@ -412,7 +424,8 @@ def _window_for(sampler_caps: list[int], words: int, num_batches: int, budget_by
 class EpochRunner:
     """Local shuffle + windowed sampling of one GPU's pool for one epoch (sampling.py:224-243)."""
 
-    def __init__(self, graph: CsrGraph, cfg: SamplingConfig, max_pool: int, placement: str = "hbm"):
+    def __init__(self, graph: CsrGraph, cfg: SamplingConfig, max_pool: int, placement: str = "hbm",
+                 sparse_visited: bool | None = None):
         self.graph = graph
         self.cfg = cfg
         lib = _lib.lib()
@@ -422,7 +435,8 @@ class EpochRunner:
         words = int(lib.gc_bitmap_words(graph.num_vertices))
         nb = max(1, math.ceil(max_pool / cfg.batch_size))
         self.window = _window_for(caps, words, nb)
-        self.sampler = WindowSampler(graph, cfg.fanouts, cfg.batch_size, self.window, placement=placement)
+        self.sampler = WindowSampler(graph, cfg.fanouts, cfg.batch_size, self.window, placement=placement,
+                                     sparse_visited=sparse_visited)
 
     def run(self, pool: np.ndarray, gpu_stream: KeyedRng, hot: DeviceHotness) -> int:
         B = self.cfg.batch_size

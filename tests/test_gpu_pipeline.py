@@ -18,9 +18,10 @@ def _device():
     torch.cuda.set_device(0)
 
 
+@pytest.mark.parametrize("sparse", [False, True])
 @pytest.mark.parametrize("window,batch,fanouts,deg", [(0, 256, (15, 10, 5), 26), (3, 100, (25, 10), 14),
                                                        (2, 77, (4, 4), 40), (5, 64, (3,), 200)])
-def test_epoch_windows_match_oracle(window, batch, fanouts, deg):
+def test_epoch_windows_match_oracle(window, batch, fanouts, deg, sparse):
     import paper_2305_16588_b200 as P
     from paper_2305_16588_b200.cache import FeatureStore
     from paper_2305_16588_b200.graph import synthetic_features_device
@@ -31,7 +32,7 @@ def test_epoch_windows_match_oracle(window, batch, fanouts, deg):
     pool = np.sort(np.random.default_rng(1).choice(n, 1500, replace=False)).astype(np.int64)
     cfg = P.SamplingConfig(fanouts=fanouts, batch_size=batch)
     store = FeatureStore.resident(synthetic_features_device(0, n, dim))
-    pipe = SampleGatherPipeline(g, cfg, store, len(pool), window=window or None)
+    pipe = SampleGatherPipeline(g, cfg, store, len(pool), window=window or None, sparse_visited=sparse)
     gs = P.KeyedRng(9).derive(2, 0, 0)
     plan = pipe.plan_epoch(pool, gs)
     table = O.synthetic_features(np.arange(n), dim)
@@ -65,7 +66,8 @@ def test_epoch_windows_match_oracle(window, batch, fanouts, deg):
     assert seen == list(range(math.ceil(len(pool) / batch)))
 
 
-def test_epoch_presampling_counters_match_reference_semantics():
+@pytest.mark.parametrize("sparse", [False, True])
+def test_epoch_presampling_counters_match_reference_semantics(sparse):
     """Hotness fused into the window pipeline equals the oracle epoch trace."""
     import paper_2305_16588_b200 as P
     from paper_2305_16588_b200.pipeline import SampleGatherPipeline
@@ -75,10 +77,11 @@ def test_epoch_presampling_counters_match_reference_semantics():
     g = P.generate_synthetic(n, 12, 1.2, seed=8)
     pool = np.arange(0, n, 13, dtype=np.int64)
     cfg = P.SamplingConfig(fanouts=(10, 5), batch_size=128)
-    pipe = SampleGatherPipeline(g, cfg, None, len(pool), window=4)
+    pipe = SampleGatherPipeline(g, cfg, None, len(pool), window=4, sparse_visited=sparse)
     hot = DeviceHotness(n)
     seed = 77
-    pipe.run_epoch(pipe.plan_epoch(pool, P.KeyedRng(seed).derive(0, 0, 0)), hot=hot)
+    plan = pipe.plan_epoch(pool, P.KeyedRng(seed).derive(0, 0, 0))
+    pipe.run_epoch(plan, hot=hot)
     reads, looks, trav, nb = O.sampling_epoch(g.row_offsets, g.col_indices, n, [pool], [(0,)], [10, 5], 128, seed, 0)[0]
     assert np.array_equal(hot.topo_reads.cpu().numpy(), reads)
     assert np.array_equal(hot.feat_lookups.cpu().numpy(), looks)
@@ -164,3 +167,37 @@ def test_plan_built_cache_traffic_equals_reference_report():
         assert t["host_txn"] == rep.sampling_cpu_txn[gpu]
         assert f["local"] == rep.feat_local_hits[gpu] and f["peer"] == rep.feat_peer_hits[gpu]
         assert f["host"] * row_txns == rep.feature_cpu_txn[gpu]
+
+
+def test_sparse_visited_reuse_across_windows_and_large_ids():
+    """Sparse compaction over a 20M-vertex id space: ids near the top block, windows
+    reusing cleared bitmaps/summaries, and the flat path agree with np.unique."""
+    import paper_2305_16588_b200 as P
+    from paper_2305_16588_b200.sampling import WindowSampler
+
+    n = 20_000_000
+    rng = np.random.default_rng(5)
+    src = np.repeat(np.arange(n - 3000, n, dtype=np.int64), 8)
+    dst = np.concatenate([rng.integers(0, n, len(src) // 2), rng.integers(n - 70_000, n, len(src) - len(src) // 2)])
+    g = P.CsrGraph.from_edges(n, src, dst)
+    all_seeds = [rng.integers(n - 3000, n, (3, 256)), rng.integers(n - 3000, n, (3, 256)), np.full((3, 256), n - 1)]
+    results = {}
+    for sparse in (False, True):
+        sp = WindowSampler(g, (5, 3), 256, 3, sparse_visited=sparse)
+        outs = []
+        for rep in range(3):  # the same buffers are cleared and reused
+            seeds = all_seeds[rep]
+            keys = np.array([[P.KeyedRng(rep).derive(b).derive(h).key for h in range(2)] for b in range(3)],
+                            dtype=np.uint64)
+            sp.load(torch.from_numpy(seeds.astype(np.int64).astype(np.uint32).view(np.int32).reshape(-1)).cuda(),
+                    np.array([256, 256, 256]), keys)
+            sp.run()
+            for b in range(3):
+                bs = sp.batch_to_host(b)
+                want = np.unique(np.concatenate([bs.seeds] + [h.neighbors for h in bs.hops]))
+                got = bs.distinct_vertices()
+                assert np.array_equal(got, want)
+                outs.append(got)
+        results[sparse] = outs
+    for a, b in zip(results[False], results[True]):
+        assert np.array_equal(a, b)
