@@ -17,8 +17,6 @@ constexpr int kWordsPerTile = kUniqThreads * kWordsPerThread;
 struct UniqueParams {
     uint32_t* bm;
     uint64_t bwords;
-    uint32_t* sm;
-    uint64_t swords;
     uint32_t tiles_per_batch;
     uint32_t* uniq;
     uint64_t ustride;
@@ -81,12 +79,17 @@ __global__ void __launch_bounds__(kUniqThreads) k_unique(UniqueParams p) {
     if (t == p.tiles_per_batch - 1 && tid == kUniqThreads - 1) p.ucount[b] = (uint32_t)s_prefix + excl + c0 + c1 + c2 + c3;
 }
 
-// Sparse compaction: one warp per summary word (32 blocks of 32 bitmap words); lane i
-// tallies block i. Pass 1 counts the set bits of each non-empty block (one coalesced
-// 128-byte load per block), a CTA scan + decoupled look-back give the batch-level
-// offset of the tile, pass 2 reloads the blocks and emits ids in ascending order,
-// rank-table entries for non-empty words, and clears what it consumed.
-constexpr int kSparseWarps = kUniqThreads / 32;  // summary words per tile
+// Sparse compaction, fully parallel over the non-empty 32-word blocks (1024 vertices):
+//   k_block_lists     one CTA per batch: summary bits -> ascending list of non-empty
+//                     blocks (and the summary is cleared as it is read)
+//   k_chunk_offsets   one CTA: exclusive scan of chunks (8 blocks) over the batches
+//   k_unique_blocks   persistent CTAs claim chunks in order; warp w of a chunk loads
+//                     block w (one coalesced 128-byte load), a CTA scan + decoupled
+//                     look-back over the batch's chunks gives the output offset, and
+//                     the warp emits ids in ascending order, rank-table entries, and
+//                     clears the words it consumed.
+// Work is O(distinct blocks + n/32768) per batch instead of O(n/32).
+constexpr int kChunkBlocks = kUniqThreads / 32;  // blocks per chunk (one warp each)
 
 __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, uint32_t& total) {
     const int lane = threadIdx.x & 31;
@@ -100,59 +103,127 @@ __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, uint32_t& total) 
     return x - v;
 }
 
-__global__ void __launch_bounds__(kUniqThreads) k_unique_sparse(UniqueParams p) {
-    __shared__ uint32_t s_vid;
-    __shared__ uint32_t s_warp[kSparseWarps];
+struct SparseParams {
+    uint32_t* bm;
+    uint64_t bwords;
+    uint32_t* sm;
+    uint64_t swords;
+    uint32_t num_batches;
+    uint32_t* lists;     // [W][list_stride] non-empty block ids
+    uint64_t list_stride;
+    uint32_t* nblocks;   // [W]
+    uint32_t* chunk_start;  // [W + 1]
+    uint64_t* state;     // look-back status per global chunk
+    uint32_t* counter;
+    uint32_t* uniq;
+    uint64_t ustride;
+    uint32_t* ucount;
+    uint2* rank;
+    uint64_t* feat;
+    int clear;
+};
+
+__global__ void __launch_bounds__(kUniqThreads) k_block_lists(SparseParams p) {
+    using Scan = cub::BlockScan<uint32_t, kUniqThreads>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ uint32_t s_run;
+    const uint32_t b = blockIdx.x;
+    uint32_t* srow = p.sm + b * p.swords;
+    uint32_t* list = p.lists + b * p.list_stride;
+    if (threadIdx.x == 0) s_run = 0;
+    __syncthreads();
+    for (uint64_t base = 0; base < p.swords; base += kUniqThreads) {
+        const uint64_t sw = base + threadIdx.x;
+        const uint32_t s = sw < p.swords ? srow[sw] : 0u;
+        uint32_t excl, total;
+        Scan(tmp).ExclusiveSum((uint32_t)__popc(s), excl, total);
+        uint32_t pos = s_run + excl;
+        for (uint32_t m = s; m; m &= m - 1u) list[pos++] = (uint32_t)(sw * 32 + (__ffs(m) - 1));
+        if (p.clear && s) srow[sw] = 0u;
+        __syncthreads();
+        if (threadIdx.x == 0) s_run += total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) p.nblocks[b] = s_run;
+}
+
+__global__ void __launch_bounds__(1024) k_chunk_offsets(SparseParams p) {
+    using Scan = cub::BlockScan<uint32_t, 1024>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ uint32_t s_run;
+    if (threadIdx.x == 0) s_run = 0;
+    __syncthreads();
+    for (uint32_t base = 0; base < p.num_batches; base += 1024) {
+        const uint32_t b = base + threadIdx.x;
+        const uint32_t nb = b < p.num_batches ? p.nblocks[b] : 0u;
+        uint32_t excl, total;
+        Scan(tmp).ExclusiveSum((nb + kChunkBlocks - 1) / kChunkBlocks, excl, total);
+        if (b < p.num_batches) {
+            p.chunk_start[b] = s_run + excl;
+            if (nb == 0) p.ucount[b] = 0;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) s_run += total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) p.chunk_start[p.num_batches] = s_run;
+}
+
+__global__ void __launch_bounds__(kUniqThreads) k_unique_blocks(SparseParams p) {
+    __shared__ uint32_t s_c, s_b;
+    __shared__ uint32_t s_warp[kChunkBlocks];
     __shared__ uint64_t s_prefix;
     __shared__ uint32_t s_total;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_vid = atomicAdd(p.tile_counter, 1u);
-    __syncthreads();
-    const uint32_t b = s_vid / p.tiles_per_batch;
-    const uint32_t t = s_vid % p.tiles_per_batch;
-    const uint64_t sw = (uint64_t)t * kSparseWarps + warp;
-    uint32_t* row = p.bm + b * p.bwords;
-    uint32_t* srow = p.sm + b * p.swords;
-    const uint32_t s = sw < p.swords ? srow[sw] : 0u;
-    // pass 1: lane i holds the population of block i of this summary word
-    uint32_t my_cnt = 0;
-    for (uint32_t m = s; m; m &= m - 1u) {
-        const int i = __ffs(m) - 1;
-        const uint64_t wi = (sw * 32 + i) * 32 + lane;
-        const uint32_t x = wi < p.bwords ? row[wi] : 0u;
-        const uint32_t c = __reduce_add_sync(kFull, (uint32_t)__popc(x));
-        if (lane == i) my_cnt = c;
-    }
-    uint32_t warp_total;
-    const uint32_t blk_excl = warp_excl_scan(my_cnt, warp_total);
-    if (lane == 0) s_warp[warp] = warp_total;
-    __syncthreads();
-    if (warp == 0) {
-        const uint32_t v = lane < kSparseWarps ? s_warp[lane] : 0u;
-        uint32_t tile_total;
-        const uint32_t ex = warp_excl_scan(v, tile_total);
-        if (lane < kSparseWarps) s_warp[lane] = ex;
-        const uint64_t sidx = (uint64_t)b * p.tiles_per_batch + t;
-        if (lane == 0 && t != 0) publish(p.tile_state + sidx, kFlagAgg | tile_total);
-        const uint64_t pre = lookback_warp(p.tile_state, (uint64_t)b * p.tiles_per_batch, sidx, tile_total);
-        if (lane == 0) {
-            s_prefix = pre;
-            s_total = tile_total;
+    const uint32_t total_chunks = p.chunk_start[p.num_batches];
+    while (true) {
+        if (tid == 0) {
+            const uint32_t c = atomicAdd(p.counter, 1u);
+            s_c = c;
+            if (c < total_chunks) {
+                // batch owning chunk c: last b with chunk_start[b] <= c
+                uint32_t lo = 0, hi = p.num_batches;
+                while (hi - lo > 1) {
+                    const uint32_t mid = (lo + hi) / 2;
+                    if (p.chunk_start[mid] <= c) lo = mid; else hi = mid;
+                }
+                s_b = lo;
+            }
         }
-    }
-    __syncthreads();
-    const uint32_t warp_base = (uint32_t)s_prefix + s_warp[warp];
-    uint32_t* out = p.uniq + b * p.ustride;
-    // pass 2: emission in ascending vertex order
-    for (uint32_t m = s; m; m &= m - 1u) {
-        const int i = __ffs(m) - 1;
-        const uint32_t blk_base = warp_base + __shfl_sync(kFull, blk_excl, i);
-        const uint64_t wi = (sw * 32 + i) * 32 + lane;
-        const uint32_t x = wi < p.bwords ? row[wi] : 0u;
-        uint32_t dummy;
-        uint32_t pos = blk_base + warp_excl_scan((uint32_t)__popc(x), dummy);
+        __syncthreads();
+        const uint32_t c = s_c;
+        if (c >= total_chunks) break;
+        const uint32_t b = s_b;
+        const uint32_t first = p.chunk_start[b];
+        const uint32_t nb = p.nblocks[b];
+        const uint32_t ci = c - first;
+        const uint32_t bi = ci * kChunkBlocks + warp;
+        uint32_t* row = p.bm + b * p.bwords;
+        const bool valid = bi < nb;
+        const uint32_t blk = valid ? p.lists[b * p.list_stride + bi] : 0u;
+        const uint64_t wi = (uint64_t)blk * 32 + lane;
+        const uint32_t x = (valid && wi < p.bwords) ? row[wi] : 0u;
+        uint32_t wtot;
+        const uint32_t wex = warp_excl_scan((uint32_t)__popc(x), wtot);
+        if (lane == 0) s_warp[warp] = wtot;
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t v = lane < kChunkBlocks ? s_warp[lane] : 0u;
+            uint32_t tile_total;
+            const uint32_t ex = warp_excl_scan(v, tile_total);
+            if (lane < kChunkBlocks) s_warp[lane] = ex;
+            if (lane == 0 && ci != 0) publish(p.state + c, kFlagAgg | tile_total);
+            const uint64_t pre = lookback_warp(p.state, first, c, tile_total);
+            if (lane == 0) {
+                s_prefix = pre;
+                s_total = tile_total;
+            }
+        }
+        __syncthreads();
+        uint32_t pos = (uint32_t)s_prefix + s_warp[warp] + wex;
         if (x) {
             if (p.rank) p.rank[b * p.bwords + wi] = make_uint2(pos, x);
+            uint32_t* out = p.uniq + b * p.ustride;
             const uint32_t vbase = (uint32_t)(wi * 32);
             for (uint32_t w = x; w; w &= w - 1u) {
                 const uint32_t u = vbase + (__ffs(w) - 1);
@@ -161,9 +232,28 @@ __global__ void __launch_bounds__(kUniqThreads) k_unique_sparse(UniqueParams p) 
             }
             if (p.clear) row[wi] = 0u;
         }
+        if (tid == 0 && (ci + 1) * kChunkBlocks >= nb) p.ucount[b] = (uint32_t)s_prefix + s_total;
+        __syncthreads();
     }
-    if (p.clear && lane == 0 && s) srow[sw] = 0u;
-    if (t == p.tiles_per_batch - 1 && tid == 0) p.ucount[b] = (uint32_t)s_prefix + s_total;
+}
+
+struct SparseLayout {
+    size_t lists, nblocks, chunk_start, state, counter, total;
+    uint64_t list_stride, max_chunks;
+};
+
+static SparseLayout sparse_layout(uint32_t W, const gc_visited_t* v) {
+    SparseLayout L{};
+    L.list_stride = v->summary_words * 32;
+    L.max_chunks = (L.list_stride + kChunkBlocks - 1) / kChunkBlocks;
+    size_t off = 0;
+    L.lists = off; off = align_up(off + (size_t)W * L.list_stride * 4, 256);
+    L.nblocks = off; off = align_up(off + (size_t)W * 4, 256);
+    L.chunk_start = off; off = align_up(off + (size_t)(W + 1) * 4, 256);
+    L.state = off; off = align_up(off + (size_t)W * L.max_chunks * 8, 256);
+    L.counter = off; off = align_up(off + 4, 256);
+    L.total = off;
+    return L;
 }
 
 __device__ __forceinline__ uint32_t rank_of(const uint2* __restrict__ rt, uint32_t u) {
@@ -223,8 +313,7 @@ __global__ void k_mark(const uint32_t* __restrict__ ids, uint64_t stride, const 
 }
 
 static unsigned uniq_tiles(const gc_visited_t* v) {
-    uint64_t t = v->summary ? (v->summary_words + kSparseWarps - 1) / kSparseWarps
-                            : (v->words + kWordsPerTile - 1) / kWordsPerTile;
+    uint64_t t = (v->words + kWordsPerTile - 1) / kWordsPerTile;
     return t ? (unsigned)t : 1u;
 }
 
@@ -253,6 +342,7 @@ uint64_t gc_summary_words(int64_t num_vertices) {
 
 size_t gc_unique_temp_bytes(uint32_t num_batches, const gc_visited_t* visited) {
     if (!visited) return 0;
+    if (visited->summary) return sparse_layout(num_batches, visited).total;
     return align_up((size_t)num_batches * uniq_tiles(visited) * sizeof(uint64_t), 256) + 256;
 }
 
@@ -268,13 +358,46 @@ int gc_unique_compact(const gc_visited_t* visited, uint32_t num_batches, uint32_
     const size_t need = gc_unique_temp_bytes(num_batches, visited);
     GC_REQUIRE(d_temp && temp_bytes >= need, GC_ERR_VALUE, "gc_unique_compact: temp buffer too small");
     cudaStream_t s = as_stream(stream);
+    if (visited->summary) {
+        const SparseLayout L = sparse_layout(num_batches, visited);
+        char* t = static_cast<char*>(d_temp);
+        SparseParams q{};
+        q.bm = visited->bitmap;
+        q.bwords = visited->words;
+        q.sm = visited->summary;
+        q.swords = visited->summary_words;
+        q.num_batches = num_batches;
+        q.lists = reinterpret_cast<uint32_t*>(t + L.lists);
+        q.list_stride = L.list_stride;
+        q.nblocks = reinterpret_cast<uint32_t*>(t + L.nblocks);
+        q.chunk_start = reinterpret_cast<uint32_t*>(t + L.chunk_start);
+        q.state = reinterpret_cast<uint64_t*>(t + L.state);
+        q.counter = reinterpret_cast<uint32_t*>(t + L.counter);
+        q.uniq = d_unique;
+        q.ustride = unique_stride;
+        q.ucount = d_unique_count;
+        q.rank = reinterpret_cast<uint2*>(d_rank_table);
+        q.feat = d_feat_lookups;
+        q.clear = clear_bitmap;
+        // the block lists need the summary; it is cleared as it is read only when the
+        // bitmap is cleared too
+        GC_TRY(cudaMemsetAsync(t + L.state, 0, L.total - L.state, s), "gc_unique_compact memset");
+        k_block_lists<<<num_batches, kUniqThreads, 0, s>>>(q);
+        GC_CHECK_LAUNCH("gc_unique_compact lists");
+        k_chunk_offsets<<<1, 1024, 0, s>>>(q);
+        GC_CHECK_LAUNCH("gc_unique_compact chunks");
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        k_unique_blocks<<<(unsigned)sms * 4, kUniqThreads, 0, s>>>(q);
+        GC_CHECK_LAUNCH("gc_unique_compact blocks");
+        return GC_OK;
+    }
     const unsigned tiles = uniq_tiles(visited);
     const size_t state_bytes = align_up((size_t)num_batches * tiles * sizeof(uint64_t), 256);
     UniqueParams p{};
     p.bm = visited->bitmap;
     p.bwords = visited->words;
-    p.sm = visited->summary;
-    p.swords = visited->summary_words;
     p.tiles_per_batch = tiles;
     p.uniq = d_unique;
     p.ustride = unique_stride;
@@ -287,10 +410,7 @@ int gc_unique_compact(const gc_visited_t* visited, uint32_t num_batches, uint32_
     GC_TRY(cudaMemsetAsync(d_temp, 0, state_bytes + 256, s), "gc_unique_compact memset");
     const uint64_t grid = (uint64_t)num_batches * tiles;
     GC_REQUIRE(grid < (1ull << 31), GC_ERR_VALUE, "gc_unique_compact: window too large");
-    if (p.sm)
-        k_unique_sparse<<<(unsigned)grid, kUniqThreads, 0, s>>>(p);
-    else
-        k_unique<<<(unsigned)grid, kUniqThreads, 0, s>>>(p);
+    k_unique<<<(unsigned)grid, kUniqThreads, 0, s>>>(p);
     GC_CHECK_LAUNCH("gc_unique_compact");
     return GC_OK;
 }
