@@ -113,6 +113,7 @@ struct SparseParams {
     uint64_t list_stride;
     uint32_t* nblocks;   // [W]
     uint32_t* chunk_start;  // [W + 1]
+    uint32_t* chunk_batch;  // [max chunks] batch owning each global chunk
     uint64_t* state;     // look-back status per global chunk
     uint32_t* counter;
     uint32_t* uniq;
@@ -169,31 +170,22 @@ __global__ void __launch_bounds__(1024) k_chunk_offsets(SparseParams p) {
     if (threadIdx.x == 0) p.chunk_start[p.num_batches] = s_run;
 }
 
+__global__ void k_chunk_batches(SparseParams p) {
+    const uint32_t b = blockIdx.x;
+    for (uint32_t c = p.chunk_start[b] + threadIdx.x; c < p.chunk_start[b + 1]; c += blockDim.x) p.chunk_batch[c] = b;
+}
+
+// Persistent CTAs take chunks c = blockIdx.x + k * gridDim.x in increasing order. A
+// chunk only waits on earlier chunks of its batch, and every CTA is resident (the
+// grid is sized to fit), so the smallest unfinished chunk always progresses.
 __global__ void __launch_bounds__(kUniqThreads) k_unique_blocks(SparseParams p) {
-    __shared__ uint32_t s_c, s_b;
     __shared__ uint32_t s_warp[kChunkBlocks];
     __shared__ uint64_t s_prefix;
     __shared__ uint32_t s_total;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t total_chunks = p.chunk_start[p.num_batches];
-    while (true) {
-        if (tid == 0) {
-            const uint32_t c = atomicAdd(p.counter, 1u);
-            s_c = c;
-            if (c < total_chunks) {
-                // batch owning chunk c: last b with chunk_start[b] <= c
-                uint32_t lo = 0, hi = p.num_batches;
-                while (hi - lo > 1) {
-                    const uint32_t mid = (lo + hi) / 2;
-                    if (p.chunk_start[mid] <= c) lo = mid; else hi = mid;
-                }
-                s_b = lo;
-            }
-        }
-        __syncthreads();
-        const uint32_t c = s_c;
-        if (c >= total_chunks) break;
-        const uint32_t b = s_b;
+    for (uint32_t c = blockIdx.x; c < total_chunks; c += gridDim.x) {
+        const uint32_t b = p.chunk_batch[c];
         const uint32_t first = p.chunk_start[b];
         const uint32_t nb = p.nblocks[b];
         const uint32_t ci = c - first;
@@ -238,7 +230,7 @@ __global__ void __launch_bounds__(kUniqThreads) k_unique_blocks(SparseParams p) 
 }
 
 struct SparseLayout {
-    size_t lists, nblocks, chunk_start, state, counter, total;
+    size_t lists, nblocks, chunk_start, chunk_batch, state, counter, total;
     uint64_t list_stride, max_chunks;
 };
 
@@ -250,6 +242,7 @@ static SparseLayout sparse_layout(uint32_t W, const gc_visited_t* v) {
     L.lists = off; off = align_up(off + (size_t)W * L.list_stride * 4, 256);
     L.nblocks = off; off = align_up(off + (size_t)W * 4, 256);
     L.chunk_start = off; off = align_up(off + (size_t)(W + 1) * 4, 256);
+    L.chunk_batch = off; off = align_up(off + (size_t)W * L.max_chunks * 4, 256);
     L.state = off; off = align_up(off + (size_t)W * L.max_chunks * 8, 256);
     L.counter = off; off = align_up(off + 4, 256);
     L.total = off;
@@ -371,6 +364,7 @@ int gc_unique_compact(const gc_visited_t* visited, uint32_t num_batches, uint32_
         q.list_stride = L.list_stride;
         q.nblocks = reinterpret_cast<uint32_t*>(t + L.nblocks);
         q.chunk_start = reinterpret_cast<uint32_t*>(t + L.chunk_start);
+        q.chunk_batch = reinterpret_cast<uint32_t*>(t + L.chunk_batch);
         q.state = reinterpret_cast<uint64_t*>(t + L.state);
         q.counter = reinterpret_cast<uint32_t*>(t + L.counter);
         q.uniq = d_unique;
@@ -386,10 +380,14 @@ int gc_unique_compact(const gc_visited_t* visited, uint32_t num_batches, uint32_
         GC_CHECK_LAUNCH("gc_unique_compact lists");
         k_chunk_offsets<<<1, 1024, 0, s>>>(q);
         GC_CHECK_LAUNCH("gc_unique_compact chunks");
-        int dev = 0, sms = 148;
+        k_chunk_batches<<<num_batches, 256, 0, s>>>(q);
+        GC_CHECK_LAUNCH("gc_unique_compact chunk map");
+        int dev = 0, sms = 148, per_sm = 4;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        k_unique_blocks<<<(unsigned)sms * 4, kUniqThreads, 0, s>>>(q);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_unique_blocks, kUniqThreads, 0);
+        // every CTA must be resident for the static chunk order (see k_unique_blocks)
+        k_unique_blocks<<<(unsigned)(sms * (per_sm < 4 ? per_sm : 4)), kUniqThreads, 0, s>>>(q);
         GC_CHECK_LAUNCH("gc_unique_compact blocks");
         return GC_OK;
     }
