@@ -113,7 +113,7 @@ struct SparseParams {
     uint64_t list_stride;
     uint32_t* nblocks;   // [W]
     uint32_t* chunk_start;  // [W + 1]
-    uint32_t* chunk_batch;  // [max chunks] batch owning each global chunk
+    uint4* chunk_desc;   // [max chunks] {batch, chunk in batch, first global chunk, blocks in batch}
     uint64_t* state;     // look-back status per global chunk
     uint32_t* counter;
     uint32_t* uniq;
@@ -172,29 +172,42 @@ __global__ void __launch_bounds__(1024) k_chunk_offsets(SparseParams p) {
 
 __global__ void k_chunk_batches(SparseParams p) {
     const uint32_t b = blockIdx.x;
-    for (uint32_t c = p.chunk_start[b] + threadIdx.x; c < p.chunk_start[b + 1]; c += blockDim.x) p.chunk_batch[c] = b;
+    const uint32_t first = p.chunk_start[b], end = p.chunk_start[b + 1], nb = p.nblocks[b];
+    for (uint32_t c = first + threadIdx.x; c < end; c += blockDim.x) p.chunk_desc[c] = make_uint4(b, c - first, first, nb);
 }
 
 // Persistent CTAs take chunks c = blockIdx.x + k * gridDim.x in increasing order. A
 // chunk only waits on earlier chunks of its batch, and every CTA is resident (the
-// grid is sized to fit), so the smallest unfinished chunk always progresses.
+// grid is sized to fit), so the smallest unfinished chunk always progresses. The next
+// chunk's descriptor, block id and bitmap word are loaded before the current chunk's
+// scan, look-back and emission, so the dependent-load chain overlaps.
 __global__ void __launch_bounds__(kUniqThreads) k_unique_blocks(SparseParams p) {
     __shared__ uint32_t s_warp[kChunkBlocks];
     __shared__ uint64_t s_prefix;
     __shared__ uint32_t s_total;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t total_chunks = p.chunk_start[p.num_batches];
+    auto fetch = [&](uint32_t c, uint4& d, uint64_t& wi, uint32_t& x) {
+        x = 0u;
+        wi = 0;
+        if (c >= total_chunks) return;
+        d = p.chunk_desc[c];
+        const uint32_t bi = d.y * kChunkBlocks + warp;
+        if (bi < d.w) {
+            wi = (uint64_t)p.lists[d.x * p.list_stride + bi] * 32 + lane;
+            if (wi < p.bwords) x = p.bm[d.x * p.bwords + wi];
+        }
+    };
+    uint4 d{};
+    uint64_t wi;
+    uint32_t x;
+    fetch(blockIdx.x, d, wi, x);
     for (uint32_t c = blockIdx.x; c < total_chunks; c += gridDim.x) {
-        const uint32_t b = p.chunk_batch[c];
-        const uint32_t first = p.chunk_start[b];
-        const uint32_t nb = p.nblocks[b];
-        const uint32_t ci = c - first;
-        const uint32_t bi = ci * kChunkBlocks + warp;
-        uint32_t* row = p.bm + b * p.bwords;
-        const bool valid = bi < nb;
-        const uint32_t blk = valid ? p.lists[b * p.list_stride + bi] : 0u;
-        const uint64_t wi = (uint64_t)blk * 32 + lane;
-        const uint32_t x = (valid && wi < p.bwords) ? row[wi] : 0u;
+        uint4 dn{};
+        uint64_t win;
+        uint32_t xn;
+        fetch(c + gridDim.x, dn, win, xn);
+        const uint32_t b = d.x, ci = d.y, first = d.z, nb = d.w;
         uint32_t wtot;
         const uint32_t wex = warp_excl_scan((uint32_t)__popc(x), wtot);
         if (lane == 0) s_warp[warp] = wtot;
@@ -222,15 +235,18 @@ __global__ void __launch_bounds__(kUniqThreads) k_unique_blocks(SparseParams p) 
                 out[pos++] = u;
                 if (p.feat) atomicAdd((unsigned long long*)(p.feat + u), 1ull);
             }
-            if (p.clear) row[wi] = 0u;
+            if (p.clear) p.bm[b * p.bwords + wi] = 0u;
         }
         if (tid == 0 && (ci + 1) * kChunkBlocks >= nb) p.ucount[b] = (uint32_t)s_prefix + s_total;
         __syncthreads();
+        d = dn;
+        wi = win;
+        x = xn;
     }
 }
 
 struct SparseLayout {
-    size_t lists, nblocks, chunk_start, chunk_batch, state, counter, total;
+    size_t lists, nblocks, chunk_start, chunk_desc, state, counter, total;
     uint64_t list_stride, max_chunks;
 };
 
@@ -242,7 +258,7 @@ static SparseLayout sparse_layout(uint32_t W, const gc_visited_t* v) {
     L.lists = off; off = align_up(off + (size_t)W * L.list_stride * 4, 256);
     L.nblocks = off; off = align_up(off + (size_t)W * 4, 256);
     L.chunk_start = off; off = align_up(off + (size_t)(W + 1) * 4, 256);
-    L.chunk_batch = off; off = align_up(off + (size_t)W * L.max_chunks * 4, 256);
+    L.chunk_desc = off; off = align_up(off + (size_t)W * L.max_chunks * 16, 256);
     L.state = off; off = align_up(off + (size_t)W * L.max_chunks * 8, 256);
     L.counter = off; off = align_up(off + 4, 256);
     L.total = off;
@@ -364,7 +380,7 @@ int gc_unique_compact(const gc_visited_t* visited, uint32_t num_batches, uint32_
         q.list_stride = L.list_stride;
         q.nblocks = reinterpret_cast<uint32_t*>(t + L.nblocks);
         q.chunk_start = reinterpret_cast<uint32_t*>(t + L.chunk_start);
-        q.chunk_batch = reinterpret_cast<uint32_t*>(t + L.chunk_batch);
+        q.chunk_desc = reinterpret_cast<uint4*>(t + L.chunk_desc);
         q.state = reinterpret_cast<uint64_t*>(t + L.state);
         q.counter = reinterpret_cast<uint32_t*>(t + L.counter);
         q.uniq = d_unique;
@@ -382,12 +398,12 @@ int gc_unique_compact(const gc_visited_t* visited, uint32_t num_batches, uint32_
         GC_CHECK_LAUNCH("gc_unique_compact chunks");
         k_chunk_batches<<<num_batches, 256, 0, s>>>(q);
         GC_CHECK_LAUNCH("gc_unique_compact chunk map");
-        int dev = 0, sms = 148, per_sm = 4;
+        int dev = 0, sms = 148, per_sm = 1;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_unique_blocks, kUniqThreads, 0);
         // every CTA must be resident for the static chunk order (see k_unique_blocks)
-        k_unique_blocks<<<(unsigned)(sms * (per_sm < 4 ? per_sm : 4)), kUniqThreads, 0, s>>>(q);
+        k_unique_blocks<<<(unsigned)(sms * (per_sm > 0 ? per_sm : 1)), kUniqThreads, 0, s>>>(q);
         GC_CHECK_LAUNCH("gc_unique_compact blocks");
         return GC_OK;
     }
