@@ -76,7 +76,66 @@ __global__ void __launch_bounds__(256) k_gather(GatherParams p) {
         } else {
             *reinterpret_cast<uint32_t*>(dst) = __ldg(reinterpret_cast<const uint32_t*>(src));
         }
-        if (c == 0) cnt[tier] += 1;
+        if (c == 0) {
+            cnt[0] += tier == 0;
+            cnt[1] += tier == 1;
+            cnt[2] += tier == 2;
+        }
+    }
+    if (p.tier_rows) {
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+            unsigned long long v = cnt[t];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+            if ((threadIdx.x & 31) == 0 && v) atomicAdd(&s_tier[t], v);
+        }
+        __syncthreads();
+        if (threadIdx.x < 3 && s_tier[threadIdx.x])
+            atomicAdd((unsigned long long*)(p.tier_rows + threadIdx.x), s_tier[threadIdx.x]);
+    }
+}
+
+// Warp-per-row gather for 16-byte-aligned rows of at most 32 vectors (D <= 128 fp32):
+// lane l moves vector l of a row. Each warp keeps ROWS rows in flight — their ids and
+// locations are fetched by ROWS lanes at once and broadcast, then ROWS independent
+// 16-byte loads per lane are issued before any store — so HBM, NVLink and PCIe
+// latency overlap instead of serialising per row.
+template <int ROWS>
+__global__ void __launch_bounds__(256) k_gather_rows(GatherParams p) {
+    __shared__ unsigned long long s_tier[3];
+    const uint32_t b = blockIdx.y;
+    const uint32_t rows = min(p.count[b], p.max_rows);
+    const uint32_t per_row = p.fs.row_bytes / 16;  // <= 32
+    const uint32_t* ids = p.ids + b * p.ids_stride;
+    char* out = p.out + b * p.out_stride_rows * p.fs.row_bytes;
+    const int lane = threadIdx.x & 31;
+    if (p.tier_rows && threadIdx.x < 3) s_tier[threadIdx.x] = 0;
+    if (p.tier_rows) __syncthreads();
+    unsigned long long cnt[3] = {0, 0, 0};
+    const uint32_t warps = gridDim.x * (blockDim.x / 32);
+    const uint32_t wid = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    for (uint32_t r0 = wid * ROWS; r0 < rows; r0 += warps * ROWS) {
+        // lanes 0..ROWS-1 resolve one row each
+        const char* my_src = nullptr;
+        int my_tier = 0;
+        if (lane < ROWS && r0 + lane < rows) my_src = row_source(p.fs, __ldg(ids + r0 + lane), my_tier);
+        uint4 v[ROWS];
+#pragma unroll
+        for (int j = 0; j < ROWS; ++j) {
+            const char* src = (const char*)__shfl_sync(kFull, (unsigned long long)my_src, j);
+            v[j] = (src && (uint32_t)lane < per_row) ? ld_stream16(src + 16 * lane) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int j = 0; j < ROWS; ++j) {
+            if (r0 + j < rows && (uint32_t)lane < per_row)
+                st_stream16(out + (uint64_t)(r0 + j) * p.fs.row_bytes + 16 * lane, v[j]);
+        }
+        if (lane < ROWS && r0 + lane < rows) {
+            cnt[0] += my_tier == 0;
+            cnt[1] += my_tier == 1;
+            cnt[2] += my_tier == 2;
+        }
     }
     if (p.tier_rows) {
 #pragma unroll
@@ -161,10 +220,18 @@ int gc_gather(const gc_feature_store_t* store, const uint32_t* d_ids, uint64_t i
     if (gx > cap) gx = cap;
     if (gx < 1) gx = 1;
     dim3 grid((unsigned)gx, num_batches);
-    if (vec16)
+    if (vec16 && per_row <= 32) {
+        // warp per row, 4 rows in flight per warp; ~16 resident warps per SM per batch slice
+        uint64_t wx = ((uint64_t)max_count + 4 * 8 - 1) / (4 * 8);
+        const uint64_t wcap = (uint64_t)148 * 16 / num_batches;
+        if (wx > wcap) wx = wcap;
+        if (wx < 1) wx = 1;
+        k_gather_rows<4><<<dim3((unsigned)wx, num_batches), 256, 0, as_stream(stream)>>>(p);
+    } else if (vec16) {
         k_gather<16><<<grid, 256, 0, as_stream(stream)>>>(p);
-    else
+    } else {
         k_gather<4><<<grid, 256, 0, as_stream(stream)>>>(p);
+    }
     GC_CHECK_LAUNCH("gc_gather");
     return GC_OK;
 }

@@ -1,0 +1,72 @@
+"""Probe: GPU gather throughput from the host tier vs host-table size and allocation.
+
+Random 512-byte rows read through UVA by the K4 gather from (a) torch pinned memory
+(cudaHostAlloc) and (b) an anonymous mmap with MADV_HUGEPAGE registered through
+gc_host_register (cudaHostRegister, mapped). Prints GB/s per case.
+"""
+
+import ctypes
+import mmap
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_2305_16588_b200 import _lib  # noqa: E402
+from paper_2305_16588_b200.cache import FeatureStore  # noqa: E402
+from paper_2305_16588_b200.graph import FeatureSpec  # noqa: E402
+
+MADV_HUGEPAGE = 14
+
+
+def thp_buffer(nbytes):
+    buf = mmap.mmap(-1, nbytes, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
+    addr = ctypes.addressof(ctypes.c_char.from_buffer(buf))
+    libc = ctypes.CDLL("libc.so.6")
+    libc.madvise(ctypes.c_void_p(addr), ctypes.c_size_t(nbytes), MADV_HUGEPAGE)
+    arr = np.frombuffer(buf, dtype=np.float32)
+    arr[::1024] = 0.0  # touch every 4 KB page so THP can back it
+    return buf, arr, addr
+
+
+def run(host_ptr, n, dim, rows=1 << 20, reps=5):
+    lib = _lib.lib()
+    loc = torch.full((n,), -1, dtype=torch.int32, device="cuda")  # all rows host-resident
+    fs = FeatureStore(FeatureSpec(dim), 0, 1, loc, [None], None)
+    fs.c_struct.host_rows = host_ptr
+    ids = torch.randint(0, n, (1, rows), dtype=torch.int64, device="cuda").to(torch.int32)
+    cnt = torch.tensor([rows], dtype=torch.int32, device="cuda")
+    out = torch.empty((1, rows, dim), dtype=torch.float32, device="cuda")
+    fs.gather(ids, cnt, out)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        fs.gather(ids, cnt, out)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / reps
+    return rows * dim * 4 / dt / 1e9
+
+
+def main():
+    dim = 128
+    for gb in (4, 16, 56):
+        n = int(gb * (1 << 30) / (dim * 4))
+        t = torch.empty((n, dim), dtype=torch.float32, pin_memory=True)
+        t.view(-1)[:: 1 << 20].fill_(1.0)
+        r1 = run(t.data_ptr(), n, dim)
+        del t
+        buf, arr, addr = thp_buffer(n * dim * 4)
+        dptr = ctypes.c_void_p()
+        lib = _lib.lib()
+        _lib.check(lib.gc_host_register(ctypes.c_void_p(addr), n * dim * 4, ctypes.byref(dptr)), "register")
+        r2 = run(dptr.value, n, dim)
+        _lib.check(lib.gc_host_unregister(ctypes.c_void_p(addr)), "unregister")
+        del arr
+        buf.close()
+        print(f"host table {gb:3d} GB: torch pinned {r1:6.1f} GB/s   THP+cudaHostRegister {r2:6.1f} GB/s", flush=True)
+
+
+if __name__ == "__main__":
+    main()
