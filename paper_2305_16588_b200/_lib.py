@@ -149,7 +149,8 @@ def load_library(path: os.PathLike | None = None) -> ctypes.CDLL:
     global _LIB
     if _LIB is not None and path is None:
         return _LIB
-    p = Path(path) if path is not None else LIB_PATH
+    # GC_LIB_PATH: load an experimental build (tools/build_variant.py) instead
+    p = Path(path) if path is not None else Path(os.environ.get("GC_LIB_PATH", LIB_PATH))
     if not p.exists():
         raise NativeUnavailable(
             f"{p} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"

@@ -81,16 +81,29 @@ struct PairHashHigh {
         const uint32_t lo = (uint32_t)x, h = (uint32_t)(x >> 32);
         return __umulhi(lo, (uint32_t)kMixB) + lo * (uint32_t)(kMixB >> 32) + h * (uint32_t)kMixB;
     }
+    // hi(c - (G & 0xFF)) for a loop counter c = (G & 0xFF) + j. The two 27-bit shifts
+    // of `x ^= x >> 27` are issued as multiplies by k32 == 32 — an opaque kernel
+    // argument, so ptxas keeps them on the FMA pipe — leaving the ALU pipe to the
+    // XORs and the selection network (both pipes issue at half rate per SMSP).
+    __device__ __forceinline__ uint32_t hi_counter(uint32_t c, uint32_t k32) const {
+        c ^= m;
+        const uint64_t x = P + (uint64_t)c * kMixA;
+        const uint32_t lo = (uint32_t)x, h = (uint32_t)(x >> 32);
+        const uint32_t lo2 = lo ^ __umulhi(lo, k32) ^ (h * k32);  // lo>>27 and hi<<5 do not overlap
+        const uint32_t h2 = h ^ __umulhi(h, k32);
+        return __umulhi(lo2, (uint32_t)kMixB) + lo2 * (uint32_t)(kMixB >> 32) + h2 * (uint32_t)kMixB;
+    }
 };
+
+constexpr uint32_t kGoldenLow = (uint32_t)(kGolden & 0xFFu);
 
 // Mark vertex u in one batch's visited set. Bits only go 0 -> 1 inside a launch, so
 // a stale cached read costs at most a redundant atomic, never a missed mark. With a
 // block summary, the one thread whose atomic turns a word non-zero flags the word's
 // 32-word block (1024 vertices) for the sparse compaction.
-__device__ __forceinline__ void mark_visited(uint32_t* bm, uint32_t* sm, uint32_t u) {
+__device__ __forceinline__ void mark_visited_unchecked(uint32_t* bm, uint32_t* sm, uint32_t u) {
     uint32_t* w = bm + (u >> 5);
     const uint32_t bit = 1u << (u & 31);
-    if (*w & bit) return;
     if (sm == nullptr) {
         atomicOr(w, bit);
         return;
@@ -99,6 +112,11 @@ __device__ __forceinline__ void mark_visited(uint32_t* bm, uint32_t* sm, uint32_
         const uint32_t blk = u >> 10;
         atomicOr(sm + (blk >> 5), 1u << (blk & 31));
     }
+}
+
+__device__ __forceinline__ void mark_visited(uint32_t* bm, uint32_t* sm, uint32_t u) {
+    if ((bm[u >> 5] >> (u & 31)) & 1u) return;
+    mark_visited_unchecked(bm, sm, u);
 }
 
 void set_error(const std::string& msg);

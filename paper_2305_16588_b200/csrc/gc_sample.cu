@@ -24,6 +24,7 @@ namespace gc {
 constexpr int kHopThreads = 256;
 constexpr int kTilePos = 256;
 constexpr int kItemCap = 4096;  // staged output items per round (32 KB of u64 edge indices)
+constexpr int kEmit = 4;        // emission items in flight per thread
 
 constexpr int kTierShift = 56;  // staged edge index = (tier code << 56) | edge within that tier's CSR
 constexpr uint64_t kEdgeMask = (1ull << kTierShift) - 1;
@@ -63,6 +64,7 @@ struct HopParams {
     uint64_t* tile_state;
     uint32_t* tile_counter;
     int exact_only;  // test hook: always take the 64-bit extraction path
+    uint32_t k32;    // == 32, opaque to the compiler (see PairHashHigh::hi_counter)
 };
 
 static int g_exact_only = 0;
@@ -243,30 +245,48 @@ __device__ void select_streaming(uint64_t hc, uint32_t deg, uint32_t fanout, uin
 
 // Thread-per-position choice path for deg <= 64 and fanout < S: the thread streams
 // its deg keys through a branchless S-slot min/max insertion network on packed
-// 32-bit values (26-bit key prefix << 6 | j), which keeps the S smallest in order.
-// Two equal prefixes among ranks 0..fanout mean the packed order may differ from
-// the exact (key, j) order: return false and let a warp redo the position exactly.
+// 32-bit values (25-bit key prefix << 7 | c, c = (G & 0xFF) + j the hash counter),
+// which keeps the S smallest in order. Two equal prefixes among ranks 0..fanout mean
+// the packed order may differ from the exact (key, j) order: return false and let a
+// warp redo the position exactly. deg > fanout >= TRI - 1, so the first TRI
+// candidates are inserted with the network peeled: slots still holding +inf fold away.
+template <int S>
+__device__ __forceinline__ void insert_slot(uint32_t (&t)[S], uint32_t x) {
+#pragma unroll
+    for (int s = S - 1; s >= 1; --s) t[s] = max(t[s - 1], min(t[s], x));
+    t[0] = min(t[0], x);
+}
+
+template <int S>
+__host__ __device__ constexpr int peeled_candidates() {
+    return S == 4 ? 2 : S == 6 ? 5 : S == 8 ? 7 : S == 11 ? 9 : S == 16 ? 12 : S == 21 ? 17 : S == 26 ? 22 : 27;
+}
+
 template <int S>
 __device__ __forceinline__ bool select_thread(uint64_t hc, uint32_t deg, uint32_t fanout, uint64_t o0, uint32_t excl,
-                                              uint32_t r0, uint32_t r1, uint64_t* s_items) {
-    constexpr int IB = 6;
+                                              uint32_t r0, uint32_t r1, uint64_t* s_items, uint32_t k32) {
+    constexpr int IB = 7;
+    constexpr int TRI = peeled_candidates<S>();
     uint32_t t[S];
 #pragma unroll
     for (int s = 0; s < S; ++s) t[s] = 0xFFFFFFFFu;
     const PairHashHigh hh(hc);  // deg <= 64: key bits 63..38 from the specialised hash
-    for (uint32_t j = 0; j < deg; ++j) {
-        const uint32_t x = (hh.hi(j) & ~((1u << IB) - 1u)) | j;
 #pragma unroll
-        for (int s = S - 1; s >= 1; --s) t[s] = max(t[s - 1], min(t[s], x));
-        t[0] = min(t[0], x);
+    for (int j = 0; j < TRI; ++j) {
+        const uint32_t c = kGoldenLow + j;
+        insert_slot<S>(t, (hh.hi_counter(c, k32) & ~((1u << IB) - 1u)) | c);
     }
+#pragma unroll 4
+    for (uint32_t c = kGoldenLow + TRI; c < kGoldenLow + deg; ++c)
+        insert_slot<S>(t, (hh.hi_counter(c, k32) & ~((1u << IB) - 1u)) | c);
     bool tie = false;
 #pragma unroll
     for (int s = 0; s + 1 < S; ++s) tie |= (s < (int)fanout) & ((t[s] >> IB) == (t[s + 1] >> IB));
     if (tie) return false;
 #pragma unroll
     for (int s = 0; s < S; ++s)
-        if (s < (int)fanout) stage(s_items, excl + s, r0, r1, o0 + (t[s] & ((1u << IB) - 1u)));
+        if (s < (int)fanout)
+            stage(s_items, excl + s, r0, r1, o0 + ((t[s] & ((1u << IB) - 1u)) - kGoldenLow));
     return true;
 }
 
@@ -303,14 +323,14 @@ __global__ void __launch_bounds__(kHopThreads, (S > 0 && S <= 16) ? 5 : 1) k_hop
         typename Reduce::TempStorage reduce;
     } tmp;
     __shared__ uint64_t s_items[kItemCap];
-    __shared__ uint32_t s_vid;
     __shared__ uint64_t s_prefix;
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
-    if (tid == 0) s_vid = atomicAdd(p.tile_counter, 1u);
-    __syncthreads();
-    const uint32_t vid = s_vid;
+    // tile id = blockIdx.x: CTAs are dispatched in increasing index order, so every
+    // predecessor a tile's look-back waits on is resident or done (as in CUB's
+    // single-pass scans)
+    const uint32_t vid = blockIdx.x;
     const uint32_t b = vid / p.tiles_per_batch;
     const uint32_t t = vid % p.tiles_per_batch;
     const uint32_t F = p.fcount[b];
@@ -407,7 +427,7 @@ __global__ void __launch_bounds__(kHopThreads, (S > 0 && S <= 16) ? 5 : 1) k_hop
             if (thread_copy) {
                 for (uint32_t k = 0; k < deg; ++k) stage(s_items, excl + k, r0, r1, o0 + k);
             } else if (thread_choice) {
-                need_warp = !select_thread<(S > 0 ? S : 1)>(hc, deg, p.fanout, o0, excl, r0, r1, s_items);
+                need_warp = !select_thread<(S > 0 ? S : 4)>(hc, deg, p.fanout, o0, excl, r0, r1, s_items, p.k32);
             } else {
                 need_warp = true;
             }
@@ -447,19 +467,42 @@ __global__ void __launch_bounds__(kHopThreads, (S > 0 && S <= 16) ? 5 : 1) k_hop
         } else {
             __syncthreads();
         }
-        // ---- phase 2b: coalesced emission of the staged items
+        // ---- phase 2b: coalesced emission of the staged items. Each thread keeps
+        // kEmit items in flight — column loads, then visited-word loads, then stores and
+        // the (rare) atomics — so the dependent-load chains of its items overlap.
         const uint32_t cnt = r1 > r0 ? r1 - r0 : 0;
         uint32_t* dst = out + (uint32_t)s_prefix + r0;
-#pragma unroll 4
-        for (uint32_t k = tid; k < cnt; k += kHopThreads) {
-            const uint64_t it = s_items[k];
-            const uint32_t code = (uint32_t)(it >> kTierShift);
-            const uint32_t* cols = code ? p.scols[code - 1] : p.ci;
-            uint32_t u = __ldg(cols + (it & kEdgeMask));
-            dst[k] = u;
-            if (bm) mark_visited(bm, sm, u);
+        for (uint32_t k0 = tid; k0 < cnt; k0 += kEmit * kHopThreads) {
+            uint32_t u[kEmit];
+#pragma unroll
+            for (int q = 0; q < kEmit; ++q) {
+                const uint32_t k = k0 + q * kHopThreads;
+                u[q] = 0;
+                if (k < cnt) {
+                    const uint64_t it = s_items[k];
+                    const uint32_t code = (uint32_t)(it >> kTierShift);
+                    const uint32_t* cols = code ? p.scols[code - 1] : p.ci;
+                    u[q] = __ldg(cols + (it & kEdgeMask));
+                }
+            }
+            if (bm) {
+                uint32_t w[kEmit];
+#pragma unroll
+                for (int q = 0; q < kEmit; ++q) w[q] = k0 + q * kHopThreads < cnt ? bm[u[q] >> 5] : ~0u;
+#pragma unroll
+                for (int q = 0; q < kEmit; ++q)
+                    if (k0 + q * kHopThreads < cnt) dst[k0 + q * kHopThreads] = u[q];
+#pragma unroll
+                for (int q = 0; q < kEmit; ++q)
+                    if (!((w[q] >> (u[q] & 31)) & 1u)) mark_visited_unchecked(bm, sm, u[q]);
+            } else {
+#pragma unroll
+                for (int q = 0; q < kEmit; ++q)
+                    if (k0 + q * kHopThreads < cnt) dst[k0 + q * kHopThreads] = u[q];
+            }
         }
-        __syncthreads();
+        // s_items is reused by the next round only; the last round exits without a barrier
+        if (r + 1 < rounds) __syncthreads();
     }
 }
 
@@ -550,6 +593,7 @@ int gc_hop_expand(const gc_topology_t* topo, const uint32_t* d_frontier, uint64_
     }
     p.mark_frontier = mark_frontier;
     p.exact_only = g_exact_only;
+    p.k32 = 32;
     p.cls = 64;
     p.u32b = 4;
     if (hot) {
