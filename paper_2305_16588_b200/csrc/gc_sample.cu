@@ -257,6 +257,18 @@ __device__ __forceinline__ void insert_slot(uint32_t (&t)[S], uint32_t x) {
     t[0] = min(t[0], x);
 }
 
+// Two candidates at once: with a < b, the k-th smallest of t U {a, b} is
+// min(t[k], max(t[k-1], a), max(t[k-2], b)) — a three-input VIMNMX3 plus two maxes
+// per slot for two candidates, against two ops per slot per candidate one at a time.
+template <int S>
+__device__ __forceinline__ void insert_pair(uint32_t (&t)[S], uint32_t x, uint32_t y) {
+    const uint32_t a = min(x, y), b = max(x, y);
+#pragma unroll
+    for (int s = S - 1; s >= 2; --s) t[s] = min(min(t[s], max(t[s - 1], a)), max(t[s - 2], b));
+    if (S > 1) t[1] = min(min(t[1], max(t[0], a)), b);
+    t[0] = min(t[0], a);
+}
+
 template <int S>
 __host__ __device__ constexpr int peeled_candidates() {
     return S == 4 ? 2 : S == 6 ? 5 : S == 8 ? 7 : S == 11 ? 9 : S == 16 ? 12 : S == 21 ? 17 : S == 26 ? 22 : 27;
@@ -266,19 +278,23 @@ template <int S>
 __device__ __forceinline__ bool select_thread(uint64_t hc, uint32_t deg, uint32_t fanout, uint64_t o0, uint32_t excl,
                                               uint32_t r0, uint32_t r1, uint64_t* s_items, uint32_t k32) {
     constexpr int IB = 7;
-    constexpr int TRI = peeled_candidates<S>();
+    constexpr uint32_t kKeep = ~((1u << IB) - 1u);
+    constexpr int TRI = peeled_candidates<S>() & ~1;  // peeled in pairs
     uint32_t t[S];
 #pragma unroll
     for (int s = 0; s < S; ++s) t[s] = 0xFFFFFFFFu;
     const PairHashHigh hh(hc);  // deg <= 64: key bits 63..38 from the specialised hash
 #pragma unroll
-    for (int j = 0; j < TRI; ++j) {
+    for (int j = 0; j < TRI; j += 2) {
         const uint32_t c = kGoldenLow + j;
-        insert_slot<S>(t, (hh.hi_counter(c, k32) & ~((1u << IB) - 1u)) | c);
+        insert_pair<S>(t, (hh.hi_counter(c, k32) & kKeep) | c, (hh.hi_counter(c + 1, k32) & kKeep) | (c + 1));
     }
-#pragma unroll 4
-    for (uint32_t c = kGoldenLow + TRI; c < kGoldenLow + deg; ++c)
-        insert_slot<S>(t, (hh.hi_counter(c, k32) & ~((1u << IB) - 1u)) | c);
+    const uint32_t cend = kGoldenLow + deg;
+    uint32_t c = kGoldenLow + TRI;
+#pragma unroll 2
+    for (; c + 1 < cend; c += 2)
+        insert_pair<S>(t, (hh.hi_counter(c, k32) & kKeep) | c, (hh.hi_counter(c + 1, k32) & kKeep) | (c + 1));
+    if (c < cend) insert_slot<S>(t, (hh.hi_counter(c, k32) & kKeep) | c);
     bool tie = false;
 #pragma unroll
     for (int s = 0; s + 1 < S; ++s) tie |= (s < (int)fanout) & ((t[s] >> IB) == (t[s + 1] >> IB));
@@ -314,7 +330,9 @@ __device__ __forceinline__ void select_warp(uint64_t hc, uint32_t d, uint32_t fa
     }
 }
 
-template <int S>
+// TIERED: the topology has a location table or lives in host memory, so rows resolve
+// through the tier rule and staged edges carry a slab code; otherwise the plain CSR.
+template <int S, bool TIERED>
 __global__ void __launch_bounds__(kHopThreads, (S > 0 && S <= 16) ? 5 : 1) k_hop_expand(HopParams p) {
     using Scan = cub::BlockScan<uint32_t, kHopThreads>;
     using Reduce = cub::BlockReduce<uint64_t, kHopThreads>;
@@ -343,10 +361,13 @@ __global__ void __launch_bounds__(kHopThreads, (S > 0 && S <= 16) ? 5 : 1) k_hop
     uint32_t v = 0, deg = 0, take = 0;
     uint64_t o0 = 0, hc = 0;
     // 0 local, 1 peer slab, 2 host; the full CSR is local unless it lives in host memory
-    int tier = (p.loc || p.full_on_host) ? 2 : 0;
+    int tier = TIERED ? 2 : 0;
     if (valid) {
         v = p.frontier[b * p.fstride + p0 + tid];
-        if (v < p.n) {
+        if (!TIERED && v < p.n) {
+            o0 = p.ro[v];
+            deg = (uint32_t)(p.ro[v + 1] - o0);
+        } else if (v < p.n) {
             const uint32_t L = p.loc ? __ldg(p.loc + v) : GC_TIER_HOST;
             if (L == GC_TIER_HOST) {
                 o0 = p.ro[v];
@@ -379,7 +400,7 @@ __global__ void __launch_bounds__(kHopThreads, (S > 0 && S <= 16) ? 5 : 1) k_hop
             }
         }
     }
-    if (p.tier_reads) {
+    if (TIERED && p.tier_reads) {
         // topology reads by tier: positions and sampled edges (PCIe bytes for the host tier)
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -480,9 +501,13 @@ __global__ void __launch_bounds__(kHopThreads, (S > 0 && S <= 16) ? 5 : 1) k_hop
                 u[q] = 0;
                 if (k < cnt) {
                     const uint64_t it = s_items[k];
-                    const uint32_t code = (uint32_t)(it >> kTierShift);
-                    const uint32_t* cols = code ? p.scols[code - 1] : p.ci;
-                    u[q] = __ldg(cols + (it & kEdgeMask));
+                    if (TIERED) {
+                        const uint32_t code = (uint32_t)(it >> kTierShift);
+                        const uint32_t* cols = code ? p.scols[code - 1] : p.ci;
+                        u[q] = __ldg(cols + (it & kEdgeMask));
+                    } else {
+                        u[q] = __ldg(p.ci + it);
+                    }
                 }
             }
             if (bm) {
@@ -524,6 +549,14 @@ static int network_slots(uint32_t fanout) {
     for (int s : sizes)
         if (fanout < (uint32_t)s) return s;
     return 0;
+}
+
+template <int S>
+static void launch_hop(const HopParams& p, unsigned grid, bool tiered, cudaStream_t s) {
+    if (tiered)
+        k_hop_expand<S, true><<<grid, kHopThreads, 0, s>>>(p);
+    else
+        k_hop_expand<S, false><<<grid, kHopThreads, 0, s>>>(p);
 }
 
 }  // namespace gc
@@ -609,16 +642,17 @@ int gc_hop_expand(const gc_topology_t* topo, const uint32_t* d_frontier, uint64_
     GC_TRY(cudaMemsetAsync(d_temp, 0, state_bytes + 256, s), "gc_hop_expand memset");
     const uint64_t grid = (uint64_t)num_batches * tiles;
     GC_REQUIRE(grid < (1ull << 31), GC_ERR_VALUE, "gc_hop_expand: window too large");
+    const bool tiered = topo->location != nullptr || topo->full_on_host;
     switch (network_slots(fanout)) {
-        case 4: k_hop_expand<4><<<(unsigned)grid, kHopThreads, 0, s>>>(p); break;
-        case 6: k_hop_expand<6><<<(unsigned)grid, kHopThreads, 0, s>>>(p); break;
-        case 8: k_hop_expand<8><<<(unsigned)grid, kHopThreads, 0, s>>>(p); break;
-        case 11: k_hop_expand<11><<<(unsigned)grid, kHopThreads, 0, s>>>(p); break;
-        case 16: k_hop_expand<16><<<(unsigned)grid, kHopThreads, 0, s>>>(p); break;
-        case 21: k_hop_expand<21><<<(unsigned)grid, kHopThreads, 0, s>>>(p); break;
-        case 26: k_hop_expand<26><<<(unsigned)grid, kHopThreads, 0, s>>>(p); break;
-        case 32: k_hop_expand<32><<<(unsigned)grid, kHopThreads, 0, s>>>(p); break;
-        default: k_hop_expand<0><<<(unsigned)grid, kHopThreads, 0, s>>>(p); break;
+        case 4: launch_hop<4>(p, (unsigned)grid, tiered, s); break;
+        case 6: launch_hop<6>(p, (unsigned)grid, tiered, s); break;
+        case 8: launch_hop<8>(p, (unsigned)grid, tiered, s); break;
+        case 11: launch_hop<11>(p, (unsigned)grid, tiered, s); break;
+        case 16: launch_hop<16>(p, (unsigned)grid, tiered, s); break;
+        case 21: launch_hop<21>(p, (unsigned)grid, tiered, s); break;
+        case 26: launch_hop<26>(p, (unsigned)grid, tiered, s); break;
+        case 32: launch_hop<32>(p, (unsigned)grid, tiered, s); break;
+        default: launch_hop<0>(p, (unsigned)grid, tiered, s); break;
     }
     GC_CHECK_LAUNCH("gc_hop_expand");
     return GC_OK;
