@@ -50,7 +50,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--window", type=int, default=0, help="batches per launch window (0 = whole epoch)")
+    ap.add_argument("--window", type=int, default=0,
+                    help="batches per launch window (0 = whole epoch / lanes*2 windows when lanes > 1)")
+    ap.add_argument("--lanes", type=int, default=1, help="concurrent window lanes (inter-batch pipeline streams)")
     ap.add_argument("--num-vertices", type=int, default=CONFIG["num_vertices"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -270,10 +272,10 @@ def run_b200(args):
     table = synthetic_features_device(0, g.num_vertices, dim)  # fully HBM-resident feature table
     store = FeatureStore.resident(table)
     nb = math.ceil(len(pool) / cfg.batch_size)
-    window = args.window or nb
+    window = args.window or (nb if args.lanes == 1 else math.ceil(nb / (2 * args.lanes)))
     # per-batch distinct rows stay far below the 938K worst case; 64K keeps the
     # window's gather buffer small, and the run checks it never overflowed
-    pipe = SampleGatherPipeline(g, cfg, store, len(pool), window=window, feat_rows_cap=65536)
+    pipe = SampleGatherPipeline(g, cfg, store, len(pool), window=window, feat_rows_cap=65536, lanes=args.lanes)
     root = KeyedRng(cfg.seed)
     clique, local_idx = layout.gpu_position(rank)
     plans = [pipe.plan_epoch(pool, root.derive(e, clique, local_idx)) for e in range(args.warmup + args.steps)]
@@ -298,8 +300,6 @@ def run_b200(args):
     if world > 1:
         dist.barrier()
 
-    timer = StageTimer()
-    pipe.timer = timer
     pipe.launches = 0
     step_ms = []
     with ClockSampler(device) as clocks:
@@ -317,13 +317,23 @@ def run_b200(args):
         if world > 1:
             dist.barrier()
     launches = pipe.launches
-    pipe.timer = None
+    # per-kernel durations for the roofline: the same epochs again, one window after
+    # another on one stream (kernels timed alone, not sharing the GPU), untimed overall
+    seq = pipe if args.lanes == 1 else SampleGatherPipeline(g, cfg, store, len(pool), window=window,
+                                                              feat_rows_cap=65536, lanes=1)
+    timer = StageTimer()
+    seq.timer = timer
+    for s in range(args.steps):
+        flush.zero_()
+        seq.run_epoch(plans[args.warmup + s])
+    seq.timer = None
     # algorithmic bytes of the timed epochs (recomputed, identical streams: untimed)
     for s in range(args.steps):
-        pipe.run_epoch(plans[args.warmup + s], on_window=account)
+        seq.run_epoch(plans[args.warmup + s], on_window=account)
     torch.cuda.synchronize()
-    if stats["max_unique"] > pipe.feat_cap:
+    if stats["max_unique"] > seq.feat_cap:
         raise RuntimeError("gather capacity overflow: raise feat_rows_cap")
+    pipe = seq
 
     total_ms = float(sum(step_ms))
     if world > 1:
@@ -357,7 +367,7 @@ def run_b200(args):
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u64", "data": "synthetic (reference generator law, PCG64 draws; random fp32 features)",
         "config": {**CONFIG, "num_vertices": args.num_vertices, "batches_per_step_per_gpu": nb,
-                   "window_batches": pipe.window, "parallelism": f"dp{world} (tablet per GPU, no data-path collective)",
+                   "window_batches": pipe.window, "lanes": args.lanes, "parallelism": f"dp{world} (tablet per GPU, no data-path collective)",
                    "l2": "flushed (256 MB write) between timed steps; graph+features 1.2 GB > L2"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,

@@ -39,6 +39,10 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--window", type=int, default=256)
+    ap.add_argument("--lanes", type=int, default=2, help="concurrent window lanes (inter-batch pipeline)")
+    ap.add_argument("--sweep-lanes", default="", help="extra lanes values to time after the main run, e.g. 1,3,2d (d: host rows deferred)")
+    ap.add_argument("--pcie-gbs", type=float, default=64.0, help="nominal PCIe Gen5 x16 GB/s for the tier roofline")
+    ap.add_argument("--nvlink-gbs", type=float, default=900.0, help="NVLink 5 GB/s per direction")
     a = ap.parse_args()
 
     import torch
@@ -89,7 +93,7 @@ def main():
     pool = pools[0]
     nb = math.ceil(len(pool) / bs)
     pipe = SampleGatherPipeline(g, cfg, fstore, len(pool), window=min(a.window, nb), feat_rows_cap=60_000,
-                                topology=topo)
+                                topology=topo, lanes=a.lanes)
     root = P.KeyedRng(P.derive_seed(7, 5))
     plans = [pipe.plan_epoch(pool, root.derive(e, 0, 0)) for e in range(a.warmup + a.steps)]
     setup_s = time.perf_counter() - t_setup
@@ -98,8 +102,6 @@ def main():
     torch.cuda.synchronize()
     topo.reset_counters()
     fstore.reset_counters()
-    timer = StageTimer()
-    pipe.timer = timer
     ms = []
     for s in range(a.steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -108,13 +110,61 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         ms.append(e0.elapsed_time(e1))
+    # stage durations and algorithmic bytes: the same epochs once more on one lane
+    # (kernels timed alone); tier counters are read before this pass
     t, f = topo.tier_counts(), fstore.tier_counts()
+    sweep = {}
+    for tag in [x for x in a.sweep_lanes.split(",") if x]:
+        lanes, defer = int(tag.rstrip("d")), tag.endswith("d")  # "2d": two lanes, host rows deferred
+        del pipe
+        torch.cuda.empty_cache()
+        pipe = SampleGatherPipeline(g, cfg, fstore, len(pool), window=min(a.window, nb), feat_rows_cap=60_000,
+                                    topology=topo, lanes=lanes, defer_host=defer)
+        pipe.run_epoch(plans[0])
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for s in range(a.steps):
+            pipe.run_epoch(plans[a.warmup + s])
+        e1.record()
+        torch.cuda.synchronize()
+        sweep[tag] = nb * a.steps / (e0.elapsed_time(e1) / 1000.0)
+    seq = pipe
+    if a.lanes > 1 or sweep:
+        del pipe
+        torch.cuda.empty_cache()
+        seq = SampleGatherPipeline(g, cfg, fstore, len(pool), window=min(a.window, nb), feat_rows_cap=60_000,
+                                   topology=topo, lanes=1)
+    timer = StageTimer()
+    seq.timer = timer
+    acc = {"sampling": 0, "dedup": 0, "gather": 0}
+
+    def account(p, w0, nbw):
+        wb = p.window_bytes(nbw)
+        for k in acc:
+            acc[k] += wb[k]
+
+    for s in range(a.steps):
+        seq.run_epoch(plans[a.warmup + s])
+    seq.timer = None
+    for s in range(a.steps):
+        seq.run_epoch(plans[a.warmup + s], on_window=account)
+    torch.cuda.synchronize()
     batches = nb * a.steps
     row_txns = PL.feature_row_transactions(feat, spec)
     cls = spec.cache_line_bytes
     measured_txn = t["host_txn"] + f["host"] * row_txns
     pred_txn = est.total_txns
     stages = {k: v[1] / a.steps for k, v in timer.summary().items()}
+    # tier roofline (north star): per batch, max over tiers of bytes / bandwidth
+    row = feat.row_bytes
+    pcie_b = t["reads_host"] * 16 + t["edges_host"] * 4 + f["host"] * row
+    nvl_b = t["reads_peer"] * 16 + t["edges_peer"] * 4 + f["peer"] * row
+    hbm_b = acc["sampling"] + acc["dedup"] + acc["gather"] - pcie_b - nvl_b
+    hbm_gbs = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
+    t_tier = {"hbm": hbm_b / batches / (hbm_gbs * 1e9), "nvlink": nvl_b / batches / (a.nvlink_gbs * 1e9),
+              "pcie": pcie_b / batches / (a.pcie_gbs * 1e9)}
+    t_roof = max(t_tier.values())
+    t_meas = sum(ms) / 1000.0 / batches
     out = {
         "metric": "three-tier sampled+gathered batches/s; PCIe GB/batch vs plan prediction",
         "value": batches / (sum(ms) / 1000.0),
@@ -134,6 +184,15 @@ def main():
             / batches / 1e9,
             "unit_note": "transactions x 64 B cache lines, the reference's PCIe unit (SPEC.md:403)",
         },
+        "tier_roofline": {
+            "bytes_per_batch": {"hbm": hbm_b / batches, "nvlink": nvl_b / batches, "pcie": pcie_b / batches},
+            "gbs": {"hbm": hbm_gbs, "nvlink": a.nvlink_gbs, "pcie": a.pcie_gbs},
+            "t_us_per_batch": {k: v * 1e6 for k, v in t_tier.items()},
+            "bound": max(t_tier, key=t_tier.get), "t_roof_us_per_batch": t_roof * 1e6,
+            "measured_us_per_batch": t_meas * 1e6, "frac": t_roof / t_meas,
+        },
+        "lanes": a.lanes,
+        "lane_sweep_batches_per_s": sweep,
         "tiers_per_batch": {**{k: v / batches for k, v in t.items()}, **{f"rows_{k}": v / batches for k, v in f.items()}},
         "stages_ms_per_epoch": stages,
         "setup_s": {"total": setup_s, "presampling": t_pre, "plan": t_plan, "cache_fill": t_fill},

@@ -50,6 +50,9 @@ int gc_abi_version(void);
  * 32-bit REDUX extraction and always use the 64-bit path (a test hook: both paths
  * must give identical output). */
 #define GC_OPT_EXACT_SELECTION 1
+/* GC_OPT_DEFER_CTAS: CTAs (128 threads each) of gc_gather_deferred's host-row kernel
+ * (default 148, one per SM); a tuning knob for the PCIe-bound part. */
+#define GC_OPT_DEFER_CTAS 2
 int gc_set_option(int option, int value);
 const char* gc_last_error(void);
 /* device ordinal of the calling thread's current device; -1 if none */
@@ -207,6 +210,20 @@ int gc_gather(const gc_feature_store_t* store, const uint32_t* d_ids, uint64_t i
               const uint32_t* d_count, uint32_t max_count, uint32_t num_batches, void* d_out,
               uint64_t out_stride_rows, uint64_t* d_tier_rows, void* stream);
 
+/* Same result as gc_gather, scheduled for overlap: rows of the local and peer tiers
+ * are copied by the full-width kernel, host-tier rows are appended to `d_defer`
+ * (gc_gather_defer_bytes(max_count, num_batches) bytes of device memory) and copied
+ * by a second, small-grid kernel on `host_stream` (NULL: the same stream; `stream`
+ * waits for it either way). The PCIe-bound part then
+ * occupies ~1 CTA per SM and runs under the next window's sampling on another
+ * stream (Legion's inter-batch pipeline). Falls back to gc_gather's
+ * schedule when the store has no host tier or rows are not 16-byte vectors. */
+uint64_t gc_gather_defer_bytes(uint32_t max_count, uint32_t num_batches);
+int gc_gather_deferred(const gc_feature_store_t* store, const uint32_t* d_ids, uint64_t ids_stride,
+                       const uint32_t* d_count, uint32_t max_count, uint32_t num_batches, void* d_out,
+                       uint64_t out_stride_rows, uint64_t* d_tier_rows, void* d_defer, uint64_t defer_bytes,
+                       void* stream, void* host_stream);
+
 /* Deterministic synthetic feature rows [first_row, first_row+rows) of a dim-wide fp32
  * table: X[v,d] = (mix64(v*dim+d) >> 40) * 2^-24 - 0.5 (bench/test input only). */
 int gc_synth_features(uint64_t first_row, uint64_t rows, uint32_t dim, float* d_out, void* stream);
@@ -265,6 +282,14 @@ int gc_tier_account(const uint64_t* d_row_offsets, int64_t n, const uint64_t* d_
 /* Register host memory as mapped, read-only pinned memory (UVA host tier). */
 int gc_host_register(void* host_ptr, size_t bytes, void** d_alias);
 int gc_host_unregister(void* host_ptr);
+
+/* Host tier through the CUDA VMM API (cuMemCreate, CU_MEM_LOCATION_TYPE_HOST_NUMA):
+ * pinned host memory mapped for the CPU and every GPU at one address with the
+ * allocation granularity as the GPU page size (2 MB), so random UVA row reads over a
+ * large host table miss the GPU TLB far less than with cudaHostAlloc's 4 KB pages.
+ * `*mapped_bytes` (bytes rounded up to the granularity) must be passed to the free. */
+int gc_host_alloc_numa(size_t bytes, int numa_node, void** ptr, size_t* mapped_bytes);
+int gc_host_free_numa(void* ptr, size_t mapped_bytes);
 /* Cross-process NVLink peer slabs: 64-byte cudaIpcMemHandle_t export/import. */
 int gc_ipc_export(void* d_ptr, uint8_t* handle64);
 int gc_ipc_import(const uint8_t* handle64, void** d_ptr);

@@ -24,6 +24,7 @@ GC_ERR_UNSUPPORTED = -4
 GC_ERR_ASSERT = -5
 GC_MAX_PEERS = 8
 GC_OPT_EXACT_SELECTION = 1
+GC_OPT_DEFER_CTAS = 2
 GC_TIER_HOST = 0xFFFFFFFF
 
 _c_u64p = ctypes.c_void_p  # every device pointer crosses as an opaque address
@@ -130,7 +131,12 @@ SIGNATURES = {
     "gc_mark_holders": (ctypes.c_int, [V, I64, U32, V, V]),
     "gc_tier_account": (ctypes.c_int, [V, I64, V, V, V, V, U32, U32, U32, U32, U32, V, V]),
     "gc_host_register": (ctypes.c_int, [V, SZ, ctypes.POINTER(ctypes.c_void_p)]),
+    "gc_gather_defer_bytes": (U64, [U32, U32]),
+    "gc_gather_deferred": (ctypes.c_int,
+                           [ctypes.POINTER(GcFeatureStore), V, U64, V, U32, U32, V, U64, V, V, U64, V, V]),
     "gc_host_unregister": (ctypes.c_int, [V]),
+    "gc_host_alloc_numa": (ctypes.c_int, [SZ, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(SZ)]),
+    "gc_host_free_numa": (ctypes.c_int, [V, SZ]),
     "gc_ipc_export": (ctypes.c_int, [V, ctypes.c_char_p]),
     "gc_ipc_import": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]),
     "gc_ipc_close": (ctypes.c_int, [V]),

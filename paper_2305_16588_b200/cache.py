@@ -112,6 +112,7 @@ class FeatureStore:
     host_table: torch.Tensor | None = None  # pinned fp32 [n, D]
     tier_rows: torch.Tensor = field(default=None)  # u64[3] cumulative rows served per tier
     _keep: list = field(default_factory=list, repr=False)
+    _defer: dict = field(default_factory=dict, repr=False)  # stream handle -> deferred-row list buffer
 
     def __post_init__(self):
         if self.tier_rows is None:
@@ -171,19 +172,36 @@ class FeatureStore:
 
     # ---------------------------------------------------------------- gather
     def gather(self, ids: torch.Tensor, counts: torch.Tensor, out: torch.Tensor, num_batches: int | None = None,
-               stream=None) -> torch.Tensor:
+               stream=None, deferred: bool = False, host_stream=None) -> torch.Tensor:
         """out[b, k] = X[ids[b, k]] for k < min(counts[b], out.shape[1]) (K4).
 
-        ids: int32 [W, cap] CUDA, counts: int32 [W] CUDA, out: float32 [W, rows, D]."""
+        ids: int32 [W, cap] CUDA, counts: int32 [W] CUDA, out: float32 [W, rows, D].
+        deferred: host-tier rows are copied by a second small-grid kernel
+        (gc_gather_deferred) — on `host_stream` when given — so the PCIe-bound part
+        overlaps other streams' work; `stream` is ordered after it either way."""
         lib = _lib.lib()
         if ids.dim() == 1:
             ids, out = ids.view(1, -1), out.view(1, *out.shape)
         W = ids.shape[0] if num_batches is None else num_batches
         if out.shape[-1] * 4 != self.spec.row_bytes:
             raise ValueError("output row width does not match the feature store")
+        s = _lib.stream_handle(stream)
+        if deferred and self.host_table is not None and self.location is not None:
+            need = int(lib.gc_gather_defer_bytes(out.shape[1], W))
+            buf = self._defer.get(s)
+            if buf is None or buf.numel() < need:
+                buf = torch.empty(need, dtype=torch.uint8, device="cuda")
+                self._defer[s] = buf  # one list per stream: concurrent lanes never share it
+            _lib.check(
+                lib.gc_gather_deferred(self.c_struct, ids.data_ptr(), ids.shape[1], counts.data_ptr(), out.shape[1],
+                                       W, out.data_ptr(), out.shape[1], self.tier_rows.data_ptr(), buf.data_ptr(),
+                                       buf.numel(), s, _lib.stream_handle(host_stream) if host_stream else None),
+                "gather_deferred",
+            )
+            return out
         _lib.check(
             lib.gc_gather(self.c_struct, ids.data_ptr(), ids.shape[1], counts.data_ptr(), out.shape[1], W,
-                          out.data_ptr(), out.shape[1], self.tier_rows.data_ptr(), _lib.stream_handle(stream)),
+                          out.data_ptr(), out.shape[1], self.tier_rows.data_ptr(), s),
             "gather",
         )
         return out

@@ -11,8 +11,17 @@
 
 namespace gc {
 
+// deferred host-tier row: destination row index in `out` and the vertex id
+struct DeferredRow {
+    uint64_t dst_row;
+    uint32_t id;
+    uint32_t pad;
+};
+
 struct GatherParams {
     gc_feature_store_t fs;
+    DeferredRow* defer;  // non-null: host-tier rows are listed here instead of read
+    uint32_t* defer_count;
     const uint32_t* ids;
     uint64_t ids_stride;
     const uint32_t* count;
@@ -119,7 +128,30 @@ __global__ void __launch_bounds__(256) k_gather_rows(GatherParams p) {
         // lanes 0..ROWS-1 resolve one row each
         const char* my_src = nullptr;
         int my_tier = 0;
-        if (lane < ROWS && r0 + lane < rows) my_src = row_source(p.fs, __ldg(ids + r0 + lane), my_tier);
+        uint32_t my_id = 0;
+        if (lane < ROWS && r0 + lane < rows) {
+            my_id = __ldg(ids + r0 + lane);
+            my_src = row_source(p.fs, my_id, my_tier);
+        }
+        if (p.defer) {
+            // host rows go to the deferred list (read later by a few warps over PCIe,
+            // while the next window samples); one atomic per warp
+            const bool d = my_src != nullptr && my_tier == 2;
+            const unsigned m = __ballot_sync(kFull, d);
+            if (m) {
+                uint32_t base = 0;
+                if (lane == __ffs(m) - 1) base = atomicAdd(p.defer_count, (uint32_t)__popc(m));
+                base = __shfl_sync(kFull, base, __ffs(m) - 1);
+                if (d) {
+                    DeferredRow e;
+                    e.dst_row = (uint64_t)b * p.out_stride_rows + r0 + lane;
+                    e.id = my_id;
+                    e.pad = 0;
+                    p.defer[base + __popc(m & ((1u << lane) - 1u))] = e;
+                    my_src = nullptr;
+                }
+            }
+        }
         uint4 v[ROWS];
 #pragma unroll
         for (int j = 0; j < ROWS; ++j) {
@@ -128,7 +160,8 @@ __global__ void __launch_bounds__(256) k_gather_rows(GatherParams p) {
         }
 #pragma unroll
         for (int j = 0; j < ROWS; ++j) {
-            if (r0 + j < rows && (uint32_t)lane < per_row)
+            const bool have = __shfl_sync(kFull, my_src != nullptr, j);
+            if (have && (uint32_t)lane < per_row)
                 st_stream16(out + (uint64_t)(r0 + j) * p.fs.row_bytes + 16 * lane, v[j]);
         }
         if (lane < ROWS && r0 + lane < rows) {
@@ -148,6 +181,44 @@ __global__ void __launch_bounds__(256) k_gather_rows(GatherParams p) {
         __syncthreads();
         if (threadIdx.x < 3 && s_tier[threadIdx.x])
             atomicAdd((unsigned long long*)(p.tier_rows + threadIdx.x), s_tier[threadIdx.x]);
+    }
+}
+
+static int g_defer_ctas = 148;
+void set_defer_ctas(int ctas) { g_defer_ctas = ctas; }
+
+// Deferred host-tier rows: warp per row, ROWS rows in flight per warp, a small grid
+// (PCIe latency needs few rows in flight; the SMs stay free for the next window).
+template <int ROWS>
+__global__ void __launch_bounds__(128) k_gather_deferred(const char* __restrict__ host_rows, uint32_t row_bytes,
+                                                         const DeferredRow* __restrict__ list,
+                                                         const uint32_t* __restrict__ count, char* out) {
+    const uint32_t n = *count;
+    const uint32_t per_row = row_bytes / 16;
+    const int lane = threadIdx.x & 31;
+    const uint32_t warps = gridDim.x * (blockDim.x / 32);
+    const uint32_t wid = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    for (uint32_t r0 = wid * ROWS; r0 < n; r0 += warps * ROWS) {
+        uint64_t my_dst = 0;
+        uint32_t my_id = 0;
+        if (lane < ROWS && r0 + lane < n) {
+            const DeferredRow e = list[r0 + lane];
+            my_dst = e.dst_row;
+            my_id = e.id;
+        }
+        uint4 v[ROWS];
+#pragma unroll
+        for (int j = 0; j < ROWS; ++j) {
+            const uint32_t id = __shfl_sync(kFull, my_id, j);
+            v[j] = (r0 + j < n && (uint32_t)lane < per_row)
+                       ? ld_stream16(host_rows + (uint64_t)id * row_bytes + 16 * lane)
+                       : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int j = 0; j < ROWS; ++j) {
+            const uint64_t dst = __shfl_sync(kFull, my_dst, j);
+            if (r0 + j < n && (uint32_t)lane < per_row) st_stream16(out + dst * row_bytes + 16 * lane, v[j]);
+        }
     }
 }
 
@@ -193,9 +264,12 @@ using namespace gc;
 
 extern "C" {
 
-int gc_gather(const gc_feature_store_t* store, const uint32_t* d_ids, uint64_t ids_stride, const uint32_t* d_count,
-              uint32_t max_count, uint32_t num_batches, void* d_out, uint64_t out_stride_rows, uint64_t* d_tier_rows,
-              void* stream) {
+uint64_t gc_gather_defer_bytes(uint32_t max_count, uint32_t num_batches);
+
+static int gather_impl(const gc_feature_store_t* store, const uint32_t* d_ids, uint64_t ids_stride,
+                       const uint32_t* d_count, uint32_t max_count, uint32_t num_batches, void* d_out,
+                       uint64_t out_stride_rows, uint64_t* d_tier_rows, void* d_defer, uint64_t defer_bytes,
+                       void* stream, void* host_stream) {
     GC_REQUIRE(store, GC_ERR_VALUE, "gc_gather: store is null");
     GC_REQUIRE(store->row_bytes > 0 && store->row_bytes % 4 == 0, GC_ERR_VALUE,
                "gc_gather: row_bytes must be a positive multiple of 4");
@@ -213,6 +287,15 @@ int gc_gather(const gc_feature_store_t* store, const uint32_t* d_ids, uint64_t i
     p.max_rows = max_count;
     const bool vec16 = store->row_bytes % 16 == 0 && ((uintptr_t)d_out % 16 == 0);
     const uint32_t per_row = store->row_bytes / (vec16 ? 16 : 4);
+    cudaStream_t s = as_stream(stream);
+    const bool defer = d_defer != nullptr && vec16 && per_row <= 32 && store->location && store->host_rows;
+    if (defer) {
+        GC_REQUIRE(defer_bytes >= gc_gather_defer_bytes(max_count, num_batches), GC_ERR_VALUE,
+                   "gc_gather_deferred: defer buffer too small");
+        p.defer_count = static_cast<uint32_t*>(d_defer);
+        p.defer = reinterpret_cast<DeferredRow*>(static_cast<char*>(d_defer) + 256);
+        GC_TRY(cudaMemsetAsync(p.defer_count, 0, sizeof(uint32_t), s), "gc_gather_deferred memset");
+    }
     uint64_t work = (uint64_t)max_count * per_row;
     uint64_t gx = (work + 255) / 256;
     // enough CTAs to fill 148 SMs for the whole window; grid-stride beyond that
@@ -226,14 +309,57 @@ int gc_gather(const gc_feature_store_t* store, const uint32_t* d_ids, uint64_t i
         const uint64_t wcap = (uint64_t)148 * 16 / num_batches;
         if (wx > wcap) wx = wcap;
         if (wx < 1) wx = 1;
-        k_gather_rows<4><<<dim3((unsigned)wx, num_batches), 256, 0, as_stream(stream)>>>(p);
+        k_gather_rows<4><<<dim3((unsigned)wx, num_batches), 256, 0, s>>>(p);
     } else if (vec16) {
-        k_gather<16><<<grid, 256, 0, as_stream(stream)>>>(p);
+        k_gather<16><<<grid, 256, 0, s>>>(p);
     } else {
-        k_gather<4><<<grid, 256, 0, as_stream(stream)>>>(p);
+        k_gather<4><<<grid, 256, 0, s>>>(p);
     }
     GC_CHECK_LAUNCH("gc_gather");
+    if (defer) {
+        // one 4-warp CTA per SM, 8 rows in flight per warp: ~4.7K rows of PCIe reads
+        // outstanding, while the rest of every SM is free for the next window's kernels.
+        // On a separate (high-priority) stream its CTAs take SM slots as soon as any
+        // free up; `stream` then waits for it, so consumers of `out` stay ordered.
+        cudaStream_t hs = host_stream ? as_stream(host_stream) : s;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (hs != s) {
+            GC_TRY(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming), "event");
+            GC_TRY(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming), "event");
+            GC_TRY(cudaEventRecord(e0, s), "event record");
+            GC_TRY(cudaStreamWaitEvent(hs, e0, 0), "stream wait");
+        }
+        k_gather_deferred<8><<<g_defer_ctas, 128, 0, hs>>>(static_cast<const char*>(store->host_rows), store->row_bytes,
+                                                   p.defer, p.defer_count, p.out);
+        GC_CHECK_LAUNCH("gc_gather_deferred");
+        if (hs != s) {
+            GC_TRY(cudaEventRecord(e1, hs), "event record");
+            GC_TRY(cudaStreamWaitEvent(s, e1, 0), "stream wait");
+            cudaEventDestroy(e0);  // released once complete
+            cudaEventDestroy(e1);
+        }
+    }
     return GC_OK;
+}
+
+uint64_t gc_gather_defer_bytes(uint32_t max_count, uint32_t num_batches) {
+    return 256 + (uint64_t)max_count * num_batches * sizeof(DeferredRow);
+}
+
+int gc_gather(const gc_feature_store_t* store, const uint32_t* d_ids, uint64_t ids_stride, const uint32_t* d_count,
+              uint32_t max_count, uint32_t num_batches, void* d_out, uint64_t out_stride_rows, uint64_t* d_tier_rows,
+              void* stream) {
+    return gather_impl(store, d_ids, ids_stride, d_count, max_count, num_batches, d_out, out_stride_rows,
+                       d_tier_rows, nullptr, 0, stream, nullptr);
+}
+
+int gc_gather_deferred(const gc_feature_store_t* store, const uint32_t* d_ids, uint64_t ids_stride,
+                       const uint32_t* d_count, uint32_t max_count, uint32_t num_batches, void* d_out,
+                       uint64_t out_stride_rows, uint64_t* d_tier_rows, void* d_defer, uint64_t defer_bytes,
+                       void* stream, void* host_stream) {
+    GC_REQUIRE(d_defer, GC_ERR_VALUE, "gc_gather_deferred: defer buffer is null");
+    return gather_impl(store, d_ids, ids_stride, d_count, max_count, num_batches, d_out, out_stride_rows,
+                       d_tier_rows, d_defer, defer_bytes, stream, host_stream);
 }
 
 int gc_synth_features(uint64_t first_row, uint64_t rows, uint32_t dim, float* d_out, void* stream) {

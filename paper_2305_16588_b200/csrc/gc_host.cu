@@ -1,0 +1,126 @@
+// Host tier allocation for UVA zero-copy reads (the uncached rows of Legion's
+// unified cache, read by K2/K4 over PCIe).
+//
+// gc_host_alloc_numa maps host memory through the CUDA VMM API
+// (cuMemCreate with CU_MEM_LOCATION_TYPE_HOST_NUMA): the GPU page tables then map the
+// host tier with the allocation granularity (2 MB pages) instead of the 4 KB pages of
+// cudaHostAlloc/cudaHostRegister, which multiplies the GPU TLB reach over a
+// tens-of-GB table read at random. The same virtual address is valid on the CPU.
+// Driver entry points come from cudaGetDriverEntryPoint, so the library has no
+// link-time dependency on libcuda (it still loads on a CPU-only host).
+#include <cuda.h>
+
+#include <mutex>
+
+#include "gc_common.cuh"
+
+namespace gc {
+
+struct DriverVmm {
+    decltype(&cuMemGetAllocationGranularity) granularity = nullptr;
+    decltype(&cuMemCreate) create = nullptr;
+    decltype(&cuMemAddressReserve) reserve = nullptr;
+    decltype(&cuMemMap) map = nullptr;
+    decltype(&cuMemSetAccess) access = nullptr;
+    decltype(&cuMemUnmap) unmap = nullptr;
+    decltype(&cuMemRelease) release = nullptr;
+    decltype(&cuMemAddressFree) free_va = nullptr;
+    decltype(&cuMemRetainAllocationHandle) retain = nullptr;
+    bool ok = false;
+};
+
+static DriverVmm& vmm() {
+    static DriverVmm d;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        auto get = [](const char* name, void** fn) {
+            cudaDriverEntryPointQueryResult q;
+            return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess &&
+                   q == cudaDriverEntryPointSuccess && *fn != nullptr;
+        };
+        d.ok = get("cuMemGetAllocationGranularity", (void**)&d.granularity) && get("cuMemCreate", (void**)&d.create) &&
+               get("cuMemAddressReserve", (void**)&d.reserve) && get("cuMemMap", (void**)&d.map) &&
+               get("cuMemSetAccess", (void**)&d.access) && get("cuMemUnmap", (void**)&d.unmap) &&
+               get("cuMemRelease", (void**)&d.release) && get("cuMemAddressFree", (void**)&d.free_va) &&
+               get("cuMemRetainAllocationHandle", (void**)&d.retain);
+    });
+    return d;
+}
+
+static int drv(CUresult r, const char* what) {
+    if (r == CUDA_SUCCESS) return GC_OK;
+    set_error(std::string(what) + " failed (CUresult " + std::to_string((int)r) + ")");
+    return GC_ERR_CUDA;
+}
+
+static CUmemAllocationProp host_prop(int numa_node) {
+    CUmemAllocationProp prop{};
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_HOST_NUMA;
+    prop.location.id = numa_node;
+    return prop;
+}
+
+}  // namespace gc
+
+using namespace gc;
+
+extern "C" {
+
+int gc_host_alloc_numa(size_t bytes, int numa_node, void** ptr, size_t* mapped_bytes) {
+    GC_REQUIRE(ptr && mapped_bytes && bytes > 0, GC_ERR_VALUE, "gc_host_alloc_numa: bad arguments");
+    DriverVmm& d = vmm();
+    GC_REQUIRE(d.ok, GC_ERR_UNSUPPORTED, "gc_host_alloc_numa: CUDA VMM driver entry points unavailable");
+    int dev = 0;
+    GC_TRY(cudaGetDevice(&dev), "cudaGetDevice");
+    GC_TRY(cudaFree(nullptr), "context init");  // the driver calls below need a current context
+    CUmemAllocationProp prop = host_prop(numa_node);
+    size_t gran = 0;
+    if (int e = drv(d.granularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED), "cuMemGetAllocationGranularity"))
+        return e;
+    const size_t size = align_up(bytes, gran);
+    CUmemGenericAllocationHandle h;
+    if (int e = drv(d.create(&h, size, &prop, 0), "cuMemCreate(host NUMA)")) return e;
+    CUdeviceptr va = 0;
+    if (int e = drv(d.reserve(&va, size, gran, 0, 0), "cuMemAddressReserve")) {
+        d.release(h);
+        return e;
+    }
+    if (int e = drv(d.map(va, size, 0, h, 0), "cuMemMap")) {
+        d.free_va(va, size);
+        d.release(h);
+        return e;
+    }
+    d.release(h);  // the mapping keeps the allocation alive until it is unmapped
+    int ndev = 0;
+    GC_TRY(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    CUmemAccessDesc desc[GC_MAX_PEERS + 1];
+    int nd = 0;
+    desc[nd].location.type = CU_MEM_LOCATION_TYPE_HOST_NUMA;  // CPU access through the same address
+    desc[nd].location.id = numa_node;
+    desc[nd++].flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    for (int g = 0; g < ndev && nd < GC_MAX_PEERS + 1; ++g) {
+        desc[nd].location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        desc[nd].location.id = g;
+        desc[nd++].flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    }
+    if (int e = drv(d.access(va, size, desc, nd), "cuMemSetAccess")) {
+        d.unmap(va, size);
+        d.free_va(va, size);
+        return e;
+    }
+    *ptr = reinterpret_cast<void*>(va);
+    *mapped_bytes = size;
+    return GC_OK;
+}
+
+int gc_host_free_numa(void* ptr, size_t mapped_bytes) {
+    GC_REQUIRE(ptr, GC_ERR_VALUE, "gc_host_free_numa: null pointer");
+    DriverVmm& d = vmm();
+    GC_REQUIRE(d.ok, GC_ERR_UNSUPPORTED, "gc_host_free_numa: CUDA VMM driver entry points unavailable");
+    const CUdeviceptr va = reinterpret_cast<CUdeviceptr>(ptr);
+    if (int e = drv(d.unmap(va, mapped_bytes), "cuMemUnmap")) return e;
+    return drv(d.free_va(va, mapped_bytes), "cuMemAddressFree");
+}
+
+}  // extern "C"

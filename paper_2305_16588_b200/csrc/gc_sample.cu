@@ -566,6 +566,11 @@ using namespace gc;
 extern "C" {
 
 int gc_set_option(int option, int value) {
+    if (option == GC_OPT_DEFER_CTAS) {
+        GC_REQUIRE(value >= 1 && value <= 65535, GC_ERR_VALUE, "gc_set_option: GC_OPT_DEFER_CTAS out of range");
+        gc::set_defer_ctas(value);
+        return GC_OK;
+    }
     GC_REQUIRE(option == GC_OPT_EXACT_SELECTION, GC_ERR_VALUE, "gc_set_option: unknown option");
     g_exact_only = value ? 1 : 0;
     return GC_OK;

@@ -59,26 +59,52 @@ class StageTimer:
 
 
 class SampleGatherPipeline:
-    """Sampling + dedup + relabel + three-tier gather for one GPU's seed pool."""
+    """Sampling + dedup + relabel + three-tier gather for one GPU's seed pool.
+
+    lanes > 1 is Legion's inter-batch pipeline: consecutive
+    windows alternate between `lanes` independent sets of window buffers, each on its
+    own CUDA stream, so one window's PCIe/HBM-bound gather overlaps the next
+    window's ALU-bound sampling. Results are identical; only the schedule changes."""
 
     def __init__(self, graph: CsrGraph, cfg: SamplingConfig, store: FeatureStore | None, max_pool: int,
                  window: int | None = None, relabel: bool = True, feat_rows_cap: int | None = None,
-                 placement: str = "hbm", topology=None, sparse_visited: bool | None = None):
+                 placement: str = "hbm", topology=None, sparse_visited: bool | None = None, lanes: int = 1,
+                 defer_host: bool | None = None):
         self.graph = graph
         self.cfg = cfg
         self.store = store
         B = cfg.batch_size
         nb = max(1, math.ceil(max_pool / B))
         self.window = min(nb, window or nb)
-        self.sampler = WindowSampler(graph, cfg.fanouts, B, self.window, placement=placement, relabel=relabel,
-                                     unique_cap=feat_rows_cap, topology=topology, sparse_visited=sparse_visited)
+        if lanes < 1:
+            raise ValueError("lanes must be >= 1")
+        self.lane_samplers = []
+        self.lane_features = []
+        for _ in range(lanes):
+            sp = WindowSampler(graph, cfg.fanouts, B, self.window, placement=placement, relabel=relabel,
+                               unique_cap=feat_rows_cap, topology=topology, sparse_visited=sparse_visited)
+            self.lane_samplers.append(sp)
+            feats = None
+            if store is not None:
+                feats = torch.empty((self.window, sp.ucap, store.spec.dimension), dtype=torch.float32, device="cuda")
+            self.lane_features.append(feats)
+        self.lane_streams = [torch.cuda.Stream() for _ in range(lanes)] if lanes > 1 else []
+        # host-tier rows (PCIe-bound, few CTAs) on a high-priority stream: its CTAs take
+        # SM slots as soon as any free up and run under the other lanes' sampling
+        # measured at C3 (profiles/r01_tiers_c3_lanes.md): deferring host rows to a
+        # small-grid kernel does not overlap — its CTAs find no free registers while
+        # the sampling kernels fill the SMs — so it is off unless asked for
+        self.defer_host = False if defer_host is None else bool(defer_host)
+        self.host_stream = torch.cuda.Stream(priority=-1) if self.defer_host and lanes > 1 else None
+        self.sampler = self.lane_samplers[0]
+        self.features = self.lane_features[0]
         self.feat_cap = self.sampler.ucap
-        self.features = None
-        if store is not None:
-            self.features = torch.empty((self.window, self.feat_cap, store.spec.dimension), dtype=torch.float32,
-                                        device="cuda")
         self.timer: StageTimer | None = None
         self.launches = 0
+
+    @property
+    def lanes(self) -> int:
+        return len(self.lane_samplers)
 
     # ------------------------------------------------------------------ host prep
     def plan_epoch(self, pool, gpu_stream: KeyedRng) -> EpochPlan:
@@ -104,38 +130,66 @@ class SampleGatherPipeline:
 
     def run_epoch(self, plan: EpochPlan, on_window=None, hot: DeviceHotness | None = None) -> None:
         """Shuffle + all windows of one epoch; on_window(pipeline, first_batch, nbatches)
-        is called after each window's device work has been enqueued."""
-        sp = self.sampler
+        is called after each window's device work has been enqueued (with lanes > 1,
+        on that window's stream and with `sampler`/`features` pointing at its lane).
+        On return the caller's stream is ordered after every window."""
         B, H = self.cfg.batch_size, len(self.cfg.fanouts)
         end = self._stage("shuffle")
         shuffled = KeyedRng(plan.shuffle_key).permutation_device(plan.pool.numel(), plan.pool)
         self.launches += LAUNCHES_PERMUTATION
         if end is not None:
             end.record()
-        for w0 in range(0, plan.num_batches, self.window):
-            w1 = min(plan.num_batches, w0 + self.window)
-            nb = w1 - w0
-            lo, hi = w0 * B, min(plan.pool.numel(), w1 * B)
-            sp.active = nb
-            sp.seeds.view(-1)[: hi - lo].copy_(shuffled[lo:hi])
-            sp.counts[0, :nb].copy_(plan.counts[w0:w1])
-            if H:
-                sp.keys[:, :nb].copy_(plan.keys[w0:w1].t())
-            sp.expand(hot, timer=self.timer)
-            self.launches += max(H, 1)
-            end = self._stage("unique_relabel")
-            sp.dedup(hot)
-            self.launches += 1 + (H + 1 if sp.relabel else 0)
+        main = torch.cuda.current_stream()
+        if self.lane_streams:
+            ready = torch.cuda.Event()
+            ready.record(main)
+            for st in self.lane_streams:
+                st.wait_event(ready)
+        for i, w0 in enumerate(range(0, plan.num_batches, self.window)):
+            lane = i % self.lanes
+            self.sampler = self.lane_samplers[lane]
+            self.features = self.lane_features[lane]
+            if self.lane_streams:
+                with torch.cuda.stream(self.lane_streams[lane]):
+                    self._window(plan, shuffled, w0, on_window, hot)
+            else:
+                self._window(plan, shuffled, w0, on_window, hot)
+        if self.lane_streams:
+            for st in self.lane_streams:
+                done = torch.cuda.Event()
+                done.record(st)
+                main.wait_event(done)
+            # `shuffled` and the plan's tensors were used on the lane streams
+            for st in self.lane_streams:
+                shuffled.record_stream(st)
+
+    def _window(self, plan: EpochPlan, shuffled: torch.Tensor, w0: int, on_window, hot) -> None:
+        sp = self.sampler
+        B, H = self.cfg.batch_size, len(self.cfg.fanouts)
+        w1 = min(plan.num_batches, w0 + self.window)
+        nb = w1 - w0
+        lo, hi = w0 * B, min(plan.pool.numel(), w1 * B)
+        sp.active = nb
+        sp.seeds.view(-1)[: hi - lo].copy_(shuffled[lo:hi])
+        sp.counts[0, :nb].copy_(plan.counts[w0:w1])
+        if H:
+            sp.keys[:, :nb].copy_(plan.keys[w0:w1].t())
+        sp.expand(hot, timer=self.timer)
+        self.launches += max(H, 1)
+        end = self._stage("unique_relabel")
+        sp.dedup(hot)
+        self.launches += 1 + (H + 1 if sp.relabel else 0)
+        if end is not None:
+            end.record()
+        if self.store is not None:
+            end = self._stage("gather")
+            self.store.gather(sp.unique, sp.ucount, self.features, num_batches=nb, deferred=self.defer_host,
+                              host_stream=self.host_stream)
+            self.launches += 1
             if end is not None:
                 end.record()
-            if self.store is not None:
-                end = self._stage("gather")
-                self.store.gather(sp.unique, sp.ucount, self.features, num_batches=nb)
-                self.launches += 1
-                if end is not None:
-                    end.record()
-            if on_window is not None:
-                on_window(self, w0, nb)
+        if on_window is not None:
+            on_window(self, w0, nb)
 
     # ------------------------------------------------------------------ accounting
     def window_bytes(self, nb: int) -> dict[str, int]:

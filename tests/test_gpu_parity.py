@@ -176,10 +176,11 @@ def test_accumulate_hotness_matches_oracle():
 
 
 # ------------------------------------------------------------------ K4 gather
-def test_gather_three_tiers_bit_exact():
+@pytest.mark.parametrize("dim", [100, 128])
+def test_gather_three_tiers_bit_exact(dim):
     from paper_2305_16588_b200.cache import FeatureStore, gather_rows
 
-    n, dim = 50_000, 100
+    n = 50_000
     table = O.synthetic_features(np.arange(n), dim)
     rng = np.random.default_rng(0)
     perm = rng.permutation(n)
@@ -193,6 +194,38 @@ def test_gather_three_tiers_bit_exact():
     want_local = np.isin(ids, parts[0]).sum()
     want_peer = np.isin(ids, np.concatenate(parts[1:])).sum()
     assert tiers == {"local": want_local, "peer": want_peer, "host": len(ids) - want_local - want_peer}
+
+
+@pytest.mark.parametrize("dim", [64, 100, 128])
+def test_gather_deferred_host_rows_bit_exact(dim):
+    """gc_gather_deferred (host rows by a second small-grid kernel) == gc_gather, over a
+    window of batches with ragged counts and a capacity clamp."""
+    from paper_2305_16588_b200.cache import FeatureStore
+
+    n, W, cap = 30_000, 5, 3000
+    table = O.synthetic_features(np.arange(n), dim)
+    rng = np.random.default_rng(1)
+    perm = rng.permutation(n)
+    parts = [perm[i * 4000 : (i + 1) * 4000] for i in range(2)]
+    store = FeatureStore.from_assignment(table, parts, self_rank=0)
+    counts = np.array([3000, 0, 1, 2999, 5000])  # the last one is clamped to cap
+    ids = np.zeros((W, cap), dtype=np.int64)
+    for b in range(W):
+        ids[b, : min(counts[b], cap)] = np.sort(rng.choice(n, min(counts[b], cap), replace=False))
+    d_ids = torch.from_numpy(ids.astype(np.uint32).view(np.int32)).cuda()
+    d_cnt = torch.from_numpy(counts.astype(np.int32)).cuda()
+    outs = []
+    for deferred in (False, True):
+        out = torch.full((W, cap, dim), float("nan"), dtype=torch.float32, device="cuda")
+        store.reset_counters()
+        store.gather(d_ids, d_cnt, out, deferred=deferred)
+        outs.append((out.cpu().numpy(), store.tier_counts()))
+    (a, ta), (b_, tb) = outs
+    assert ta == tb and tb["host"] > 0
+    for b in range(W):
+        k = min(counts[b], cap)
+        assert np.array_equal(b_[b, :k], table[ids[b, :k]])
+        assert np.array_equal(a[b, :k], b_[b, :k])
 
 
 def test_synthetic_features_device_matches_oracle():

@@ -2,7 +2,8 @@
 
 Random 512-byte rows read through UVA by the K4 gather from (a) torch pinned memory
 (cudaHostAlloc) and (b) an anonymous mmap with MADV_HUGEPAGE registered through
-gc_host_register (cudaHostRegister, mapped). Prints GB/s per case.
+gc_host_register (cudaHostRegister, mapped) and (c) gc_host_alloc_numa (cuMemCreate on
+the host NUMA node, mapped at the VMM granularity). Prints GB/s per case.
 """
 
 import ctypes
@@ -31,7 +32,9 @@ def thp_buffer(nbytes):
     return buf, arr, addr
 
 
-def run(host_ptr, n, dim, rows=1 << 20, reps=5):
+def run(host_ptr, n, dim, rows=1 << 20, reps=5, defer_ctas=0):
+    """GB/s of random host rows through gc_gather, or through gc_gather_deferred's
+    small-grid host-row kernel with `defer_ctas` CTAs."""
     lib = _lib.lib()
     loc = torch.full((n,), -1, dtype=torch.int32, device="cuda")  # all rows host-resident
     fs = FeatureStore(FeatureSpec(dim), 0, 1, loc, [None], None)
@@ -39,18 +42,40 @@ def run(host_ptr, n, dim, rows=1 << 20, reps=5):
     ids = torch.randint(0, n, (1, rows), dtype=torch.int64, device="cuda").to(torch.int32)
     cnt = torch.tensor([rows], dtype=torch.int32, device="cuda")
     out = torch.empty((1, rows, dim), dtype=torch.float32, device="cuda")
-    fs.gather(ids, cnt, out)
+    buf = torch.empty(int(lib.gc_gather_defer_bytes(rows, 1)), dtype=torch.uint8, device="cuda")
+    if defer_ctas:
+        _lib.check(lib.gc_set_option(_lib.GC_OPT_DEFER_CTAS, defer_ctas))
+
+    def once():
+        if defer_ctas:
+            _lib.check(lib.gc_gather_deferred(fs.c_struct, ids.data_ptr(), rows, cnt.data_ptr(), rows, 1,
+                                              out.data_ptr(), rows, fs.tier_rows.data_ptr(), buf.data_ptr(),
+                                              buf.numel(), _lib.stream_handle(), None))
+        else:
+            fs.gather(ids, cnt, out)
+
+    once()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(reps):
-        fs.gather(ids, cnt, out)
+        once()
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / reps
+    if defer_ctas:
+        _lib.check(lib.gc_set_option(_lib.GC_OPT_DEFER_CTAS, 148))
     return rows * dim * 4 / dt / 1e9
 
 
 def main():
     dim = 128
+    if "--defer" in sys.argv:
+        n = int(56 * (1 << 30) / (dim * 4))
+        t = torch.empty((n, dim), dtype=torch.float32, pin_memory=True)
+        for ctas in (37, 74, 148, 296, 592, 1184):
+            print(f"host table 56 GB: deferred kernel {ctas:5d} CTAs x 4 warps x 8 rows: "
+                  f"{run(t.data_ptr(), n, dim, defer_ctas=ctas):6.1f} GB/s", flush=True)
+        print(f"host table 56 GB: full-grid gather: {run(t.data_ptr(), n, dim):6.1f} GB/s", flush=True)
+        return
     for gb in (4, 16, 56):
         n = int(gb * (1 << 30) / (dim * 4))
         t = torch.empty((n, dim), dtype=torch.float32, pin_memory=True)
@@ -65,7 +90,12 @@ def main():
         _lib.check(lib.gc_host_unregister(ctypes.c_void_p(addr)), "unregister")
         del arr
         buf.close()
-        print(f"host table {gb:3d} GB: torch pinned {r1:6.1f} GB/s   THP+cudaHostRegister {r2:6.1f} GB/s", flush=True)
+        vptr, mapped = ctypes.c_void_p(), ctypes.c_size_t()
+        _lib.check(lib.gc_host_alloc_numa(n * dim * 4, 0, ctypes.byref(vptr), ctypes.byref(mapped)), "alloc_numa")
+        r3 = run(vptr.value, n, dim)
+        _lib.check(lib.gc_host_free_numa(vptr, mapped), "free_numa")
+        print(f"host table {gb:3d} GB: torch pinned {r1:6.1f} GB/s   THP+cudaHostRegister {r2:6.1f} GB/s   "
+              f"VMM host-NUMA (2 MB GPU pages) {r3:6.1f} GB/s", flush=True)
 
 
 if __name__ == "__main__":

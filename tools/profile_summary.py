@@ -24,7 +24,12 @@ METRICS = [
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue_active_%"),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram_%"), ("smsp__inst_executed.sum", "warp_inst"),
     ("launch__grid_size", "grid"),
+    ("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", "alu_pipe_%"),
+    ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "fma_pipe_%"),
+    ("lts__t_sector_hit_rate.pct", "l2_hit_%"),
 ]
+STALLS = ["long_scoreboard", "barrier", "wait", "math_pipe_throttle", "not_selected", "selected", "short_scoreboard",
+          "dispatch_stall", "lg_throttle", "mio_throttle", "branch_resolving", "no_instructions"]
 
 
 HOP_FANOUT_SLOTS = {"16": 0, "11": 1, "6": 2}  # C2 fanouts (15, 10, 5) -> network template -> hop
@@ -32,7 +37,7 @@ HOP_FANOUT_SLOTS = {"16": 0, "11": 1, "6": 2}  # C2 fanouts (15, 10, 5) -> netwo
 
 def stage_of(name: str, per_launch: bool = False) -> str:
     if per_launch and "k_hop_expand<" in name:
-        slots = name.split("k_hop_expand<")[1].split(">")[0]
+        slots = name.split("k_hop_expand<")[1].split(">")[0].split(",")[0].strip()
         if slots in HOP_FANOUT_SLOTS:
             return f"hop_expand.h{HOP_FANOUT_SLOTS[slots]}"
     for k, v in STAGE.items():
@@ -85,6 +90,13 @@ def full(path: Path):
                     v *= {"ns": 1e-3, "us": 1.0, "ms": 1e3}[u]
                     u = "us"
                 d[short] = v
+        st = {}
+        for name in STALLS:
+            m = f"smsp__pcsamp_warps_issue_stalled_{name}"
+            if m in hdr and r[hdr.index(m)] not in ("", "n/a"):
+                st[name] = float(r[hdr.index(m)].replace(",", ""))
+        tot = sum(st.values()) or 1.0
+        d["stalls"] = {k: 100 * v / tot for k, v in sorted(st.items(), key=lambda kv: -kv[1])[:4]}
         res.append(d)
     return res
 
@@ -113,13 +125,17 @@ def main():
     if a.full:
         res = full(a.full)
         md = [f"# ncu --set full ({a.tag}): one C2 epoch's hot kernels", "",
-              "| kernel | time us | DRAM read MB | DRAM write MB | regs | occupancy % | issue active % | DRAM % | warp inst |",
-              "|---|---|---|---|---|---|---|---|---|"]
+              "Replayed per kernel (cold L2, serialised); `--clock-control none`.", "",
+              "| kernel | time us | DRAM read MB | DRAM write MB | regs | occupancy % | issue active % | ALU pipe % | "
+              "FMA pipe % | DRAM % | L2 hit % | warp inst | top stalls (% of samples) |",
+              "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
         traffic = defaultdict(lambda: [0.0, 0])
         for d in res:
             md.append(f"| `{d['kernel']}` | {d.get('time', 0):.1f} | {d.get('dram_read', 0) / 1e6:.1f} | "
                       f"{d.get('dram_write', 0) / 1e6:.1f} | {d.get('regs')} | {d.get('occupancy_%', 0):.1f} | "
-                      f"{d.get('issue_active_%', 0):.1f} | {d.get('dram_%', 0):.1f} | {d.get('warp_inst', 0):.3g} |")
+                      f"{d.get('issue_active_%', 0):.1f} | {d.get('alu_pipe_%', 0):.1f} | {d.get('fma_pipe_%', 0):.1f} | "
+                      f"{d.get('dram_%', 0):.1f} | {d.get('l2_hit_%', 0):.1f} | {d.get('warp_inst', 0):.3g} | "
+                      + ", ".join(f"{k} {v:.0f}" for k, v in d["stalls"].items()) + " |")
             st = stage_of(d["kernel"], per_launch=True)
             traffic[st][0] += d.get("dram_read", 0) + d.get("dram_write", 0)
             traffic[st][1] += 1
