@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(kHopThreads, (S > 0 && S <= 16) ? 5 : 1) k_hop
             __syncthreads();
             const uint32_t prefix = (uint32_t)s_prefix;
             uint32_t* offs = p.out_off + b * p.ostride;
-            if (valid) offs[p0 + tid] = prefix + excl;
+            if (valid) __stcs(offs + p0 + tid, prefix + excl);
             if (valid && p0 + tid + 1 == F) {
                 offs[F] = prefix + excl + take;
                 p.out_count[b] = prefix + excl + take;
@@ -516,14 +516,14 @@ __global__ void __launch_bounds__(kHopThreads, (S > 0 && S <= 16) ? 5 : 1) k_hop
                 for (int q = 0; q < kEmit; ++q) w[q] = k0 + q * kHopThreads < cnt ? bm[u[q] >> 5] : ~0u;
 #pragma unroll
                 for (int q = 0; q < kEmit; ++q)
-                    if (k0 + q * kHopThreads < cnt) dst[k0 + q * kHopThreads] = u[q];
+                    if (k0 + q * kHopThreads < cnt) __stcs(dst + k0 + q * kHopThreads, u[q]);
 #pragma unroll
                 for (int q = 0; q < kEmit; ++q)
                     if (!((w[q] >> (u[q] & 31)) & 1u)) mark_visited_unchecked(bm, sm, u[q]);
             } else {
 #pragma unroll
                 for (int q = 0; q < kEmit; ++q)
-                    if (k0 + q * kHopThreads < cnt) dst[k0 + q * kHopThreads] = u[q];
+                    if (k0 + q * kHopThreads < cnt) __stcs(dst + k0 + q * kHopThreads, u[q]);
             }
         }
         // s_items is reused by the next round only; the last round exits without a barrier
