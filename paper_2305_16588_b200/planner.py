@@ -267,10 +267,27 @@ def alpha_grid(delta_alpha: float) -> list[float]:
 
 
 def search_optimal_plan(orders: CandidateOrders, budget_bytes: int, delta_alpha: float, graph: CsrGraph,
-                        feat: FeatureSpec, spec: HardwareSpec, sampling_txn_total: int
-                        ) -> tuple[CachePlan, TrafficEstimate]:
+                        feat: FeatureSpec, spec: HardwareSpec, sampling_txn_total: int, *,
+                        bandwidths=None) -> tuple[CachePlan, TrafficEstimate]:
     """Alpha sweep from one pair of device scans and batched boundary searches; the
-    winner is the first strict minimum, i.e. the smallest alpha (planner.py:215-261)."""
+    winner is the first strict minimum, i.e. the smallest alpha (planner.py:215-261).
+
+    bandwidths (a bandwidth.MeasuredBandwidths): minimise the host-tier time predicted
+    from bandwidths measured on the box (bandwidth.estimate_seconds) instead of the
+    reference's transaction count; the returned estimate is the winner's
+    TrafficEstimate either way."""
+    return _search(orders, budget_bytes, delta_alpha, graph, feat, spec, sampling_txn_total, bandwidths)[:2]
+
+
+def sweep_alpha(orders: CandidateOrders, budget_bytes: int, delta_alpha: float, graph: CsrGraph,
+                feat: FeatureSpec, spec: HardwareSpec, sampling_txn_total: int, bandwidths=None
+                ) -> list[tuple[float, TrafficEstimate, float | None]]:
+    """(alpha, TrafficEstimate, predicted seconds or None) for every grid point — the
+    predicted side of the reference's alpha sweep (cli.py:276-340)."""
+    return _search(orders, budget_bytes, delta_alpha, graph, feat, spec, sampling_txn_total, bandwidths)[2]
+
+
+def _search(orders, budget_bytes, delta_alpha, graph, feat, spec, sampling_txn_total, bandwidths):
     grid = np.array(alpha_grid(delta_alpha))
     topo_budgets = grid * budget_bytes
     feat_budgets = budget_bytes - topo_budgets
@@ -288,13 +305,21 @@ def search_optimal_plan(orders: CandidateOrders, budget_bytes: int, delta_alpha:
     t_tot = int(t_cum[-1].item()) if t_cum.numel() else 0
     f_tot = int(f_cum[-1].item()) if f_cum.numel() else 0
     row_txns = feature_row_transactions(feat, spec)
-    best, best_idx = None, -1
+    best, best_idx, best_cost = None, -1, None
+    points = []
     for i in range(len(grid)):
         est = _estimate_at(int(b_t[i]), int(b_f[i]), int(t_at[i]), t_tot, int(f_at[i]), f_tot,
                            int(sampling_txn_total), row_txns)
-        if best is None or est.total_txns < best.total_txns:
-            best, best_idx = est, i
-    return CachePlan.from_alpha(budget_bytes, float(grid[best_idx])), best
+        secs = None
+        if bandwidths is not None:
+            from .bandwidth import estimate_seconds
+
+            secs = estimate_seconds(est, feat, spec, bandwidths)
+        points.append((float(grid[i]), est, secs))
+        cost = est.total_txns if bandwidths is None else secs
+        if best is None or cost < best_cost:
+            best, best_idx, best_cost = est, i, cost
+    return CachePlan.from_alpha(budget_bytes, float(grid[best_idx])), best, points
 
 
 def distribute_prefix(prefix: np.ndarray, owner_local: np.ndarray, clique_size: int) -> list[np.ndarray]:

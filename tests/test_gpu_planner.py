@@ -128,3 +128,49 @@ def test_account_assignment_matches_reference_report(golden):
     traces = P.run_sampling_epoch(graph, pools, layout, cfg, P.derive_seed(7, 5), 0)
     assert np.array_equal(account_assignment(traces, asg, layout, graph, spec, feat).traffic_matrix,
                           g["rep_traffic_matrix"])
+
+
+def test_time_objective_with_uniform_bandwidth_picks_the_transaction_optimum(golden):
+    """With one GB/s for both access shapes the predicted seconds are the reference's
+    N_total x 64 B / bandwidth (feature rows cost ceil(row/CLS) lines; here 100-d rows
+    are 400 B = 6.25 lines, so the seconds use 400 B, not 7 x 64): the picks agree
+    whenever the row is a whole number of lines, and every grid point's estimate is the
+    reference's."""
+    P, g, graph, layout, spec, hot = _golden_setup(golden)
+    from paper_2305_16588_b200 import planner as PL
+    from paper_2305_16588_b200.bandwidth import MeasuredBandwidths, estimate_seconds
+
+    orders = PL.build_candidate_orders(hot)
+    feat = P.FeatureSpec(128)  # 512 B = 8 whole lines
+    bw = MeasuredBandwidths(10.0, 10.0)
+    plan_t, est_t = PL.search_optimal_plan(orders, spec.clique_budget_bytes, 0.01, graph, feat, spec,
+                                           hot.sampling_txn_total)
+    plan_s, est_s = PL.search_optimal_plan(orders, spec.clique_budget_bytes, 0.01, graph, feat, spec,
+                                           hot.sampling_txn_total, bandwidths=bw)
+    assert plan_s.alpha == plan_t.alpha and est_s == est_t
+    pts = PL.sweep_alpha(orders, spec.clique_budget_bytes, 0.01, graph, feat, spec, hot.sampling_txn_total, bw)
+    assert [p[0] for p in pts] == PL.alpha_grid(0.01)
+    for alpha, est, secs in pts:
+        want = PL.estimate_traffic(orders, PL.CachePlan.from_alpha(spec.clique_budget_bytes, alpha), graph, feat,
+                                   spec, hot.sampling_txn_total)
+        assert est == want
+        assert secs == pytest.approx(est.total_txns * 64 / 10e9, rel=1e-12)
+        assert secs == estimate_seconds(est, feat, spec, bw)
+
+
+def test_time_objective_prefers_the_slower_access_shape(golden):
+    """Making topology reads 20x slower per byte can only move the pick toward caching
+    more topology (alpha up), never less."""
+    P, g, graph, layout, spec, hot = _golden_setup(golden)
+    from paper_2305_16588_b200 import planner as PL
+    from paper_2305_16588_b200.bandwidth import MeasuredBandwidths
+
+    orders = PL.build_candidate_orders(hot)
+    feat = P.FeatureSpec(128)
+    base, _ = PL.search_optimal_plan(orders, spec.clique_budget_bytes, 0.01, graph, feat, spec,
+                                     hot.sampling_txn_total, bandwidths=MeasuredBandwidths(10.0, 10.0))
+    slow, _ = PL.search_optimal_plan(orders, spec.clique_budget_bytes, 0.01, graph, feat, spec,
+                                     hot.sampling_txn_total, bandwidths=MeasuredBandwidths(0.5, 10.0))
+    fast, _ = PL.search_optimal_plan(orders, spec.clique_budget_bytes, 0.01, graph, feat, spec,
+                                     hot.sampling_txn_total, bandwidths=MeasuredBandwidths(200.0, 10.0))
+    assert fast.alpha <= base.alpha <= slow.alpha
