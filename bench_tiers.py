@@ -221,14 +221,18 @@ def alpha_sweep(a, g, cfg, hot, orders, budget, feat, spec, layout, host_table, 
 
     full = g.device("host")
     hbm = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] if (ROOT / "MEASURED_PEAKS.json").exists() else None
-    bw = BW.measure_host_tier(full.c_struct.col_indices, g.num_edges * 4, host_table.data_ptr(),
-                              host_table.numel() * 4, feat, spec, hbm_gbs=hbm)
+    probe = BW.measure_host_tier(full.c_struct.col_indices, g.num_edges * 4, host_table.data_ptr(),
+                                 host_table.numel() * 4, feat, spec, hbm_gbs=hbm)
+    bw = BW.calibrate_host_tier(g, np.asarray(pool)[: 64 * cfg.batch_size], cfg.fanouts, cfg.batch_size,
+                                host_table.data_ptr(), host_table.numel() * 4, feat, spec, hbm_gbs=hbm)
     pts = PL.sweep_alpha(orders, budget, 0.01, g, feat, spec, hot.sampling_txn_total, bw)
+    pts_probe = PL.sweep_alpha(orders, budget, 0.01, g, feat, spec, hot.sampling_txn_total, probe)
+    p_probe, _ = PL.search_optimal_plan(orders, budget, 0.01, g, feat, spec, hot.sampling_txn_total, bandwidths=probe)
     p_txn, _ = PL.search_optimal_plan(orders, budget, 0.01, g, feat, spec, hot.sampling_txn_total)
     p_time, _ = PL.search_optimal_plan(orders, budget, 0.01, g, feat, spec, hot.sampling_txn_total, bandwidths=bw)
     step = max(1, (len(pts) - 1) // max(1, a.alpha_sweep - 1))
     idx = sorted(set(list(range(0, len(pts), step)) + [len(pts) - 1] +
-                     [i for i, p in enumerate(pts) if p[0] in (p_txn.alpha, p_time.alpha)]))
+                     [i for i, p in enumerate(pts) if p[0] in (p_txn.alpha, p_time.alpha, p_probe.alpha)]))
     rows = []
     row_txns = PL.feature_row_transactions(feat, spec)
     for i in idx:
@@ -249,6 +253,7 @@ def alpha_sweep(a, g, cfg, hot, orders, budget, feat, spec, layout, host_table, 
         torch.cuda.synchronize()
         tc, fc = ts.tier_counts(), fs.tier_counts()
         rows.append({"alpha": alpha, "predicted_txn": est.total_txns, "predicted_s": secs,
+                     "predicted_s_probe": pts_probe[i][2],
                      "measured_host_txn": tc["host_txn"] + fc["host"] * row_txns,
                      "measured_ms": e0.elapsed_time(e1)})
         del pipe, ts, fs, asg
@@ -258,13 +263,17 @@ def alpha_sweep(a, g, cfg, hot, orders, budget, feat, spec, layout, host_table, 
     pick = lambda al: next(r for r in rows if r["alpha"] == al)  # noqa: E731
     return {
         "bandwidths": json.loads(bw.to_json()),
+        "bandwidths_random_probe": json.loads(probe.to_json()),
         "points": rows,
         "spearman_txn_vs_measured_txn": BW.spearman(col("predicted_txn"), col("measured_host_txn")),
         "spearman_txn_vs_time": BW.spearman(col("predicted_txn"), col("measured_ms")),
         "spearman_seconds_vs_time": BW.spearman(col("predicted_s"), col("measured_ms")),
+        "spearman_probe_seconds_vs_time": BW.spearman(col("predicted_s_probe"), col("measured_ms")),
+        "alpha_probe_objective": p_probe.alpha,
         "alpha_txn_objective": p_txn.alpha, "alpha_time_objective": p_time.alpha,
         "measured_ms_txn_pick": pick(p_txn.alpha)["measured_ms"],
         "measured_ms_time_pick": pick(p_time.alpha)["measured_ms"],
+        "measured_ms_probe_pick": pick(p_probe.alpha)["measured_ms"],
         "best_measured": {"alpha": best["alpha"], "ms": best["measured_ms"]},
         "note": "predicted seconds are host-tier (PCIe) time only; measured_ms is the whole epoch",
     }

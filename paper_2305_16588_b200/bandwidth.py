@@ -96,6 +96,65 @@ def measure_host_tier(topology_ptr: int, topology_bytes: int, feature_ptr: int, 
     return MeasuredBandwidths(topo, feat_gbs, hbm_gbs, nvlink_gbs, src)
 
 
+def topology_line_gbs(graph, seeds: np.ndarray, fanouts, batch_size: int, stream_key: int = 1, reps: int = 3
+                      ) -> tuple[float, dict]:
+    """Effective GB/s of host-tier topology reads *inside the sampler* (K2), in the cost
+    model's unit of 64-byte lines: the same window of batches is sampled with every
+    neighbour list on the host tier (UVA over PCIe) and with the same lists in HBM;
+    the extra time divided by the host run's t(v) line count prices one line.
+    (Random-read probes of 64-byte lines underestimate this by ~3x on a B200: the
+    hop kernel overlaps its row reads with selection work and other CTAs.)"""
+    from .cache import TopologyStore
+    from .rng import KeyedRng
+    from .sampling import WindowSampler, batch_hop_keys
+
+    B = int(batch_size)
+    nb = max(1, len(seeds) // B)
+    seeds = np.asarray(seeds[: nb * B], dtype=np.int64)
+    keys = batch_hop_keys(KeyedRng(stream_key), 0, nb, len(fanouts))
+    counts = np.full(nb, B, dtype=np.int32)
+    flat = torch.from_numpy(seeds.astype(np.uint32).view(np.int32)).cuda()
+    empty = [np.empty(0, dtype=np.int64)]
+    times, txn = {}, 0
+    for where in ("host", "hbm"):
+        ts = TopologyStore(graph, empty, 0, host_full=(where == "host"))
+        sp = WindowSampler(graph, fanouts, B, nb, relabel=False, topology=ts)
+        sp.load(flat, counts, keys)
+        sp.expand()  # warm-up
+        torch.cuda.synchronize()
+        ts.reset_counters()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            sp.expand()
+        e1.record()
+        torch.cuda.synchronize()
+        times[where] = e0.elapsed_time(e1) / 1000.0 / reps
+        if where == "host":
+            txn = ts.tier_counts()["host_txn"] / reps
+        sp.bitmap.zero_()
+        del sp, ts
+    extra = max(times["host"] - times["hbm"], 1e-9)
+    gbs = txn * 64 / extra / 1e9
+    return gbs, {"batches": nb, "host_s": times["host"], "hbm_s": times["hbm"], "host_lines": txn}
+
+
+def calibrate_host_tier(graph, seeds: np.ndarray, fanouts, batch_size: int, feature_ptr: int, feature_bytes: int,
+                        feat: FeatureSpec, spec: HardwareSpec, hbm_gbs: float | None = None,
+                        nvlink_gbs: float | None = None) -> MeasuredBandwidths:
+    """Both host-tier costs measured through the product kernels: topology lines by the
+    sampler differential (topology_line_gbs), feature rows by the K4 gather of random
+    rows over the real host table (the gather is PCIe-bound: its time is the row cost)."""
+    t0 = time.perf_counter()
+    topo, info = topology_line_gbs(graph, seeds, fanouts, batch_size)
+    row = feat.row_bytes if feat.row_bytes % 16 == 0 else spec.cache_line_bytes
+    feat_gbs = random_read_gbs(feature_ptr, feature_bytes, row)
+    src = (f"sampler differential (host vs HBM topology, {info['batches']} batches, "
+           f"{info['host_lines']:.0f} host lines, {info['host_s'] * 1e3:.2f} vs {info['hbm_s'] * 1e3:.2f} ms) and "
+           f"K4 random {row} B rows over {feature_bytes / 1e9:.1f} GB ({time.perf_counter() - t0:.1f} s)")
+    return MeasuredBandwidths(topo, feat_gbs, hbm_gbs, nvlink_gbs, src)
+
+
 def estimate_seconds(est, feat: FeatureSpec, spec: HardwareSpec, bw: MeasuredBandwidths) -> float:
     """Host-tier seconds per epoch of one TrafficEstimate (the time objective)."""
     topo_bytes = float(est.sampling_txns) * spec.cache_line_bytes

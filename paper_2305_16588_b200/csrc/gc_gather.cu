@@ -9,6 +9,10 @@
 // contiguous output and each row's source bytes are read once, fully coalesced.
 #include "gc_common.cuh"
 
+#ifndef GC_GATHER_MIN_BLOCKS
+#define GC_GATHER_MIN_BLOCKS 1
+#endif
+
 namespace gc {
 
 // deferred host-tier row: destination row index in `out` and the vertex id
@@ -111,7 +115,7 @@ __global__ void __launch_bounds__(256) k_gather(GatherParams p) {
 // 16-byte loads per lane are issued before any store — so HBM, NVLink and PCIe
 // latency overlap instead of serialising per row.
 template <int ROWS>
-__global__ void __launch_bounds__(256) k_gather_rows(GatherParams p) {
+__global__ void __launch_bounds__(256, GC_GATHER_MIN_BLOCKS) k_gather_rows(GatherParams p) {
     __shared__ unsigned long long s_tier[3];
     const uint32_t b = blockIdx.y;
     const uint32_t rows = min(p.count[b], p.max_rows);

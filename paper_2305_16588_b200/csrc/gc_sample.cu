@@ -25,6 +25,18 @@ constexpr int kHopThreads = 256;
 constexpr int kTilePos = 256;
 constexpr int kItemCap = 4096;  // staged output items per round (32 KB of u64 edge indices)
 constexpr int kEmit = 4;        // emission items in flight per thread
+// resident CTAs per SM the register budget targets: 6 (40 registers, no spills) for
+// S <= 8, 5 up to S = 16 (C3 hop 2, S = 11: 15.0 ms at 5 vs 16.1 at 6), 4 (64 registers) above and for the
+// generic kernel (measured: C2 hop 3 1.73 -> 1.68 ms; C3 hop 1, fanout 25, was at one
+// CTA per SM with 181 registers)
+#ifndef GC_HOP_MIN_BLOCKS
+#define GC_HOP_MIN_BLOCKS 6
+#endif
+constexpr int kHopMinBlocks = GC_HOP_MIN_BLOCKS;
+template <int S>
+constexpr int hop_min_blocks() {
+    return S > 0 && S <= 8 ? kHopMinBlocks : (S > 0 && S <= 16 ? 5 : 4);
+}
 
 constexpr int kTierShift = 56;  // staged edge index = (tier code << 56) | edge within that tier's CSR
 constexpr uint64_t kEdgeMask = (1ull << kTierShift) - 1;
@@ -333,7 +345,7 @@ __device__ __forceinline__ void select_warp(uint64_t hc, uint32_t d, uint32_t fa
 // TIERED: the topology has a location table or lives in host memory, so rows resolve
 // through the tier rule and staged edges carry a slab code; otherwise the plain CSR.
 template <int S, bool TIERED>
-__global__ void __launch_bounds__(kHopThreads, (S > 0 && S <= 16) ? 5 : 1) k_hop_expand(HopParams p) {
+__global__ void __launch_bounds__(kHopThreads, hop_min_blocks<S>()) k_hop_expand(HopParams p) {
     using Scan = cub::BlockScan<uint32_t, kHopThreads>;
     using Reduce = cub::BlockReduce<uint64_t, kHopThreads>;
     __shared__ union {
