@@ -12,6 +12,9 @@
 #ifndef GC_GATHER_MIN_BLOCKS
 #define GC_GATHER_MIN_BLOCKS 1
 #endif
+#ifndef GC_GATHER_ROWS
+#define GC_GATHER_ROWS 4  // rows in flight per warp in k_gather_rows
+#endif
 
 namespace gc {
 
@@ -128,18 +131,23 @@ __global__ void __launch_bounds__(256, GC_GATHER_MIN_BLOCKS) k_gather_rows(Gathe
     unsigned long long cnt[3] = {0, 0, 0};
     const uint32_t warps = gridDim.x * (blockDim.x / 32);
     const uint32_t wid = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-    for (uint32_t r0 = wid * ROWS; r0 < rows; r0 += warps * ROWS) {
-        // lanes 0..ROWS-1 resolve one row each
+    // each warp takes 32 consecutive rows: one coalesced id load and one location
+    // lookup per lane resolve all 32 sources, then ROWS rows at a time move with
+    // ROWS independent 16-byte loads per lane in flight before their stores
+    for (uint32_t c0 = wid * 32; c0 < rows; c0 += warps * 32) {
         const char* my_src = nullptr;
         int my_tier = 0;
         uint32_t my_id = 0;
-        if (lane < ROWS && r0 + lane < rows) {
-            my_id = __ldg(ids + r0 + lane);
+        if (c0 + lane < rows) {
+            my_id = __ldg(ids + c0 + lane);
             my_src = row_source(p.fs, my_id, my_tier);
+            cnt[0] += my_tier == 0;
+            cnt[1] += my_tier == 1;
+            cnt[2] += my_tier == 2;
         }
         if (p.defer) {
-            // host rows go to the deferred list (read later by a few warps over PCIe,
-            // while the next window samples); one atomic per warp
+            // host rows go to the deferred list (read later by a few warps over PCIe);
+            // one atomic per warp
             const bool d = my_src != nullptr && my_tier == 2;
             const unsigned m = __ballot_sync(kFull, d);
             if (m) {
@@ -148,7 +156,7 @@ __global__ void __launch_bounds__(256, GC_GATHER_MIN_BLOCKS) k_gather_rows(Gathe
                 base = __shfl_sync(kFull, base, __ffs(m) - 1);
                 if (d) {
                     DeferredRow e;
-                    e.dst_row = (uint64_t)b * p.out_stride_rows + r0 + lane;
+                    e.dst_row = (uint64_t)b * p.out_stride_rows + c0 + lane;
                     e.id = my_id;
                     e.pad = 0;
                     p.defer[base + __popc(m & ((1u << lane) - 1u))] = e;
@@ -156,22 +164,21 @@ __global__ void __launch_bounds__(256, GC_GATHER_MIN_BLOCKS) k_gather_rows(Gathe
                 }
             }
         }
-        uint4 v[ROWS];
+        const uint32_t n = min(32u, rows - c0);
+        for (uint32_t j0 = 0; j0 < n; j0 += ROWS) {
+            uint4 v[ROWS];
 #pragma unroll
-        for (int j = 0; j < ROWS; ++j) {
-            const char* src = (const char*)__shfl_sync(kFull, (unsigned long long)my_src, j);
-            v[j] = (src && (uint32_t)lane < per_row) ? ld_stream16(src + 16 * lane) : make_uint4(0, 0, 0, 0);
-        }
+            for (int j = 0; j < ROWS; ++j) {
+                const char* src = (const char*)__shfl_sync(kFull, (unsigned long long)my_src, (j0 + j) & 31);
+                v[j] = (j0 + j < n && src && (uint32_t)lane < per_row) ? ld_stream16(src + 16 * lane)
+                                                                         : make_uint4(0, 0, 0, 0);
+            }
 #pragma unroll
-        for (int j = 0; j < ROWS; ++j) {
-            const bool have = __shfl_sync(kFull, my_src != nullptr, j);
-            if (have && (uint32_t)lane < per_row)
-                st_stream16(out + (uint64_t)(r0 + j) * p.fs.row_bytes + 16 * lane, v[j]);
-        }
-        if (lane < ROWS && r0 + lane < rows) {
-            cnt[0] += my_tier == 0;
-            cnt[1] += my_tier == 1;
-            cnt[2] += my_tier == 2;
+            for (int j = 0; j < ROWS; ++j) {
+                const bool have = __shfl_sync(kFull, my_src != nullptr, (j0 + j) & 31);
+                if (j0 + j < n && have && (uint32_t)lane < per_row)
+                    st_stream16(out + (uint64_t)(c0 + j0 + j) * p.fs.row_bytes + 16 * lane, v[j]);
+            }
         }
     }
     if (p.tier_rows) {
@@ -308,12 +315,13 @@ static int gather_impl(const gc_feature_store_t* store, const uint32_t* d_ids, u
     if (gx < 1) gx = 1;
     dim3 grid((unsigned)gx, num_batches);
     if (vec16 && per_row <= 32) {
-        // warp per row, 4 rows in flight per warp; ~16 resident warps per SM per batch slice
-        uint64_t wx = ((uint64_t)max_count + 4 * 8 - 1) / (4 * 8);
+        // warp per row, 32-row chunks per warp, 4 rows in flight; ~16 resident warps per
+        // SM per batch slice
+        uint64_t wx = ((uint64_t)max_count + 32 * 8 - 1) / (32 * 8);
         const uint64_t wcap = (uint64_t)148 * 16 / num_batches;
         if (wx > wcap) wx = wcap;
         if (wx < 1) wx = 1;
-        k_gather_rows<4><<<dim3((unsigned)wx, num_batches), 256, 0, s>>>(p);
+        k_gather_rows<GC_GATHER_ROWS><<<dim3((unsigned)wx, num_batches), 256, 0, s>>>(p);
     } else if (vec16) {
         k_gather<16><<<grid, 256, 0, s>>>(p);
     } else {
