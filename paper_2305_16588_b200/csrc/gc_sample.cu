@@ -21,9 +21,12 @@
 
 namespace gc {
 
-constexpr int kHopThreads = 256;
-constexpr int kTilePos = 256;
-constexpr int kItemCap = 4096;  // staged output items per round (32 KB of u64 edge indices)
+#ifndef GC_HOP_THREADS
+#define GC_HOP_THREADS 256  // 128 measured 2% slower at C2 hop 3
+#endif
+constexpr int kHopThreads = GC_HOP_THREADS;  // CTA = one tile of kTilePos frontier positions
+constexpr int kTilePos = kHopThreads;
+constexpr int kItemCap = 16 * kHopThreads;  // staged output items per round (u64 edge indices)
 // emission items in flight per thread: a full tile of 256 positions with take =
 // fanout stages exactly `fanout` items per thread, so for the small networks S - 1
 // (the largest fanout of the network) covers it in one pass (C2 hop 3: 1.68 -> 1.60
@@ -42,7 +45,7 @@ __host__ __device__ constexpr int emit_items() {
 constexpr int kHopMinBlocks = GC_HOP_MIN_BLOCKS;
 template <int S>
 constexpr int hop_min_blocks() {
-    return S > 0 && S <= 8 ? kHopMinBlocks : (S > 0 && S <= 16 ? 5 : 4);
+    return (S > 0 && S <= 8 ? kHopMinBlocks : (S > 0 && S <= 16 ? 5 : 4)) * 256 / kHopThreads;
 }
 
 constexpr int kTierShift = 56;  // staged edge index = (tier code << 56) | edge within that tier's CSR
