@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--window", type=int, default=0,
                     help="batches per launch window (0 = whole epoch / lanes*2 windows when lanes > 1)")
     ap.add_argument("--lanes", type=int, default=1, help="concurrent window lanes (inter-batch pipeline streams)")
+    ap.add_argument("--visited", default="auto", choices=["auto", "dense", "sparse"],
+                    help="visited-set layout for dedup (auto: sparse above 4M vertices)")
     ap.add_argument("--num-vertices", type=int, default=CONFIG["num_vertices"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -275,7 +277,9 @@ def run_b200(args):
     window = args.window or (nb if args.lanes == 1 else math.ceil(nb / (2 * args.lanes)))
     # per-batch distinct rows stay far below the 938K worst case; 64K keeps the
     # window's gather buffer small, and the run checks it never overflowed
-    pipe = SampleGatherPipeline(g, cfg, store, len(pool), window=window, feat_rows_cap=65536, lanes=args.lanes)
+    sparse = None if args.visited == "auto" else args.visited == "sparse"
+    pipe = SampleGatherPipeline(g, cfg, store, len(pool), window=window, feat_rows_cap=65536, lanes=args.lanes,
+                                sparse_visited=sparse)
     root = KeyedRng(cfg.seed)
     clique, local_idx = layout.gpu_position(rank)
     plans = [pipe.plan_epoch(pool, root.derive(e, clique, local_idx)) for e in range(args.warmup + args.steps)]
@@ -319,7 +323,7 @@ def run_b200(args):
     launches = pipe.launches
     # per-kernel durations for the roofline: the same epochs again, one window after
     # another on one stream (kernels timed alone, not sharing the GPU), untimed overall
-    seq = pipe if args.lanes == 1 else SampleGatherPipeline(g, cfg, store, len(pool), window=window,
+    seq = pipe if args.lanes == 1 else SampleGatherPipeline(g, cfg, store, len(pool), window=window, sparse_visited=sparse,
                                                               feat_rows_cap=65536, lanes=1)
     timer = StageTimer()
     seq.timer = timer
@@ -445,7 +449,8 @@ def e2e_run(args, g, cfg, store, pool, root, clique, local_idx, world):
     from paper_2305_16588_b200.pipeline import SampleGatherPipeline
 
     nb = math.ceil(len(pool) / cfg.batch_size)
-    pipe = SampleGatherPipeline(g, cfg, store, len(pool), window=args.window or nb, feat_rows_cap=65536)
+    pipe = SampleGatherPipeline(g, cfg, store, len(pool), window=args.window or nb, feat_rows_cap=65536,
+                                sparse_visited=None if args.visited == "auto" else args.visited == "sparse")
     host_pool = torch.from_numpy(np.asarray(pool, dtype=np.int64)).pin_memory()
     sp = pipe.sampler
     H = len(cfg.fanouts)

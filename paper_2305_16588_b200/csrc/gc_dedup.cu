@@ -80,16 +80,20 @@ __global__ void __launch_bounds__(kUniqThreads) k_unique(UniqueParams p) {
 }
 
 // Sparse compaction, fully parallel over the non-empty 32-word blocks (1024 vertices):
-//   k_block_lists     one CTA per batch: summary bits -> ascending list of non-empty
-//                     blocks (and the summary is cleared as it is read)
-//   k_chunk_offsets   one CTA: exclusive scan of chunks (8 blocks) over the batches
-//   k_unique_blocks   persistent CTAs claim chunks in order; warp w of a chunk loads
-//                     block w (one coalesced 128-byte load), a CTA scan + decoupled
-//                     look-back over the batch's chunks gives the output offset, and
-//                     the warp emits ids in ascending order, rank-table entries, and
-//                     clears the words it consumed.
-// Work is O(distinct blocks + n/32768) per batch instead of O(n/32).
-constexpr int kChunkBlocks = kUniqThreads / 32;  // blocks per chunk (one warp each)
+//   k_block_lists   one CTA per batch: summary bits -> ascending list of non-empty
+//                   blocks (and the summary is cleared as it is read)
+//   k_block_counts  warp per listed block: one coalesced 128-byte load, popcount
+//   k_block_scan    one CTA per batch: exclusive scan of its block counts (the
+//                   output offset of every block; ucount)
+//   k_block_emit    warp per listed block: ids in ascending order, rank-table entries,
+//                   the words it consumed cleared.
+// Work is O(distinct blocks + n/32768) per batch instead of O(n/32), with no barrier or
+// inter-block wait in the per-block passes. (A single pass with a decoupled look-back
+// across chunks of blocks was measured at 32 ms per C3 epoch: with one wave of
+// persistent CTAs every chunk's look-back walks back through the whole wave; a
+// chunk-granular two-pass version at 16 ms.)
+constexpr int kBlockWarps = kUniqThreads / 32;
+constexpr int kBlocksInFlight = 4;  // listed blocks per warp per step (independent load chains)
 
 __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, uint32_t& total) {
     const int lane = threadIdx.x & 31;
@@ -112,10 +116,7 @@ struct SparseParams {
     uint32_t* lists;     // [W][list_stride] non-empty block ids
     uint64_t list_stride;
     uint32_t* nblocks;   // [W]
-    uint32_t* chunk_start;  // [W + 1]
-    uint4* chunk_desc;   // [max chunks] {batch, chunk in batch, first global chunk, blocks in batch}
-    uint64_t* state;     // look-back status per global chunk
-    uint32_t* counter;
+    uint32_t* bcount;    // [W][list_stride] distinct ids per listed block, then their exclusive prefix
     uint32_t* uniq;
     uint64_t ustride;
     uint32_t* ucount;
@@ -148,119 +149,112 @@ __global__ void __launch_bounds__(kUniqThreads) k_block_lists(SparseParams p) {
     if (threadIdx.x == 0) p.nblocks[b] = s_run;
 }
 
-__global__ void __launch_bounds__(1024) k_chunk_offsets(SparseParams p) {
+// grid (x, W): the warps of batch b's CTAs stride over its listed blocks,
+// kBlocksInFlight at a time
+__global__ void __launch_bounds__(kUniqThreads) k_block_counts(SparseParams p) {
+    const uint32_t b = blockIdx.y;
+    const int lane = threadIdx.x & 31;
+    const uint32_t nb = p.nblocks[b];
+    const uint32_t* list = p.lists + b * p.list_stride;
+    const uint32_t* row = p.bm + b * p.bwords;
+    uint32_t* cnt = p.bcount + b * p.list_stride;
+    const uint32_t warps = gridDim.x * kBlockWarps;
+    for (uint32_t i0 = (blockIdx.x * kBlockWarps + (threadIdx.x >> 5)) * kBlocksInFlight; i0 < nb;
+         i0 += warps * kBlocksInFlight) {
+        uint32_t x[kBlocksInFlight];
+#pragma unroll
+        for (int k = 0; k < kBlocksInFlight; ++k) {
+            x[k] = 0u;
+            if (i0 + k < nb) {
+                const uint64_t wi = (uint64_t)list[i0 + k] * 32 + lane;
+                if (wi < p.bwords) x[k] = row[wi];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kBlocksInFlight; ++k) {
+            const uint32_t c = __reduce_add_sync(kFull, (uint32_t)__popc(x[k]));
+            if (lane == 0 && i0 + k < nb) cnt[i0 + k] = c;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_block_scan(SparseParams p) {
     using Scan = cub::BlockScan<uint32_t, 1024>;
     __shared__ typename Scan::TempStorage tmp;
     __shared__ uint32_t s_run;
+    const uint32_t b = blockIdx.x;
+    const uint32_t nb = p.nblocks[b];
+    uint32_t* cnt = p.bcount + b * p.list_stride;
     if (threadIdx.x == 0) s_run = 0;
     __syncthreads();
-    for (uint32_t base = 0; base < p.num_batches; base += 1024) {
-        const uint32_t b = base + threadIdx.x;
-        const uint32_t nb = b < p.num_batches ? p.nblocks[b] : 0u;
+    for (uint32_t base = 0; base < nb; base += 1024) {
+        const uint32_t i = base + threadIdx.x;
+        const uint32_t v = i < nb ? cnt[i] : 0u;
         uint32_t excl, total;
-        Scan(tmp).ExclusiveSum((nb + kChunkBlocks - 1) / kChunkBlocks, excl, total);
-        if (b < p.num_batches) {
-            p.chunk_start[b] = s_run + excl;
-            if (nb == 0) p.ucount[b] = 0;
-        }
+        Scan(tmp).ExclusiveSum(v, excl, total);
+        if (i < nb) cnt[i] = s_run + excl;  // in place: count -> exclusive prefix
         __syncthreads();
         if (threadIdx.x == 0) s_run += total;
         __syncthreads();
     }
-    if (threadIdx.x == 0) p.chunk_start[p.num_batches] = s_run;
+    if (threadIdx.x == 0) p.ucount[b] = s_run;
 }
 
-__global__ void k_chunk_batches(SparseParams p) {
-    const uint32_t b = blockIdx.x;
-    const uint32_t first = p.chunk_start[b], end = p.chunk_start[b + 1], nb = p.nblocks[b];
-    for (uint32_t c = first + threadIdx.x; c < end; c += blockDim.x) p.chunk_desc[c] = make_uint4(b, c - first, first, nb);
-}
-
-// Persistent CTAs take chunks c = blockIdx.x + k * gridDim.x in increasing order. A
-// chunk only waits on earlier chunks of its batch, and every CTA is resident (the
-// grid is sized to fit), so the smallest unfinished chunk always progresses. The next
-// chunk's descriptor, block id and bitmap word are loaded before the current chunk's
-// scan, look-back and emission, so the dependent-load chain overlaps.
-__global__ void __launch_bounds__(kUniqThreads) k_unique_blocks(SparseParams p) {
-    __shared__ uint32_t s_warp[kChunkBlocks];
-    __shared__ uint64_t s_prefix;
-    __shared__ uint32_t s_total;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t total_chunks = p.chunk_start[p.num_batches];
-    auto fetch = [&](uint32_t c, uint4& d, uint64_t& wi, uint32_t& x) {
-        x = 0u;
-        wi = 0;
-        if (c >= total_chunks) return;
-        d = p.chunk_desc[c];
-        const uint32_t bi = d.y * kChunkBlocks + warp;
-        if (bi < d.w) {
-            wi = (uint64_t)p.lists[d.x * p.list_stride + bi] * 32 + lane;
-            if (wi < p.bwords) x = p.bm[d.x * p.bwords + wi];
-        }
-    };
-    uint4 d{};
-    uint64_t wi;
-    uint32_t x;
-    fetch(blockIdx.x, d, wi, x);
-    for (uint32_t c = blockIdx.x; c < total_chunks; c += gridDim.x) {
-        uint4 dn{};
-        uint64_t win;
-        uint32_t xn;
-        fetch(c + gridDim.x, dn, win, xn);
-        const uint32_t b = d.x, ci = d.y, first = d.z, nb = d.w;
-        uint32_t wtot;
-        const uint32_t wex = warp_excl_scan((uint32_t)__popc(x), wtot);
-        if (lane == 0) s_warp[warp] = wtot;
-        __syncthreads();
-        if (warp == 0) {
-            const uint32_t v = lane < kChunkBlocks ? s_warp[lane] : 0u;
-            uint32_t tile_total;
-            const uint32_t ex = warp_excl_scan(v, tile_total);
-            if (lane < kChunkBlocks) s_warp[lane] = ex;
-            if (lane == 0 && ci != 0) publish(p.state + c, kFlagAgg | tile_total);
-            const uint64_t pre = lookback_warp(p.state, first, c, tile_total);
-            if (lane == 0) {
-                s_prefix = pre;
-                s_total = tile_total;
+__global__ void __launch_bounds__(kUniqThreads) k_block_emit(SparseParams p) {
+    const uint32_t b = blockIdx.y;
+    const int lane = threadIdx.x & 31;
+    const uint32_t nb = p.nblocks[b];
+    const uint32_t* list = p.lists + b * p.list_stride;
+    uint32_t* row = p.bm + b * p.bwords;
+    const uint32_t* pre = p.bcount + b * p.list_stride;
+    uint32_t* out = p.uniq + b * p.ustride;
+    uint2* rt = p.rank ? p.rank + b * p.bwords : nullptr;
+    const uint32_t warps = gridDim.x * kBlockWarps;
+    for (uint32_t i0 = (blockIdx.x * kBlockWarps + (threadIdx.x >> 5)) * kBlocksInFlight; i0 < nb;
+         i0 += warps * kBlocksInFlight) {
+        uint32_t x[kBlocksInFlight], base[kBlocksInFlight];
+        uint64_t wi[kBlocksInFlight];
+#pragma unroll
+        for (int k = 0; k < kBlocksInFlight; ++k) {
+            x[k] = 0u;
+            wi[k] = 0;
+            base[k] = 0;
+            if (i0 + k < nb) {
+                wi[k] = (uint64_t)list[i0 + k] * 32 + lane;
+                base[k] = pre[i0 + k];
+                if (wi[k] < p.bwords) x[k] = row[wi[k]];
             }
         }
-        __syncthreads();
-        uint32_t pos = (uint32_t)s_prefix + s_warp[warp] + wex;
-        if (x) {
-            if (p.rank) p.rank[b * p.bwords + wi] = make_uint2(pos, x);
-            uint32_t* out = p.uniq + b * p.ustride;
-            const uint32_t vbase = (uint32_t)(wi * 32);
-            for (uint32_t w = x; w; w &= w - 1u) {
-                const uint32_t u = vbase + (__ffs(w) - 1);
-                out[pos++] = u;
-                if (p.feat) atomicAdd((unsigned long long*)(p.feat + u), 1ull);
+#pragma unroll
+        for (int k = 0; k < kBlocksInFlight; ++k) {
+            uint32_t tot;
+            uint32_t pos = base[k] + warp_excl_scan((uint32_t)__popc(x[k]), tot);
+            if (x[k]) {
+                if (rt) rt[wi[k]] = make_uint2(pos, x[k]);
+                const uint32_t vbase = (uint32_t)(wi[k] * 32);
+                for (uint32_t w = x[k]; w; w &= w - 1u) {
+                    const uint32_t u = vbase + (__ffs(w) - 1);
+                    out[pos++] = u;
+                    if (p.feat) atomicAdd((unsigned long long*)(p.feat + u), 1ull);
+                }
+                if (p.clear) row[wi[k]] = 0u;
             }
-            if (p.clear) p.bm[b * p.bwords + wi] = 0u;
         }
-        if (tid == 0 && (ci + 1) * kChunkBlocks >= nb) p.ucount[b] = (uint32_t)s_prefix + s_total;
-        __syncthreads();
-        d = dn;
-        wi = win;
-        x = xn;
     }
 }
 
 struct SparseLayout {
-    size_t lists, nblocks, chunk_start, chunk_desc, state, counter, total;
-    uint64_t list_stride, max_chunks;
+    size_t lists, nblocks, bcount, total;
+    uint64_t list_stride;
 };
 
 static SparseLayout sparse_layout(uint32_t W, const gc_visited_t* v) {
     SparseLayout L{};
     L.list_stride = v->summary_words * 32;
-    L.max_chunks = (L.list_stride + kChunkBlocks - 1) / kChunkBlocks;
     size_t off = 0;
     L.lists = off; off = align_up(off + (size_t)W * L.list_stride * 4, 256);
     L.nblocks = off; off = align_up(off + (size_t)W * 4, 256);
-    L.chunk_start = off; off = align_up(off + (size_t)(W + 1) * 4, 256);
-    L.chunk_desc = off; off = align_up(off + (size_t)W * L.max_chunks * 16, 256);
-    L.state = off; off = align_up(off + (size_t)W * L.max_chunks * 8, 256);
-    L.counter = off; off = align_up(off + 4, 256);
+    L.bcount = off; off = align_up(off + (size_t)W * L.list_stride * 4, 256);
     L.total = off;
     return L;
 }
@@ -379,10 +373,7 @@ int gc_unique_compact(const gc_visited_t* visited, uint32_t num_batches, uint32_
         q.lists = reinterpret_cast<uint32_t*>(t + L.lists);
         q.list_stride = L.list_stride;
         q.nblocks = reinterpret_cast<uint32_t*>(t + L.nblocks);
-        q.chunk_start = reinterpret_cast<uint32_t*>(t + L.chunk_start);
-        q.chunk_desc = reinterpret_cast<uint4*>(t + L.chunk_desc);
-        q.state = reinterpret_cast<uint64_t*>(t + L.state);
-        q.counter = reinterpret_cast<uint32_t*>(t + L.counter);
+        q.bcount = reinterpret_cast<uint32_t*>(t + L.bcount);
         q.uniq = d_unique;
         q.ustride = unique_stride;
         q.ucount = d_unique_count;
@@ -391,19 +382,17 @@ int gc_unique_compact(const gc_visited_t* visited, uint32_t num_batches, uint32_
         q.clear = clear_bitmap;
         // the block lists need the summary; it is cleared as it is read only when the
         // bitmap is cleared too
-        GC_TRY(cudaMemsetAsync(t + L.state, 0, L.total - L.state, s), "gc_unique_compact memset");
         k_block_lists<<<num_batches, kUniqThreads, 0, s>>>(q);
         GC_CHECK_LAUNCH("gc_unique_compact lists");
-        k_chunk_offsets<<<1, 1024, 0, s>>>(q);
-        GC_CHECK_LAUNCH("gc_unique_compact chunks");
-        k_chunk_batches<<<num_batches, 256, 0, s>>>(q);
-        GC_CHECK_LAUNCH("gc_unique_compact chunk map");
-        int dev = 0, sms = 148, per_sm = 1;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_unique_blocks, kUniqThreads, 0);
-        // every CTA must be resident for the static chunk order (see k_unique_blocks)
-        k_unique_blocks<<<(unsigned)(sms * (per_sm > 0 ? per_sm : 1)), kUniqThreads, 0, s>>>(q);
+        // ~8 CTAs per SM over the whole window
+        unsigned gx = (unsigned)((148u * 8u + num_batches - 1) / num_batches);
+        if (gx < 1) gx = 1;
+        const dim3 grid(gx, num_batches);
+        k_block_counts<<<grid, kUniqThreads, 0, s>>>(q);
+        GC_CHECK_LAUNCH("gc_unique_compact counts");
+        k_block_scan<<<num_batches, 1024, 0, s>>>(q);
+        GC_CHECK_LAUNCH("gc_unique_compact scan");
+        k_block_emit<<<grid, kUniqThreads, 0, s>>>(q);
         GC_CHECK_LAUNCH("gc_unique_compact blocks");
         return GC_OK;
     }
