@@ -4,6 +4,7 @@
 // of the bitmap (no sort). The per-word exclusive popcount, stored interleaved with
 // the word itself as a rank table {prefix, bits}, is the relabel map:
 // local(u) = prefix[u >> 5] + popc(bits[u >> 5] & lanes-below(u)) — one 8-byte load.
+#include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 
 #include "gc_common.cuh"
@@ -24,35 +25,60 @@ struct UniqueParams {
     uint2* rank;
     uint64_t* feat;
     int clear;
-    uint64_t* tile_state;
-    uint32_t* tile_counter;
+    uint32_t* tile_count;  // [W][tiles] distinct ids per tile, then their exclusive prefix
 };
+
+// Dense compaction in three passes over tiles of 1024 words (no inter-tile wait; a
+// single pass with a decoupled look-back spent 69% of its time at barriers behind
+// the look-back convoy): tile popcounts, a per-batch scan of them, then the ordered
+// emission of every tile from its known offset.
+__global__ void __launch_bounds__(kUniqThreads) k_unique_counts(UniqueParams p) {
+    using Reduce = cub::BlockReduce<uint32_t, kUniqThreads>;
+    __shared__ typename Reduce::TempStorage tmp;
+    const uint32_t b = blockIdx.y, t = blockIdx.x;
+    const uint64_t w0 = (uint64_t)t * kWordsPerTile + (uint64_t)threadIdx.x * kWordsPerThread;
+    uint4 x = make_uint4(0, 0, 0, 0);
+    if (w0 < p.bwords) x = *reinterpret_cast<const uint4*>(p.bm + b * p.bwords + w0);  // bwords % 4 == 0
+    const uint32_t c = Reduce(tmp).Sum(__popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w));
+    if (threadIdx.x == 0) p.tile_count[(uint64_t)b * p.tiles_per_batch + t] = c;
+}
+
+__global__ void __launch_bounds__(1024) k_unique_tile_scan(UniqueParams p) {
+    using Scan = cub::BlockScan<uint32_t, 1024>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ uint32_t s_run;
+    const uint32_t b = blockIdx.x;
+    uint32_t* cnt = p.tile_count + (uint64_t)b * p.tiles_per_batch;
+    if (threadIdx.x == 0) s_run = 0;
+    __syncthreads();
+    for (uint32_t base = 0; base < p.tiles_per_batch; base += 1024) {
+        const uint32_t i = base + threadIdx.x;
+        const uint32_t v = i < p.tiles_per_batch ? cnt[i] : 0u;
+        uint32_t excl, total;
+        Scan(tmp).ExclusiveSum(v, excl, total);
+        if (i < p.tiles_per_batch) cnt[i] = s_run + excl;
+        __syncthreads();
+        if (threadIdx.x == 0) s_run += total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) p.ucount[b] = s_run;
+}
 
 __global__ void __launch_bounds__(kUniqThreads) k_unique(UniqueParams p) {
     using Scan = cub::BlockScan<uint32_t, kUniqThreads>;
     __shared__ typename Scan::TempStorage scan_tmp;
-    __shared__ uint32_t s_vid;
-    __shared__ uint64_t s_prefix;
+    const uint32_t b = blockIdx.y, t = blockIdx.x;
     const int tid = threadIdx.x;
-    if (tid == 0) s_vid = atomicAdd(p.tile_counter, 1u);
-    __syncthreads();
-    const uint32_t b = s_vid / p.tiles_per_batch;
-    const uint32_t t = s_vid % p.tiles_per_batch;
     const uint64_t w0 = (uint64_t)t * kWordsPerTile + (uint64_t)tid * kWordsPerThread;
     uint32_t* row = p.bm + b * p.bwords;
+    const uint32_t tile_base = p.tile_count[(uint64_t)b * p.tiles_per_batch + t];
     uint4 x = make_uint4(0, 0, 0, 0);
-    if (w0 < p.bwords) x = *reinterpret_cast<const uint4*>(row + w0);  // bwords is a multiple of 4
+    if (w0 < p.bwords) x = *reinterpret_cast<const uint4*>(row + w0);
     const uint32_t c0 = __popc(x.x), c1 = __popc(x.y), c2 = __popc(x.z), c3 = __popc(x.w);
     uint32_t excl, total;
     Scan(scan_tmp).ExclusiveSum(c0 + c1 + c2 + c3, excl, total);
-    const uint64_t sidx = (uint64_t)b * p.tiles_per_batch + t;
-    if (tid == 0 && t != 0) publish(p.tile_state + sidx, kFlagAgg | total);
-    if (tid < 32) {
-        uint64_t pre = lookback_warp(p.tile_state, (uint64_t)b * p.tiles_per_batch, sidx, total);
-        if (tid == 0) s_prefix = pre;
-    }
-    __syncthreads();
-    const uint32_t base = (uint32_t)s_prefix + excl;
+    if (total == 0) return;
+    const uint32_t base = tile_base + excl;
     if (w0 < p.bwords) {
         // relabel only looks up words holding a present id: empty words need no entry
         if (p.rank && (x.x | x.y | x.z | x.w)) {
@@ -76,7 +102,6 @@ __global__ void __launch_bounds__(kUniqThreads) k_unique(UniqueParams p) {
         }
         if (p.clear && (x.x | x.y | x.z | x.w)) *reinterpret_cast<uint4*>(row + w0) = make_uint4(0, 0, 0, 0);
     }
-    if (t == p.tiles_per_batch - 1 && tid == kUniqThreads - 1) p.ucount[b] = (uint32_t)s_prefix + excl + c0 + c1 + c2 + c3;
 }
 
 // Sparse compaction, fully parallel over the non-empty 32-word blocks (1024 vertices):
@@ -346,7 +371,7 @@ uint64_t gc_summary_words(int64_t num_vertices) {
 size_t gc_unique_temp_bytes(uint32_t num_batches, const gc_visited_t* visited) {
     if (!visited) return 0;
     if (visited->summary) return sparse_layout(num_batches, visited).total;
-    return align_up((size_t)num_batches * uniq_tiles(visited) * sizeof(uint64_t), 256) + 256;
+    return align_up((size_t)num_batches * uniq_tiles(visited) * sizeof(uint32_t), 256);
 }
 
 int gc_unique_compact(const gc_visited_t* visited, uint32_t num_batches, uint32_t* d_unique,
@@ -397,7 +422,6 @@ int gc_unique_compact(const gc_visited_t* visited, uint32_t num_batches, uint32_
         return GC_OK;
     }
     const unsigned tiles = uniq_tiles(visited);
-    const size_t state_bytes = align_up((size_t)num_batches * tiles * sizeof(uint64_t), 256);
     UniqueParams p{};
     p.bm = visited->bitmap;
     p.bwords = visited->words;
@@ -408,12 +432,14 @@ int gc_unique_compact(const gc_visited_t* visited, uint32_t num_batches, uint32_
     p.rank = reinterpret_cast<uint2*>(d_rank_table);
     p.feat = d_feat_lookups;
     p.clear = clear_bitmap;
-    p.tile_state = static_cast<uint64_t*>(d_temp);
-    p.tile_counter = reinterpret_cast<uint32_t*>(static_cast<char*>(d_temp) + state_bytes);
-    GC_TRY(cudaMemsetAsync(d_temp, 0, state_bytes + 256, s), "gc_unique_compact memset");
-    const uint64_t grid = (uint64_t)num_batches * tiles;
-    GC_REQUIRE(grid < (1ull << 31), GC_ERR_VALUE, "gc_unique_compact: window too large");
-    k_unique<<<(unsigned)grid, kUniqThreads, 0, s>>>(p);
+    p.tile_count = static_cast<uint32_t*>(d_temp);
+    GC_REQUIRE(num_batches < 65536, GC_ERR_VALUE, "gc_unique_compact: at most 65535 batches per call");
+    const dim3 grid(tiles, num_batches);
+    k_unique_counts<<<grid, kUniqThreads, 0, s>>>(p);
+    GC_CHECK_LAUNCH("gc_unique_compact counts");
+    k_unique_tile_scan<<<num_batches, 1024, 0, s>>>(p);
+    GC_CHECK_LAUNCH("gc_unique_compact scan");
+    k_unique<<<grid, kUniqThreads, 0, s>>>(p);
     GC_CHECK_LAUNCH("gc_unique_compact");
     return GC_OK;
 }
