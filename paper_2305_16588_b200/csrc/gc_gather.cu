@@ -195,13 +195,17 @@ __global__ void __launch_bounds__(256, GC_GATHER_MIN_BLOCKS) k_gather_rows(Gathe
     }
 }
 
-static int g_defer_ctas = 148;
+// host-row kernel footprint: 2 warps and ~32 registers per thread per CTA, so its CTAs
+// still fit in the few thousand registers the sampling kernels leave free on an SM
+constexpr int kDeferThreads = 64;
+constexpr int kDeferRows = 4;
+static int g_defer_ctas = 296;
 void set_defer_ctas(int ctas) { g_defer_ctas = ctas; }
 
 // Deferred host-tier rows: warp per row, ROWS rows in flight per warp, a small grid
 // (PCIe latency needs few rows in flight; the SMs stay free for the next window).
 template <int ROWS>
-__global__ void __launch_bounds__(128) k_gather_deferred(const char* __restrict__ host_rows, uint32_t row_bytes,
+__global__ void __launch_bounds__(kDeferThreads) k_gather_deferred(const char* __restrict__ host_rows, uint32_t row_bytes,
                                                          const DeferredRow* __restrict__ list,
                                                          const uint32_t* __restrict__ count, char* out) {
     const uint32_t n = *count;
@@ -329,7 +333,7 @@ static int gather_impl(const gc_feature_store_t* store, const uint32_t* d_ids, u
     }
     GC_CHECK_LAUNCH("gc_gather");
     if (defer) {
-        // one 4-warp CTA per SM, 8 rows in flight per warp: ~4.7K rows of PCIe reads
+        // two 2-warp CTAs per SM, 4 rows in flight per warp: ~2.4K rows of PCIe reads
         // outstanding, while the rest of every SM is free for the next window's kernels.
         // On a separate (high-priority) stream its CTAs take SM slots as soon as any
         // free up; `stream` then waits for it, so consumers of `out` stay ordered.
@@ -341,7 +345,7 @@ static int gather_impl(const gc_feature_store_t* store, const uint32_t* d_ids, u
             GC_TRY(cudaEventRecord(e0, s), "event record");
             GC_TRY(cudaStreamWaitEvent(hs, e0, 0), "stream wait");
         }
-        k_gather_deferred<8><<<g_defer_ctas, 128, 0, hs>>>(static_cast<const char*>(store->host_rows), store->row_bytes,
+        k_gather_deferred<kDeferRows><<<g_defer_ctas, kDeferThreads, 0, hs>>>(static_cast<const char*>(store->host_rows), store->row_bytes,
                                                    p.defer, p.defer_count, p.out);
         GC_CHECK_LAUNCH("gc_gather_deferred");
         if (hs != s) {
