@@ -7,6 +7,14 @@ and PCIe transactions from the CPU otherwise. The same rule decides where the K4
 gather fetches each row (cache.FeatureStore), so this report is the transaction
 view of what the device path moves. Baseline cache policies and the experiment
 CLI are out of scope.
+
+The comparison cache policies of the reference (gnnlab-replicated, quiver-plus,
+pagraph-plus next to legion-hierarchical; simulator.py:41-91, :259-402) run through the
+same device kernels: presampling (K2/K3/K5), hotness ranking and prefix split (K6/K8
+helpers), the plan search for the hierarchical policy (K7) and the epoch replay + tier
+accounting (K9). The LDG streaming partitioner they need for more than one clique or
+for pagraph-plus is host preprocessing outside this build: pass its result as
+`partitioning=`.
 """
 
 from __future__ import annotations
@@ -19,8 +27,22 @@ import torch
 from . import _lib
 from .graph import CsrGraph, FeatureSpec
 from .hardware import CliqueLayout, HardwareSpec
-from .planner import CacheAssignment, feature_row_transactions
-from .sampling import GpuTrace, SamplingConfig, run_sampling_epoch
+import warnings
+
+from .graph import TrainingSet
+from .hardware import block_layout
+from .partition import Partitioning, assign_tablets, split_intra_clique
+from .planner import (
+    CacheAssignment,
+    build_candidate_orders,
+    distribute_prefix,
+    feature_row_transactions,
+    hotness_descending_order,
+    materialize_assignment,
+    search_optimal_plan,
+)
+from .rng import derive_seed
+from .sampling import GpuTrace, HotnessMatrices, SamplingConfig, run_presampling, run_sampling_epoch
 
 
 @dataclass
@@ -134,3 +156,153 @@ def hit_rate_summary(report: TrafficReport) -> HitRateSummary:
     agg_f = float((report.feat_local_hits + report.feat_peer_hits).sum() / fl) if fl else 0.0
     return HitRateSummary(topo, feats, agg_t, agg_f, float(topo.max() - topo.min()) if len(topo) else 0.0,
                           float(feats.max() - feats.min()) if len(feats) else 0.0)
+
+
+# ---------------------------------------------------------------------------- policies
+POLICY_HIERARCHICAL = "legion-hierarchical"
+POLICY_REPLICATED = "gnnlab-replicated"
+POLICY_QUIVER = "quiver-plus"
+POLICY_PAGRAPH = "pagraph-plus"
+POLICY_VARIANTS = (POLICY_HIERARCHICAL, POLICY_REPLICATED, POLICY_QUIVER, POLICY_PAGRAPH)
+_GLOBAL_SHUFFLE = (POLICY_REPLICATED, POLICY_QUIVER)  # shuffle the training set globally
+_NO_NVLINK = (POLICY_REPLICATED, POLICY_PAGRAPH)  # no cache sharing over NVLink
+
+
+@dataclass(frozen=True)
+class CachePolicy:
+    """A cache strategy and its per-GPU size (simulator.py:53-84): cache_ratio (fraction
+    of |V| feature rows per GPU) or budget_bytes, else the hardware budget / clique size."""
+
+    variant: str
+    cache_ratio: float | None = None
+    budget_bytes: int | None = None
+    delta_alpha: float = 0.01
+
+    def __post_init__(self):
+        if self.variant not in POLICY_VARIANTS:
+            raise ValueError(f"unknown policy variant {self.variant!r}")
+        if self.cache_ratio is not None and self.budget_bytes is not None:
+            raise ValueError("give cache_ratio or budget_bytes, not both")
+
+    def per_gpu_bytes(self, graph: CsrGraph, feat: FeatureSpec, spec: HardwareSpec | None = None) -> int:
+        if self.cache_ratio is not None:
+            return int(round(self.cache_ratio * graph.num_vertices)) * feat.row_bytes
+        if self.budget_bytes is not None:
+            return self.budget_bytes
+        if spec is None:
+            raise ValueError("policy has no size parameter and no hardware budget to fall back on")
+        return spec.clique_budget_bytes // spec.layout.clique_size
+
+    def per_gpu_rows(self, graph: CsrGraph, feat: FeatureSpec, spec: HardwareSpec) -> int:
+        return self.per_gpu_bytes(graph, feat, spec) // feat.row_bytes
+
+
+def effective_layout(policy: CachePolicy, layout: CliqueLayout) -> CliqueLayout:
+    """Baselines that ignore NVLink run with every GPU in its own clique (simulator.py:87-91)."""
+    return block_layout(layout.num_gpus, 1) if policy.variant in _NO_NVLINK else layout
+
+
+def _need_partitioning(partitioning: Partitioning | None, parts: int, graph: CsrGraph) -> Partitioning:
+    if parts == 1:
+        return Partitioning(np.zeros(graph.num_vertices, dtype=np.int32), 1)
+    if partitioning is None or partitioning.num_parts != parts:
+        raise NotImplementedError(
+            f"this policy needs an LDG partition into {parts} parts (partition_inter_clique, host "
+            "preprocessing outside the B200 path); pass it as partitioning=")
+    return partitioning
+
+
+def policy_seed_pools(policy: CachePolicy, graph: CsrGraph, training: TrainingSet, layout: CliqueLayout, seed: int,
+                      epsilon: float = 0.05, partitioning: Partitioning | None = None) -> list[np.ndarray]:
+    """Per-GPU seed pools under the policy's shuffling discipline (simulator.py:259-278)."""
+    num_gpus = layout.num_gpus
+    if policy.variant in _GLOBAL_SHUFFLE:
+        perm = np.random.default_rng(derive_seed(seed, 0x51)).permutation(training.vertex_ids)
+        return [np.sort(perm[g::num_gpus]) for g in range(num_gpus)]
+    if policy.variant == POLICY_PAGRAPH:
+        parts = _need_partitioning(partitioning, num_gpus, graph)
+        ids = training.vertex_ids
+        return [ids[parts.assignments[ids] == g] for g in range(num_gpus)]
+    parts = _need_partitioning(partitioning, layout.clique_count, graph)
+    return assign_tablets(split_intra_clique(training, parts, layout), layout)
+
+
+def build_policy_cache(policy: CachePolicy, hotness: list[HotnessMatrices], layout: CliqueLayout, graph: CsrGraph,
+                       feat: FeatureSpec, spec: HardwareSpec) -> CacheAssignment:
+    """The cache each policy fills from the presampled hotness (simulator.py:281-347):
+    gnnlab-replicated, one global hottest-row prefix on every GPU; quiver-plus, a
+    clique-size prefix of the global order split by local preference inside each
+    clique; pagraph-plus, each GPU's own hottest rows; legion-hierarchical, the plan
+    search over each clique's hotness."""
+    n = graph.num_vertices
+    num_gpus = layout.num_gpus
+    rows_per_gpu = policy.per_gpu_rows(graph, feat, spec)
+    if policy.variant == POLICY_HIERARCHICAL:
+        budget = policy.per_gpu_bytes(graph, feat, spec) * layout.clique_size
+        orders, plans = [], []
+        for hot in hotness:
+            o = build_candidate_orders(hot)
+            plan, _ = search_optimal_plan(o, budget, policy.delta_alpha, graph, feat, spec, hot.sampling_txn_total)
+            orders.append(o)
+            plans.append(plan)
+        return materialize_assignment(orders, plans, layout, graph, feat, spec)
+    out = CacheAssignment.empty(num_gpus)
+    global_feat = np.zeros(n, dtype=np.int64)
+    for hot in hotness:
+        global_feat += hot.feat_hotness.sum(axis=0)
+    global_order = hotness_descending_order(global_feat)
+    if policy.variant == POLICY_REPLICATED:
+        prefix = global_order[: min(rows_per_gpu, n)]
+        for gpu in range(num_gpus):
+            out.feat_vertices[gpu] = prefix.copy()
+            out.feat_bytes[gpu] = len(prefix) * feat.row_bytes
+        return out
+    if policy.variant == POLICY_QUIVER:
+        if layout.clique_size == 1:
+            warnings.warn("quiver-plus with single-GPU cliques degrades to gnnlab-replicated")
+        for ci, members in enumerate(layout.cliques):
+            k = len(members)
+            prefix = global_order[: min(rows_per_gpu * k, n)]
+            owner = np.argmax(hotness[ci].feat_hotness, axis=0).astype(np.int32)
+            queues = distribute_prefix(prefix, owner, k)
+            for li, gpu in enumerate(members):
+                q = queues[li]
+                out.feat_vertices[gpu] = q
+                out.feat_bytes[gpu] = len(q) * feat.row_bytes
+        return out
+    for ci, members in enumerate(layout.cliques):  # pagraph-plus
+        for li, gpu in enumerate(members):
+            prefix = hotness_descending_order(hotness[ci].feat_hotness[li])[: min(rows_per_gpu, n)]
+            out.feat_vertices[gpu] = prefix
+            out.feat_bytes[gpu] = len(prefix) * feat.row_bytes
+    return out
+
+
+@dataclass
+class PolicyRun:
+    """Everything one policy produced on one configuration (simulator.py:350-359)."""
+
+    policy: CachePolicy
+    layout: CliqueLayout
+    pools: list
+    hotness: list
+    assignment: CacheAssignment
+    report: TrafficReport
+
+
+def run_policy_pipeline(policy: CachePolicy, graph: CsrGraph, training: TrainingSet, layout: CliqueLayout,
+                        cfg: SamplingConfig, spec: HardwareSpec, feat: FeatureSpec, master_seed: int,
+                        epsilon: float = 0.05, partitioning: Partitioning | None = None) -> PolicyRun:
+    """Seed pools, presampling, the policy's cache and one fresh simulated epoch
+    (simulator.py:362-402), all sampling and accounting on the device."""
+    lay = effective_layout(policy, layout)
+    spec_eff = HardwareSpec(layout=lay, clique_budget_bytes=policy.per_gpu_bytes(graph, feat, spec) * lay.clique_size,
+                            cache_line_bytes=spec.cache_line_bytes, uint32_bytes=spec.uint32_bytes,
+                            uint64_bytes=spec.uint64_bytes, float32_bytes=spec.float32_bytes)
+    pools = policy_seed_pools(policy, graph, training, lay, master_seed, epsilon, partitioning)
+    pcfg = SamplingConfig(fanouts=cfg.fanouts, batch_size=cfg.batch_size, presample_epochs=cfg.presample_epochs,
+                          seed=derive_seed(master_seed, 0x10))
+    hotness = run_presampling(graph, pools, lay, pcfg, spec_eff)
+    assignment = build_policy_cache(policy, hotness, lay, graph, feat, spec_eff)
+    report = simulate_epoch(graph, pools, pcfg, assignment, lay, spec_eff, feat, seed=derive_seed(master_seed, 0x20))
+    return PolicyRun(policy, lay, pools, hotness, assignment, report)

@@ -181,10 +181,52 @@ def planner_vectors():
     np.savez_compressed(OUT / "planner.npz", **d)
 
 
+def policy_vectors():
+    """run_policy_pipeline for every cache policy (simulator.py:259-402) on two layouts;
+    the LDG partitions the reference computes (partition.py:85-130) are recorded too,
+    so the device side can be fed the same partitioning."""
+    from gnncache.partition import partition_inter_clique
+    from gnncache.simulator import POLICY_VARIANTS, CachePolicy, run_policy_pipeline
+
+    d = {}
+    g = generate_synthetic(2500, 10, 1.2, seed=41)
+    train = select_training_set(g, 0.1, seed=derive_seed(5, 2))
+    feat = FeatureSpec(64)
+    cfg = SamplingConfig(fanouts=(8, 4), batch_size=32, presample_epochs=1, seed=derive_seed(5, 4))
+    d["graph_ro"], d["graph_ci"], d["train_ids"] = g.row_offsets, g.col_indices, train.vertex_ids
+    cases = []
+    for li, (ngpu, csize) in enumerate([(4, 2), (4, 4)]):
+        layout = block_layout(ngpu, csize)
+        spec = HardwareSpec(layout, clique_budget_bytes=60_000 * csize)
+        for n_parts in {layout.clique_count, layout.num_gpus}:
+            part = partition_inter_clique(g, n_parts, 0.05, derive_seed(5, 0x52))
+            d[f"L{li}_part{n_parts}"] = part.assignments
+        for vi, variant in enumerate(POLICY_VARIANTS):
+            for ri, kw in enumerate([{"cache_ratio": 0.05}, {"budget_bytes": 40_000}]):
+                policy = CachePolicy(variant, **kw)
+                run = run_policy_pipeline(policy, g, train, layout, cfg, spec, feat, master_seed=5, epsilon=0.05)
+                key = f"L{li}_v{vi}_r{ri}"
+                cases.append((li, vi, ri))
+                for gi in range(run.layout.num_gpus):
+                    d[f"{key}_pool{gi}"] = run.pools[gi]
+                    d[f"{key}_topo{gi}"] = run.assignment.topo_vertices[gi]
+                    d[f"{key}_feat{gi}"] = run.assignment.feat_vertices[gi]
+                d[f"{key}_cpu_txn"] = np.array([run.report.total_cpu_txn])
+                d[f"{key}_matrix"] = run.report.traffic_matrix
+                d[f"{key}_csize"] = np.array([run.layout.clique_size])
+    d["cases"] = np.array(cases, dtype=np.int64)
+    d["variants"] = np.array(POLICY_VARIANTS)
+    np.savez_compressed(OUT / "policies.npz", **d)
+
+
 if __name__ == "__main__":
+    if "--policies" in sys.argv:
+        policy_vectors()
+        raise SystemExit(0)
     rng_vectors()
     sampling_vectors()
     presampling_vectors()
     planner_vectors()
+    policy_vectors()
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)

@@ -174,3 +174,53 @@ def test_time_objective_prefers_the_slower_access_shape(golden):
     fast, _ = PL.search_optimal_plan(orders, spec.clique_budget_bytes, 0.01, graph, feat, spec,
                                      hot.sampling_txn_total, bandwidths=MeasuredBandwidths(200.0, 10.0))
     assert fast.alpha <= base.alpha <= slow.alpha
+
+
+def test_cache_policies_match_reference(golden):
+    """run_policy_pipeline for all four policies (simulator.py:259-402) on 4 GPUs as two
+    cliques of 2 and one clique of 4, two size parameters each: seed pools, cache
+    contents and the epoch's CPU transactions / traffic matrix equal the reference's
+    (the LDG partitions are the reference's own, recorded in the golden file)."""
+    import warnings
+
+    import paper_2305_16588_b200 as P
+    from paper_2305_16588_b200 import simulator as S
+
+    g = golden("policies")
+    graph = P.CsrGraph(len(g["graph_ro"]) - 1, len(g["graph_ci"]), g["graph_ro"], g["graph_ci"])
+    train = P.TrainingSet(g["train_ids"], 0.1)
+    feat = P.FeatureSpec(64)
+    cfg = P.SamplingConfig(fanouts=(8, 4), batch_size=32, presample_epochs=1, seed=P.derive_seed(5, 4))
+    for li, vi, ri in g["cases"]:
+        ngpu, csize = [(4, 2), (4, 4)][li]
+        layout = P.block_layout(ngpu, csize)
+        spec = P.HardwareSpec(layout, clique_budget_bytes=60_000 * csize)
+        variant = str(g["variants"][vi])
+        policy = S.CachePolicy(variant, **[{"cache_ratio": 0.05}, {"budget_bytes": 40_000}][ri])
+        parts_needed = ngpu if variant == S.POLICY_PAGRAPH else layout.clique_count
+        part = P.Partitioning(g[f"L{li}_part{parts_needed}"], parts_needed)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            run = S.run_policy_pipeline(policy, graph, train, layout, cfg, spec, feat, master_seed=5, epsilon=0.05,
+                                        partitioning=part)
+        key = f"L{li}_v{vi}_r{ri}"
+        assert run.layout.clique_size == int(g[f"{key}_csize"][0])
+        for gi in range(ngpu):
+            assert np.array_equal(run.pools[gi], g[f"{key}_pool{gi}"]), (key, gi)
+            assert np.array_equal(run.assignment.topo_vertices[gi], g[f"{key}_topo{gi}"]), (key, gi)
+            assert np.array_equal(run.assignment.feat_vertices[gi], g[f"{key}_feat{gi}"]), (key, gi)
+        assert run.report.total_cpu_txn == int(g[f"{key}_cpu_txn"][0]), key
+        assert np.array_equal(run.report.traffic_matrix, g[f"{key}_matrix"]), key
+
+
+def test_policy_without_partition_raises_for_multi_clique():
+    import paper_2305_16588_b200 as P
+    from paper_2305_16588_b200 import simulator as S
+
+    g = P.generate_synthetic(500, 6, 1.2, seed=1)
+    train = P.select_training_set(g, 0.2, seed=3)
+    with pytest.raises(NotImplementedError):
+        S.policy_seed_pools(S.CachePolicy(S.POLICY_PAGRAPH, cache_ratio=0.1), g, train, P.block_layout(4, 2), 5)
+    pools = S.policy_seed_pools(S.CachePolicy(S.POLICY_HIERARCHICAL, cache_ratio=0.1), g, train,
+                                P.block_layout(4, 4), 5)
+    assert sorted(np.concatenate(pools).tolist()) == sorted(train.vertex_ids.tolist())
