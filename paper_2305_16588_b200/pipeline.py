@@ -178,7 +178,8 @@ class SampleGatherPipeline:
         self.launches += max(H, 1)
         end = self._stage("unique_relabel")
         sp.dedup(hot)
-        self.launches += 1 + (H + 1 if sp.relabel else 0)
+        # compaction: tile counts, scan, emit (+ block lists when sparse); one relabel per level
+        self.launches += (4 if sp.summary is not None else 3) + (H + 1 if sp.relabel else 0)
         if end is not None:
             end.record()
         if self.store is not None:
