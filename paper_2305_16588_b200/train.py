@@ -66,13 +66,29 @@ class SAGELayer(nn.Module):
         return self.lin_self(h_self) + self.lin_neigh(segment_mean(h_children, offsets))
 
 
-class GraphSAGE(nn.Module):
-    """L-layer mean-aggregator GraphSAGE on sampled position trees."""
+class GCNLayer(nn.Module):
+    """Graph convolution on a sampled tree: h' = W (h_self + sum of children) / (deg + 1) + b
+    — the mean over the closed neighbourhood (self loop included), one weight matrix."""
 
-    def __init__(self, d_in: int, hidden: int, num_classes: int, num_layers: int):
+    def __init__(self, d_in: int, d_out: int):
+        super().__init__()
+        self.lin = nn.Linear(d_in, d_out)
+
+    def forward(self, h_self, h_children, offsets):
+        deg = (offsets[1:] - offsets[:-1]).to(h_self.dtype).unsqueeze(1)
+        agg = segment_mean(h_children, offsets) * deg  # segment sum (0 for empty segments)
+        return self.lin((h_self + agg) / (deg + 1.0))
+
+
+class GraphSAGE(nn.Module):
+    """L-layer mean-aggregator GraphSAGE on sampled position trees (layer="gcn": the
+    same tree walk with GCNLayer, BASELINE configs[3]'s GCN)."""
+
+    def __init__(self, d_in: int, hidden: int, num_classes: int, num_layers: int, layer: str = "sage"):
         super().__init__()
         dims = [d_in] + [hidden] * num_layers
-        self.layers = nn.ModuleList(SAGELayer(dims[i], dims[i + 1]) for i in range(num_layers))
+        kind = {"sage": SAGELayer, "gcn": GCNLayer}[layer]
+        self.layers = nn.ModuleList(kind(dims[i], dims[i + 1]) for i in range(num_layers))
         self.classifier = nn.Linear(hidden, num_classes)
 
     def forward(self, batch: TreeBatch) -> torch.Tensor:

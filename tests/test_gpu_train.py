@@ -22,7 +22,8 @@ def _cpu_batch(g, table, seeds, fanouts, key, labels):
     return TreeBatch(torch.from_numpy(O.gather(table, uniq)), local, offsets, torch.from_numpy(labels[seeds]))
 
 
-def test_graphsage_loss_parity_fp32():
+@pytest.mark.parametrize("layer", ["sage", "gcn"])
+def test_graphsage_loss_parity_fp32(layer):
     import paper_2305_16588_b200 as P
     from paper_2305_16588_b200.cache import FeatureStore
     from paper_2305_16588_b200.graph import synthetic_features_device
@@ -38,7 +39,7 @@ def test_graphsage_loss_parity_fp32():
     cfg = P.SamplingConfig(fanouts=fanouts, batch_size=128)
     table = O.synthetic_features(np.arange(n), dim)
     labels = synthetic_labels(np.arange(n), classes)
-    model = GraphSAGE(dim, 48, classes, len(fanouts))
+    model = GraphSAGE(dim, 48, classes, len(fanouts), layer=layer)
     cpu_model = copy.deepcopy(model)
     gpu_model = model.cuda()
     opt_g = torch.optim.SGD(gpu_model.parameters(), lr=0.5)
