@@ -356,14 +356,16 @@ def run_b200(args):
     dom = max((k for k in stage if k in stage_bytes), key=lambda k: stage[k][1])
     dom_launches, dom_ms = stage[dom]
     achieved = stage_bytes[dom] / (dom_ms / 1000.0) / 1e9
-    traffic = None
+    traffic, pipes = None, None
     prof = ROOT / "profiles" / "ncu_traffic.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get(dom)
+            pj = json.loads(prof.read_text())
+            traffic = pj.get(dom)
             traffic = float(traffic) if traffic is not None else None
+            pipes = pj.get("_pipes", {}).get(dom)
         except Exception:
-            traffic = None
+            traffic, pipes = None, None
     step_bytes = stats["bytes"]["sampling"] + stats["bytes"]["dedup"] + stats["bytes"]["gather"]
 
     line = {
@@ -376,7 +378,10 @@ def run_b200(args):
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "launches": dom_launches, "avg_launch_ms": dom_ms / max(dom_launches, 1),
-                     "bytes_per_launch": stage_bytes[dom] / max(dom_launches, 1)},
+                     "bytes_per_launch": stage_bytes[dom] / max(dom_launches, 1),
+                     # the kernel is issue/ALU-bound, not HBM-bound: its pipe counters
+                     # from the committed ncu capture (profiles/r01_ncu_full.md)
+                     "ncu_pipes": pipes},
         "step_roofline": {"bytes_per_batch": step_bytes / (nb * args.steps),
                           "t_roof_us_per_batch": step_bytes / (nb * args.steps) / (peak * 1e9) * 1e6,
                           "measured_us_per_batch": total_ms * 1000 / (nb * args.steps),

@@ -130,6 +130,7 @@ def main():
               "FMA pipe % | DRAM % | L2 hit % | warp inst | top stalls (% of samples) |",
               "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
         traffic = defaultdict(lambda: [0.0, 0])
+        pipes = {}
         for d in res:
             md.append(f"| `{d['kernel']}` | {d.get('time', 0):.1f} | {d.get('dram_read', 0) / 1e6:.1f} | "
                       f"{d.get('dram_write', 0) / 1e6:.1f} | {d.get('regs')} | {d.get('occupancy_%', 0):.1f} | "
@@ -139,11 +140,16 @@ def main():
             st = stage_of(d["kernel"], per_launch=True)
             traffic[st][0] += d.get("dram_read", 0) + d.get("dram_write", 0)
             traffic[st][1] += 1
+            if st.startswith("hop_expand"):
+                pipes[st] = {"issue_active_pct": d.get("issue_active_%"), "alu_pipe_pct": d.get("alu_pipe_%"),
+                             "fma_pipe_pct": d.get("fma_pipe_%"), "dram_pct": d.get("dram_%"),
+                             "warp_inst": d.get("warp_inst"), "top_stalls_pct": d["stalls"]}
         (out / f"{a.tag}_ncu_full.md").write_text("\n".join(md) + "\n")
         # per-launch DRAM traffic by stage, consumed by bench.py's roofline.traffic
         (out / "ncu_traffic.json").write_text(json.dumps(
             {k: v[0] / v[1] for k, v in traffic.items()} | {"_source": f"profiles/{a.tag}_ncu_full.md",
-                                                             "_unit": "bytes per launch"}, indent=1) + "\n")
+                                                             "_unit": "bytes per launch", "_pipes": pipes},
+            indent=1) + "\n")
     print("\n".join(lines))
 
 
