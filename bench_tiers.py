@@ -40,7 +40,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--window", type=int, default=256)
     ap.add_argument("--lanes", type=int, default=2, help="concurrent window lanes (inter-batch pipeline)")
-    ap.add_argument("--sweep-lanes", default="", help="extra lanes values to time after the main run, e.g. 1,3,2d (d: host rows deferred)")
+    ap.add_argument("--sweep-lanes", default="", help="extra schedules to time after the main run, e.g. 1,3,2d,2w64 (d: host rows deferred, wN: window)")
     ap.add_argument("--alpha-sweep", type=int, default=0,
                     help="validate the cost model: time one epoch at this many alpha points (+ both objectives' picks)")
     ap.add_argument("--pcie-gbs", type=float, default=64.0, help="nominal PCIe Gen5 x16 GB/s for the tier roofline")
@@ -117,10 +117,13 @@ def main():
     t, f = topo.tier_counts(), fstore.tier_counts()
     sweep = {}
     for tag in [x for x in a.sweep_lanes.split(",") if x]:
-        lanes, defer = int(tag.rstrip("d")), tag.endswith("d")  # "2d": two lanes, host rows deferred
+        # "2": two lanes; "2d": host rows deferred; "2w64": windows of 64 batches
+        head, _, win = tag.partition("w")
+        lanes, defer = int(head.rstrip("d")), head.endswith("d")
+        wsize = int(win) if win else a.window
         del pipe
         torch.cuda.empty_cache()
-        pipe = SampleGatherPipeline(g, cfg, fstore, len(pool), window=min(a.window, nb), feat_rows_cap=60_000,
+        pipe = SampleGatherPipeline(g, cfg, fstore, len(pool), window=min(wsize, nb), feat_rows_cap=60_000,
                                     topology=topo, lanes=lanes, defer_host=defer)
         pipe.run_epoch(plans[0])
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
