@@ -43,10 +43,37 @@ __global__ void k_hash_pairs(uint64_t key, const int64_t* __restrict__ a, const 
 }
 
 // keys[i] = hash_counters(i), vals[i] = i : the inputs of the stable argsort (rng.py:82)
-__global__ void k_perm_keys(uint64_t key, uint64_t* __restrict__ keys, uint32_t* __restrict__ vals, int64_t n) {
+// The permutation sorts the high 32 bits of each key (4 radix passes instead of 8);
+// k_perm_ties then orders every run of equal high words by the full 64-bit key.
+__global__ void k_perm_keys(uint64_t key, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        keys[i] = hash_counter(key, (uint64_t)i);
+        keys[i] = (uint32_t)(hash_counter(key, (uint64_t)i) >> 32);
         vals[i] = (uint32_t)i;
+    }
+}
+
+// A run of equal high words (n^2 / 2^33 pairs expected, almost all of length 2) is in
+// ascending index order after the stable sort; its first thread insertion-sorts it by
+// (full key, index) — the order of argsort(kind="stable") on the 64-bit keys.
+__global__ void k_perm_ties(uint64_t key, const uint32_t* __restrict__ hi, uint32_t* __restrict__ perm, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i + 1 < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t h = hi[i];
+        if (hi[i + 1] != h || (i > 0 && hi[i - 1] == h)) continue;  // not the start of a run
+        int64_t j = i + 1;
+        while (j + 1 < n && hi[j + 1] == h) ++j;
+        for (int64_t a = i + 1; a <= j; ++a) {
+            const uint32_t pa = perm[a];
+            const uint64_t ka = hash_counter(key, pa);
+            int64_t b = a - 1;
+            while (b >= i) {
+                const uint32_t pb = perm[b];
+                const uint64_t kb = hash_counter(key, pb);
+                if (kb < ka || (kb == ka && pb < pa)) break;
+                perm[b + 1] = pb;
+                --b;
+            }
+            perm[b + 1] = pa;
+        }
     }
 }
 
@@ -65,12 +92,12 @@ struct PermLayout {
 static PermLayout perm_layout(int64_t n) {
     PermLayout L{};
     size_t cub_bytes = 0;
-    cub::DoubleBuffer<uint64_t> kb(nullptr, nullptr);
+    cub::DoubleBuffer<uint32_t> kb(nullptr, nullptr);
     cub::DoubleBuffer<uint32_t> vb(nullptr, nullptr);
     cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, kb, vb, (int)(n > 0 ? n : 1));
     size_t off = 0;
-    L.keys0 = off; off = align_up(off + 8 * (size_t)n, 256);
-    L.keys1 = off; off = align_up(off + 8 * (size_t)n, 256);
+    L.keys0 = off; off = align_up(off + 4 * (size_t)n, 256);
+    L.keys1 = off; off = align_up(off + 4 * (size_t)n, 256);
     L.vals0 = off; off = align_up(off + 4 * (size_t)n, 256);
     L.vals1 = off; off = align_up(off + 4 * (size_t)n, 256);
     L.cub = off; off = align_up(off + cub_bytes, 256);
@@ -133,18 +160,21 @@ int gc_permutation(uint64_t key, int64_t n, const int64_t* d_pool, int64_t* d_ou
     GC_REQUIRE(temp_bytes >= L.total && d_temp, GC_ERR_VALUE, "gc_permutation: temp buffer too small");
     char* t = static_cast<char*>(d_temp);
     cudaStream_t s = as_stream(stream);
-    auto* k0 = reinterpret_cast<uint64_t*>(t + L.keys0);
-    auto* k1 = reinterpret_cast<uint64_t*>(t + L.keys1);
+    auto* k0 = reinterpret_cast<uint32_t*>(t + L.keys0);
+    auto* k1 = reinterpret_cast<uint32_t*>(t + L.keys1);
     auto* v0 = reinterpret_cast<uint32_t*>(t + L.vals0);
     auto* v1 = reinterpret_cast<uint32_t*>(t + L.vals1);
     k_perm_keys<<<grid_for(n, 256), 256, 0, s>>>(key, k0, v0, n);
     GC_CHECK_LAUNCH("gc_permutation keys");
     // LSD radix sort is stable: equal keys keep ascending index, matching
-    // np.argsort(kind="stable") (rng.py:82).
-    cub::DoubleBuffer<uint64_t> kb(k0, k1);
+    // np.argsort(kind="stable") (rng.py:82); ties of the high words are then ordered
+    // by the full keys.
+    cub::DoubleBuffer<uint32_t> kb(k0, k1);
     cub::DoubleBuffer<uint32_t> vb(v0, v1);
     size_t cub_bytes = L.cub_bytes;
-    GC_TRY(cub::DeviceRadixSort::SortPairs(t + L.cub, cub_bytes, kb, vb, (int)n, 0, 64, s), "gc_permutation sort");
+    GC_TRY(cub::DeviceRadixSort::SortPairs(t + L.cub, cub_bytes, kb, vb, (int)n, 0, 32, s), "gc_permutation sort");
+    k_perm_ties<<<grid_for(n, 256), 256, 0, s>>>(key, kb.Current(), vb.Current(), n);
+    GC_CHECK_LAUNCH("gc_permutation ties");
     k_perm_emit<<<grid_for(n, 256), 256, 0, s>>>(vb.Current(), d_pool, d_out, n);
     GC_CHECK_LAUNCH("gc_permutation emit");
     return GC_OK;

@@ -24,8 +24,8 @@ from .rng import ROLE_SHUFFLE, KeyedRng
 from .sampling import DeviceHotness, SamplingConfig, WindowSampler, batch_hop_keys
 
 # kernels each stage launches (for the bench's gpu_launches count): CUB's onesweep
-# radix sort of 64-bit keys is 1 histogram + 1 scan + 8 digit passes (ncu launch list)
-LAUNCHES_PERMUTATION = 2 + 10
+# radix sort of the keys' high 32 bits is 1 histogram + 1 scan + 4 digit passes, plus keys, ties, emit
+LAUNCHES_PERMUTATION = 3 + 6
 
 
 @dataclass

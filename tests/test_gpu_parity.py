@@ -39,11 +39,16 @@ def test_rng_device_matches_reference(golden):
         assert np.array_equal(P.KeyedRng(pk).permutation(n), g[f"perm_{n}"]), n
 
 
-def test_permutation_large_matches_oracle():
+@pytest.mark.parametrize("n", [1_390_000, 4_000_000])
+def test_permutation_large_matches_oracle(n):
+    """1.39M = one C3 tablet at 8 GPUs; 4M keys hold ~1.9K pairs of equal high words,
+    which the 32-bit radix sort leaves to the tie fix-up."""
     P = _pkg()
     key = P.KeyedRng(99).derive(1).key
-    n = 1_390_000  # one C3 tablet at 8 GPUs
-    assert np.array_equal(P.KeyedRng(key).permutation(n), O.permutation(key, n))
+    want = O.permutation(key, n)
+    hi = (O.hash_counters(key, np.arange(n)) >> np.uint64(32))[want]
+    assert (hi[1:] == hi[:-1]).sum() > 100  # the fix-up path is exercised
+    assert np.array_equal(P.KeyedRng(key).permutation(n), want)
 
 
 def test_shuffle_fused_gather():
