@@ -35,7 +35,12 @@ sys.path.insert(0, str(ROOT))
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--scale", type=float, default=0.1)
-    ap.add_argument("--budget-frac", type=float, default=0.1, help="cache budget / (topology + feature bytes)")
+    ap.add_argument("--budget-frac", type=float, default=0.1,
+                    help="per-GPU cache budget / (topology + feature bytes); the clique budget is K times it")
+    ap.add_argument("--clique", type=int, default=1,
+                    help="emulate GPU 0 of a K-GPU NVSwitch clique on this one GPU: K tablets, the K-way "
+                         "partitioned cache with every peer slab in local HBM (peer rows then move at HBM "
+                         "speed; the tier roofline still charges them to NVLink)")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--window", type=int, default=256)
@@ -62,11 +67,12 @@ def main():
     deg, dim, fanouts, bs = 14, 128, (25, 10), 1024
     g = P.generate_synthetic(n, deg, 1.2, seed=P.derive_seed(7, 1))
     train = P.select_training_set(g, 0.1, seed=P.derive_seed(7, 2))
-    layout = P.block_layout(1, 1)
+    K = a.clique
+    layout = P.block_layout(K, K)
     pools = P.assign_tablets(P.split_intra_clique(train, single_clique_partitioning(g), layout), layout)
     feat = P.FeatureSpec(dim)
     total_bytes = g.num_edges * 4 + 8 * n + n * feat.row_bytes
-    budget = int(a.budget_frac * total_bytes)
+    budget = int(a.budget_frac * total_bytes) * K
     spec = P.HardwareSpec(layout, clique_budget_bytes=budget)
     cfg = P.SamplingConfig(fanouts=fanouts, batch_size=bs, presample_epochs=1, seed=P.derive_seed(7, 4))
 
@@ -155,6 +161,7 @@ def main():
         seq.run_epoch(plans[a.warmup + s], on_window=account)
     torch.cuda.synchronize()
     batches = nb * a.steps
+    clique_batches = sum(math.ceil(len(pl) / bs) for pl in pools)  # the presampling epoch's batches
     row_txns = PL.feature_row_transactions(feat, spec)
     cls = spec.cache_line_bytes
     measured_txn = t["host_txn"] + f["host"] * row_txns
@@ -178,13 +185,14 @@ def main():
         "steps": a.steps,
         "config": {"workload": f"C3 ogbn-papers100M-shaped synthetic x{a.scale}", "num_vertices": n,
                    "num_edges": g.num_edges, "feature_dim": dim, "fanouts": list(fanouts), "batch_size": bs,
-                   "budget_bytes": budget, "budget_frac": a.budget_frac, "batches_per_epoch": nb},
+                   "budget_bytes": budget, "budget_frac_per_gpu": a.budget_frac, "batches_per_epoch": nb,
+                   "clique": K, "peers": "emulated in local HBM" if K > 1 else None},
         "plan": {"alpha": plan.alpha, "topo_prefix_len": est.topo_prefix_len, "feat_prefix_len": est.feat_prefix_len,
                  "predicted_txn_per_epoch": pred_txn, "presample_txn_total": hot.sampling_txn_total},
         "pcie": {
             "measured_gb_per_batch": measured_txn * cls / batches / 1e9,
-            "predicted_gb_per_batch": pred_txn * cls / nb / 1e9,
-            "measured_over_predicted": (measured_txn / batches) / (pred_txn / nb) if pred_txn else None,
+            "predicted_gb_per_batch": pred_txn * cls / clique_batches / 1e9,
+            "measured_over_predicted": (measured_txn / batches) / (pred_txn / clique_batches) if pred_txn else None,
             "payload_gb_per_batch": (t["reads_host"] * 16 + t["edges_host"] * 4 + f["host"] * feat.row_bytes)
             / batches / 1e9,
             "unit_note": "transactions x 64 B cache lines, the reference's PCIe unit (SPEC.md:403)",
