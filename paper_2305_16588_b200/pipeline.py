@@ -69,7 +69,7 @@ class SampleGatherPipeline:
     def __init__(self, graph: CsrGraph, cfg: SamplingConfig, store: FeatureStore | None, max_pool: int,
                  window: int | None = None, relabel: bool = True, feat_rows_cap: int | None = None,
                  placement: str = "hbm", topology=None, sparse_visited: bool | None = None, lanes: int = 1,
-                 defer_host: bool | None = None):
+                 defer_host: bool | None = None, overlap_relabel: bool = True):
         self.graph = graph
         self.cfg = cfg
         self.store = store
@@ -98,6 +98,8 @@ class SampleGatherPipeline:
         self.host_stream = torch.cuda.Stream(priority=-1) if self.defer_host and lanes > 1 else None
         self.sampler = self.lane_samplers[0]
         self.features = self.lane_features[0]
+        # relabel overlaps the gather on a side stream (None: run them back to back)
+        self._relabel_side = torch.cuda.Stream() if overlap_relabel else None
         self.feat_cap = self.sampler.ucap
         self.timer: StageTimer | None = None
         self.launches = 0
@@ -177,7 +179,10 @@ class SampleGatherPipeline:
         sp.expand(hot, timer=self.timer)
         self.launches += max(H, 1)
         end = self._stage("unique_relabel")
-        sp.dedup(hot)
+        # relabel and gather both only need the compaction: with the side stream the two
+        # HBM-bound passes share the GPU instead of running back to back
+        side = self._relabel_side if (self.store is not None and self.timer is None) else None
+        sp.dedup(hot, relabel_stream=side)
         # compaction: tile counts, scan, emit (+ block lists when sparse); one relabel per level
         self.launches += (4 if sp.summary is not None else 3) + (H + 1 if sp.relabel else 0)
         if end is not None:
@@ -189,6 +194,10 @@ class SampleGatherPipeline:
             self.launches += 1
             if end is not None:
                 end.record()
+        if side is not None:
+            joined = torch.cuda.Event()
+            joined.record(side)
+            torch.cuda.current_stream().wait_event(joined)
         if on_window is not None:
             on_window(self, w0, nb)
 

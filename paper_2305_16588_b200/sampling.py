@@ -250,9 +250,11 @@ class WindowSampler:
                 "mark_visited",
             )
 
-    def dedup(self, hot: DeviceHotness | None = None, stream=None) -> None:
+    def dedup(self, hot: DeviceHotness | None = None, stream=None, relabel_stream=None) -> None:
         """Sorted unique ids per batch; the visited bitmap is cleared as it is consumed
-        (relabel reads the interleaved rank table instead)."""
+        (relabel reads the interleaved rank table instead). relabel_stream: run the
+        relabel launches there (ordered after the compaction) so they overlap whatever
+        the caller enqueues next on `stream`; the caller joins that stream."""
         s = _lib.stream_handle(stream)
         _lib.check(
             self.lib.gc_unique_compact(
@@ -263,6 +265,11 @@ class WindowSampler:
             "unique_compact",
         )
         if self.relabel:
+            if relabel_stream is not None:
+                ready = torch.cuda.Event()
+                ready.record(stream if stream is not None else torch.cuda.current_stream())
+                relabel_stream.wait_event(ready)
+                s = _lib.stream_handle(relabel_stream)
             arrays = [(self.seeds, self.counts[0], self.local_seeds, self.B)] + [
                 (self.nbrs[h], self.counts[h + 1], self.local_nbrs[h], self.caps[h + 1]) for h in range(self.H)
             ]
