@@ -123,10 +123,15 @@ def main():
     t, f = topo.tier_counts(), fstore.tier_counts()
     sweep = {}
     for tag in [x for x in a.sweep_lanes.split(",") if x]:
-        # "2": two lanes; "2d": host rows deferred; "2w64": windows of 64 batches
-        head, _, win = tag.partition("w")
+        # "2": two lanes; "2d": host rows deferred; "2w64": windows of 64 batches;
+        # "2g2": gather grid of 2 CTAs per SM
+        from paper_2305_16588_b200 import _lib
+
+        head, _, gsm = tag.partition("g")
+        head, _, win = head.partition("w")
         lanes, defer = int(head.rstrip("d")), head.endswith("d")
         wsize = int(win) if win else a.window
+        _lib.check(_lib.lib().gc_set_option(_lib.GC_OPT_GATHER_CTAS_PER_SM, int(gsm) if gsm else 16))
         del pipe
         torch.cuda.empty_cache()
         pipe = SampleGatherPipeline(g, cfg, fstore, len(pool), window=min(wsize, nb), feat_rows_cap=60_000,
@@ -139,6 +144,7 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         sweep[tag] = nb * a.steps / (e0.elapsed_time(e1) / 1000.0)
+        _lib.check(_lib.lib().gc_set_option(_lib.GC_OPT_GATHER_CTAS_PER_SM, 16))
     seq = pipe
     if a.lanes > 1 or sweep:
         del pipe

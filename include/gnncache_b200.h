@@ -53,6 +53,10 @@ int gc_abi_version(void);
 /* GC_OPT_DEFER_CTAS: CTAs (128 threads each) of gc_gather_deferred's host-row kernel
  * (default 148, one per SM); a tuning knob for the PCIe-bound part. */
 #define GC_OPT_DEFER_CTAS 2
+/* GC_OPT_GATHER_CTAS_PER_SM: grid of the warp-per-row gather in CTAs per SM over the
+ * whole window (default 16: the GPU is full). Fewer leave SM room for another lane's
+ * kernels while a PCIe-bound gather runs. */
+#define GC_OPT_GATHER_CTAS_PER_SM 3
 int gc_set_option(int option, int value);
 const char* gc_last_error(void);
 /* device ordinal of the calling thread's current device; -1 if none */

@@ -121,6 +121,7 @@ __device__ __forceinline__ void mark_visited(uint32_t* bm, uint32_t* sm, uint32_
 
 void set_error(const std::string& msg);
 void set_defer_ctas(int ctas);  // gc_gather.cu
+void set_gather_ctas_per_sm(int v);  // gc_gather.cu
 int cuda_status(cudaError_t err, const char* what);
 
 #define GC_CHECK_LAUNCH(what)                                               \

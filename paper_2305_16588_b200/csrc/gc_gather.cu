@@ -201,6 +201,10 @@ constexpr int kDeferThreads = 64;
 constexpr int kDeferRows = 4;
 static int g_defer_ctas = 296;
 void set_defer_ctas(int ctas) { g_defer_ctas = ctas; }
+// warp-per-row gather grid: CTAs per SM over the whole window (16 fills the GPU; fewer
+// leave room for another lane's kernels while a PCIe-bound gather runs)
+static int g_gather_ctas_per_sm = 16;
+void set_gather_ctas_per_sm(int v) { g_gather_ctas_per_sm = v; }
 
 // Deferred host-tier rows: warp per row, ROWS rows in flight per warp, a small grid
 // (PCIe latency needs few rows in flight; the SMs stay free for the next window).
@@ -322,7 +326,8 @@ static int gather_impl(const gc_feature_store_t* store, const uint32_t* d_ids, u
         // warp per row, 32-row chunks per warp, 4 rows in flight; ~16 resident warps per
         // SM per batch slice
         uint64_t wx = ((uint64_t)max_count + 32 * 8 - 1) / (32 * 8);
-        const uint64_t wcap = (uint64_t)148 * 16 / num_batches;
+        uint64_t wcap = (uint64_t)148 * g_gather_ctas_per_sm / num_batches;
+        if (wcap < 1) wcap = 1;
         if (wx > wcap) wx = wcap;
         if (wx < 1) wx = 1;
         k_gather_rows<GC_GATHER_ROWS><<<dim3((unsigned)wx, num_batches), 256, 0, s>>>(p);

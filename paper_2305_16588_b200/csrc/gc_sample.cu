@@ -589,6 +589,11 @@ using namespace gc;
 extern "C" {
 
 int gc_set_option(int option, int value) {
+    if (option == GC_OPT_GATHER_CTAS_PER_SM) {
+        GC_REQUIRE(value >= 1 && value <= 64, GC_ERR_VALUE, "gc_set_option: GC_OPT_GATHER_CTAS_PER_SM out of range");
+        gc::set_gather_ctas_per_sm(value);
+        return GC_OK;
+    }
     if (option == GC_OPT_DEFER_CTAS) {
         GC_REQUIRE(value >= 1 && value <= 65535, GC_ERR_VALUE, "gc_set_option: GC_OPT_DEFER_CTAS out of range");
         gc::set_defer_ctas(value);
