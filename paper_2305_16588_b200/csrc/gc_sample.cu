@@ -1,15 +1,17 @@
 // K2 hop_expand: one hop of the reference's L-hop sampler (_expand_frontier,
 // sampling.py:84-117) for a window of W independent mini-batches in one launch.
 //
-// Per CTA tile of 256 frontier positions (claimed in order from a counter):
+// Per CTA tile of up to 256 frontier positions (tile id = blockIdx.x):
 //   phase 1  thread-per-position: v, row offsets, deg, take = min(deg, fanout);
 //            presampling counters (warp-aggregated), seed marking; CTA scan of take;
 //            the tile aggregate is published for the decoupled look-back.
-//   phase 2a warp-per-position selection into a shared-memory list of source edge
-//            indices (copy path: CSR order; choice path: the `fanout` smallest
-//            (hash_pairs(i, j), j) in ascending order — bit-exact with the lexsort at
-//            sampling.py:108-114 and the scalar oracle tests/helpers.py:95-110).
-//   look-back exclusive prefix of the batch's output (overlaps phase 2a latency).
+//   phase 2a selection into a shared-memory list of source edge indices (copy path:
+//            CSR order; choice path: the `fanout` smallest (hash_pairs(i, j), j) in
+//            ascending order — bit-exact with the lexsort at sampling.py:108-114 and
+//            the scalar oracle tests/helpers.py:95-110) — thread-per-position sorted
+//            networks for short lists, warp-per-position extraction otherwise.
+//   look-back exclusive prefix of the batch's output (after phase 2a, so the
+//            predecessor tiles have normally finished).
 //   phase 2b flat, coalesced emission: out[prefix + k] = col[src_edge[k]], marking the
 //            batch's visited bitmap for dedup (K3).
 // Keys depend only on (position, edge index), never on neighbour ids (rng.py:68-72),
@@ -84,7 +86,6 @@ struct HopParams {
     uint32_t cls;
     uint32_t u32b;
     uint64_t* tile_state;
-    uint32_t* tile_counter;
     int exact_only;  // test hook: always take the 64-bit extraction path
     uint32_t k32;    // == 32, opaque to the compiler (see PairHashHigh::hi_counter)
 };
@@ -671,8 +672,7 @@ int gc_hop_expand(const gc_topology_t* topo, const uint32_t* d_frontier, uint64_
     }
     const size_t state_bytes = align_up((size_t)num_batches * tiles * sizeof(uint64_t), 256);
     p.tile_state = static_cast<uint64_t*>(d_temp);
-    p.tile_counter = reinterpret_cast<uint32_t*>(static_cast<char*>(d_temp) + state_bytes);
-    GC_TRY(cudaMemsetAsync(d_temp, 0, state_bytes + 256, s), "gc_hop_expand memset");
+    GC_TRY(cudaMemsetAsync(d_temp, 0, state_bytes, s), "gc_hop_expand memset");
     const uint64_t grid = (uint64_t)num_batches * tiles;
     GC_REQUIRE(grid < (1ull << 31), GC_ERR_VALUE, "gc_hop_expand: window too large");
     const bool tiered = topo->location != nullptr || topo->full_on_host;
