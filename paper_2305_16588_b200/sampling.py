@@ -451,14 +451,24 @@ class EpochRunner:
         pool_dev = torch.from_numpy(np.ascontiguousarray(pool, dtype=np.int64)).cuda()
         shuffled = gpu_stream.derive(ROLE_SHUFFLE).permutation_device(L, pool_dev).to(torch.int32)
         nb = math.ceil(L / B)
-        keys = batch_hop_keys(gpu_stream, 0, nb, len(self.cfg.fanouts))
-        W = self.sampler.W
+        H = len(self.cfg.fanouts)
+        # the epoch's batch sizes and hop keys go to the device once: per window only
+        # device-to-device copies, so no pageable copy stalls the host between windows
+        counts = np.full(nb, B, dtype=np.int32)
+        counts[-1] = L - (nb - 1) * B
+        d_counts = torch.from_numpy(counts).cuda()
+        d_keys = torch.from_numpy(batch_hop_keys(gpu_stream, 0, nb, H).view(np.int64)).cuda() if H else None
+        sp = self.sampler
+        W = sp.W
         for w0 in range(0, nb, W):
             w1 = min(nb, w0 + W)
-            counts = np.full(w1 - w0, B, dtype=np.int64)
-            counts[-1] = min(B, L - (w1 - 1) * B)
-            self.sampler.load(shuffled[w0 * B :], counts, keys[w0:w1])
-            self.sampler.run(hot)
+            lo, hi = w0 * B, min(L, w1 * B)
+            sp.active = w1 - w0
+            sp.seeds.view(-1)[: hi - lo].copy_(shuffled[lo:hi])
+            sp.counts[0, : w1 - w0].copy_(d_counts[w0:w1])
+            if H:
+                sp.keys[:, : w1 - w0].copy_(d_keys[w0:w1].t())
+            sp.run(hot)
         return nb
 
 
