@@ -16,6 +16,8 @@
 //            batch's visited bitmap for dedup (K3).
 // Keys depend only on (position, edge index), never on neighbour ids (rng.py:68-72),
 // so only the `take` selected column entries are read from the topology.
+#include <type_traits>
+
 #include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 
@@ -92,8 +94,11 @@ struct HopParams {
 
 static int g_exact_only = 0;
 
-__device__ __forceinline__ void stage(uint64_t* s_items, uint32_t item, uint32_t r0, uint32_t r1, uint64_t edge) {
-    if (item >= r0 && item < r1) s_items[item - r0] = edge;
+// Staged output items: u64 edge indices (tier code in bits 56..63 when TIERED), or u32
+// edge indices for the plain CSR (m < 2^32), which halves the staging traffic.
+template <typename Item>
+__device__ __forceinline__ void stage(Item* s_items, uint32_t item, uint32_t r0, uint32_t r1, uint64_t edge) {
+    if (item >= r0 && item < r1) s_items[item - r0] = (Item)edge;
 }
 
 // Exact winner among lanes in `cand` by (lo32 of key, edge index) once the high
@@ -117,9 +122,9 @@ __device__ __forceinline__ uint32_t tie_break(unsigned cand, uint64_t key, uint3
 
 // Choice path with every candidate key resident in registers: lane l holds edges
 // j = l + 32 r for r < R. Extracts the first min(fanout, needed) minima in order.
-template <int R>
+template <int R, typename Item>
 __device__ __forceinline__ void select_registers(uint64_t hc, uint32_t deg, uint32_t fanout, uint64_t o0,
-                                                 uint32_t excl, uint32_t r0, uint32_t r1, uint64_t* s_items) {
+                                                 uint32_t excl, uint32_t r0, uint32_t r1, Item* s_items) {
     const int lane = threadIdx.x & 31;
     uint64_t key[R];
     uint32_t rank[R];
@@ -183,9 +188,9 @@ __device__ __forceinline__ void select_registers(uint64_t hc, uint32_t deg, uint
 // prefixes among consecutively extracted values (one extra extraction covers the
 // selection boundary), in which case this returns false and the caller reruns the
 // exact 64-bit path. Ties need two of <=128 uniform keys to agree in 25-27 bits.
-template <int R>
+template <int R, typename Item>
 __device__ __forceinline__ bool select_packed(uint64_t hc, uint32_t deg, uint32_t fanout, uint64_t o0, uint32_t excl,
-                                              uint32_t r0, uint32_t r1, uint64_t* s_items) {
+                                              uint32_t r0, uint32_t r1, Item* s_items) {
     constexpr int IB = R == 1 ? 5 : (R == 2 ? 6 : 7);
     constexpr uint32_t kIdx = (1u << IB) - 1u;
     const uint32_t lane = threadIdx.x & 31;
@@ -231,8 +236,9 @@ __device__ __forceinline__ bool select_packed(uint64_t hc, uint32_t deg, uint32_
 
 // Choice path for long adjacency lists: keys are recomputed each extraction step
 // above the last emitted (key, j), so any degree is handled exactly.
+template <typename Item>
 __device__ void select_streaming(uint64_t hc, uint32_t deg, uint32_t fanout, uint64_t o0, uint32_t excl, uint32_t r0,
-                                 uint32_t r1, uint64_t* s_items) {
+                                 uint32_t r1, Item* s_items) {
     const int lane = threadIdx.x & 31;
     uint64_t lk = 0;
     uint32_t lj = 0;
@@ -297,9 +303,9 @@ __host__ __device__ constexpr int peeled_candidates() {
     return S == 4 ? 2 : S == 6 ? 5 : S == 8 ? 7 : S == 11 ? 9 : S == 16 ? 12 : S == 21 ? 17 : S == 26 ? 22 : 27;
 }
 
-template <int S>
+template <int S, typename Item>
 __device__ __forceinline__ bool select_thread(uint64_t hc, uint32_t deg, uint32_t fanout, uint64_t o0, uint32_t excl,
-                                              uint32_t r0, uint32_t r1, uint64_t* s_items, uint32_t k32) {
+                                              uint32_t r0, uint32_t r1, Item* s_items, uint32_t k32) {
     constexpr int IB = 7;
     constexpr uint32_t kKeep = ~((1u << IB) - 1u);
     constexpr int TRI = peeled_candidates<S>() & ~1;  // peeled in pairs
@@ -330,8 +336,9 @@ __device__ __forceinline__ bool select_thread(uint64_t hc, uint32_t deg, uint32_
 }
 
 // Warp-cooperative selection of one position (long lists, wide fanouts, tie redo).
+template <typename Item>
 __device__ __forceinline__ void select_warp(uint64_t hc, uint32_t d, uint32_t fanout, uint64_t base, uint32_t e0,
-                                            uint32_t r0, uint32_t r1, uint64_t* s_items, bool exact) {
+                                            uint32_t r0, uint32_t r1, Item* s_items, bool exact) {
     if (exact && d <= 128) {
         if (d <= 32)
             select_registers<1>(hc, d, fanout, base, e0, r0, r1, s_items);
@@ -363,7 +370,8 @@ __global__ void __launch_bounds__(kHopThreads, hop_min_blocks<S>()) k_hop_expand
         typename Scan::TempStorage scan;
         typename Reduce::TempStorage reduce;
     } tmp;
-    __shared__ uint64_t s_items[kItemCap];
+    using Item = typename std::conditional<TIERED, uint64_t, uint32_t>::type;
+    __shared__ Item s_items[kItemCap];
     __shared__ uint64_t s_prefix;
 
     const int tid = threadIdx.x;
@@ -524,7 +532,7 @@ __global__ void __launch_bounds__(kHopThreads, hop_min_blocks<S>()) k_hop_expand
                 const uint32_t k = k0 + q * kHopThreads;
                 u[q] = 0;
                 if (k < cnt) {
-                    const uint64_t it = s_items[k];
+                    const uint64_t it = s_items[k];  // u32 items widen for the plain CSR
                     if (TIERED) {
                         const uint32_t code = (uint32_t)(it >> kTierShift);
                         const uint32_t* cols = code ? p.scols[code - 1] : p.ci;
@@ -675,7 +683,9 @@ int gc_hop_expand(const gc_topology_t* topo, const uint32_t* d_frontier, uint64_
     GC_TRY(cudaMemsetAsync(d_temp, 0, state_bytes, s), "gc_hop_expand memset");
     const uint64_t grid = (uint64_t)num_batches * tiles;
     GC_REQUIRE(grid < (1ull << 31), GC_ERR_VALUE, "gc_hop_expand: window too large");
-    const bool tiered = topo->location != nullptr || topo->full_on_host;
+    // the plain-CSR kernel stages 32-bit edge indices; a CSR with 2^32 or more edges
+    // takes the tiered kernel (64-bit items), which also reads a location-free CSR
+    const bool tiered = topo->location != nullptr || topo->full_on_host || graph->num_edges >= (1ull << 32);
     switch (network_slots(fanout)) {
         case 4: launch_hop<4>(p, (unsigned)grid, tiered, s); break;
         case 6: launch_hop<6>(p, (unsigned)grid, tiered, s); break;
