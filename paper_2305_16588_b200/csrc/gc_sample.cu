@@ -303,7 +303,9 @@ __host__ __device__ constexpr int peeled_candidates() {
     return S == 4 ? 2 : S == 6 ? 5 : S == 8 ? 7 : S == 11 ? 9 : S == 16 ? 12 : S == 21 ? 17 : S == 26 ? 22 : 27;
 }
 
-template <int S, typename Item>
+// CHECKED = false: the tile stages in one round (r0 = 0, every item in range), so the
+// per-item window test is dropped
+template <int S, bool CHECKED, typename Item>
 __device__ __forceinline__ bool select_thread(uint64_t hc, uint32_t deg, uint32_t fanout, uint64_t o0, uint32_t excl,
                                               uint32_t r0, uint32_t r1, Item* s_items, uint32_t k32) {
     constexpr int IB = 7;
@@ -330,8 +332,13 @@ __device__ __forceinline__ bool select_thread(uint64_t hc, uint32_t deg, uint32_
     if (tie) return false;
 #pragma unroll
     for (int s = 0; s < S; ++s)
-        if (s < (int)fanout)
-            stage(s_items, excl + s, r0, r1, o0 + ((t[s] & ((1u << IB) - 1u)) - kGoldenLow));
+        if (s < (int)fanout) {
+            const uint64_t e = o0 + ((t[s] & ((1u << IB) - 1u)) - kGoldenLow);
+            if (CHECKED)
+                stage(s_items, excl + s, r0, r1, e);
+            else
+                s_items[excl + s] = (Item)e;
+        }
     return true;
 }
 
@@ -477,9 +484,16 @@ __global__ void __launch_bounds__(kHopThreads, hop_min_blocks<S>()) k_hop_expand
         bool need_warp = false;
         if (valid && take && excl + take > r0 && excl < r1) {
             if (thread_copy) {
-                for (uint32_t k = 0; k < deg; ++k) stage(s_items, excl + k, r0, r1, o0 + k);
+                if (rounds <= 1)
+                    for (uint32_t k = 0; k < deg; ++k) s_items[excl + k] = (Item)(o0 + k);
+                else
+                    for (uint32_t k = 0; k < deg; ++k) stage(s_items, excl + k, r0, r1, o0 + k);
             } else if (thread_choice) {
-                need_warp = !select_thread<(S > 0 ? S : 4)>(hc, deg, p.fanout, o0, excl, r0, r1, s_items, p.k32);
+                need_warp = rounds <= 1
+                                ? !select_thread<(S > 0 ? S : 4), false>(hc, deg, p.fanout, o0, excl, r0, r1, s_items,
+                                                                        p.k32)
+                                : !select_thread<(S > 0 ? S : 4), true>(hc, deg, p.fanout, o0, excl, r0, r1, s_items,
+                                                                       p.k32);
             } else {
                 need_warp = true;
             }
