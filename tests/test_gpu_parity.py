@@ -273,3 +273,30 @@ def test_packed_and_exact_selection_agree(deg, fanouts):
     want = O.sample_batch(gr.row_offsets, gr.col_indices, gr.num_vertices, seeds, fanouts, stream.key)
     for a, (_, off, nbr) in zip(exact.hops, want):
         assert np.array_equal(a.neighbors, nbr)
+
+
+@pytest.mark.parametrize("fanouts", [(10, 5), (3, 300), (64, 1)])
+def test_heavy_tailed_out_degrees_match_oracle(fanouts):
+    """Power-law out-degrees (the reference generator's are constant): most lists are
+    short, a few hubs hold 1K-3K edges, some vertices have none — every selection path
+    (thread network, packed/exact warp extraction, streaming extraction, copy) and
+    multi-round staging (fanout 300) in one batch."""
+    P = _pkg()
+    rng = np.random.default_rng(sum(fanouts))
+    n = 30_000
+    deg = np.minimum((rng.pareto(1.1, n) * 3).astype(np.int64), 3000)
+    deg[rng.choice(n, 20, replace=False)] = rng.integers(1000, 3001, 20)
+    src = np.repeat(np.arange(n), deg)
+    dst = rng.integers(0, n, len(src))
+    g = P.CsrGraph.from_edges(n, src, dst)
+    seeds = rng.integers(0, n, 400)
+    seeds[:20] = np.flatnonzero(deg >= 1000)[:20]  # hubs among the seeds
+    stream = P.KeyedRng(12).derive(0, 0, 2).derive(2, 9)
+    cfg = P.SamplingConfig(fanouts=fanouts, batch_size=len(seeds))
+    got = P.sample_batch(g, seeds, cfg, stream)
+    want = O.sample_batch(g.row_offsets, g.col_indices, n, seeds, fanouts, stream.key)
+    for hop, (s, off, nbr) in zip(got.hops, want):
+        assert np.array_equal(hop.sources, s)
+        assert np.array_equal(hop.offsets, off)
+        assert np.array_equal(hop.neighbors, nbr)
+    assert np.array_equal(got.distinct_vertices(), O.distinct_vertices(seeds, want))
