@@ -399,6 +399,9 @@ def run_b200(args):
         line["graphsage_epoch"] = train_run(args, g, cfg, pipe, pool, root, clique, local_idx, world)
     if not args.no_e2e:
         line["e2e"] = e2e_run(args, g, cfg, store, pool, root, clique, local_idx, world)
+        # the training-feed view: same API and H2D, results left in HBM for the trainer
+        line["e2e_device_consumer"] = e2e_run(args, g, cfg, store, pool, root, clique, local_idx, world,
+                                              results_to_host=False)
     if world > 1:
         line["config"]["dist_backend"] = dist.get_backend()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -444,10 +447,12 @@ def train_run(args, g, cfg, pipe, pool, root, clique, local_idx, world):
             "first_loss": float(losses[0]), "last_loss": float(losses[-1])}
 
 
-def e2e_run(args, g, cfg, store, pool, root, clique, local_idx, world):
+def e2e_run(args, g, cfg, store, pool, root, clique, local_idx, world, results_to_host: bool = True):
     """Same metric through the public pipeline API with host buffers: the tablet goes
     host->device from pinned memory each step, and every batch's result (distinct
-    ids, gathered rows, relabelled hop ids and offsets) comes back to pinned host."""
+    ids, gathered rows, relabelled hop ids and offsets) comes back to pinned host.
+    results_to_host=False: the results stay on the device for an on-device consumer
+    (the trainer) and only each window's per-batch sizes come back."""
     import torch
     import torch.distributed as dist
 
@@ -470,6 +475,9 @@ def e2e_run(args, g, cfg, store, pool, root, clique, local_idx, world):
     def drain(p, w0, nbw):
         counts = sp.counts[:, :nbw].cpu()  # sync point: sizes of this window
         ucnt = sp.ucount[:nbw].cpu()
+        moved["d2h"] += 4 * (counts.numel() + ucnt.numel())
+        if not results_to_host:
+            return
         for b in range(nbw):
             u = int(ucnt[b])
             pinned["feat"][b, :u].copy_(pipe.features[b, :u], non_blocking=True)
