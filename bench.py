@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--window", type=int, default=0,
                     help="batches per launch window (0 = whole epoch / lanes*2 windows when lanes > 1)")
     ap.add_argument("--lanes", type=int, default=1, help="concurrent window lanes (inter-batch pipeline streams)")
+    ap.add_argument("--graph", type=int, default=1, help="1: each timed epoch is one CUDA-graph launch")
     ap.add_argument("--visited", default="auto", choices=["auto", "dense", "sparse"],
                     help="visited-set layout for dedup (auto: sparse above 4M vertices)")
     ap.add_argument("--num-vertices", type=int, default=CONFIG["num_vertices"])
@@ -298,8 +299,9 @@ def run_b200(args):
         stats["sampled"] += b["sampled"]
         stats["max_unique"] = max(stats["max_unique"], int(p.sampler.ucount[:nbw].max().item()))
 
+    epoch_fn = pipe.run_epoch_graph if args.graph else pipe.run_epoch
     for e in range(args.warmup):
-        pipe.run_epoch(plans[e])
+        epoch_fn(plans[e])
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -314,7 +316,7 @@ def run_b200(args):
             flush.zero_()  # L2 flush outside the timed events
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            pipe.run_epoch(plans[args.warmup + s])
+            epoch_fn(plans[args.warmup + s])
             e1.record()
             torch.cuda.synchronize()
             step_ms.append(e0.elapsed_time(e1))
@@ -373,7 +375,7 @@ def run_b200(args):
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u64", "data": "synthetic (reference generator law, PCG64 draws; random fp32 features)",
         "config": {**CONFIG, "num_vertices": args.num_vertices, "batches_per_step_per_gpu": nb,
-                   "window_batches": pipe.window, "lanes": args.lanes, "parallelism": f"dp{world} (tablet per GPU, no data-path collective)",
+                   "window_batches": pipe.window, "lanes": args.lanes, "cuda_graph": bool(args.graph), "parallelism": f"dp{world} (tablet per GPU, no data-path collective)",
                    "l2": "flushed (256 MB write) between timed steps; graph+features 1.2 GB > L2"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,

@@ -78,6 +78,10 @@ int gc_hash_pairs(uint64_t key, const int64_t* d_a, const int64_t* d_b, uint64_t
 size_t gc_permutation_temp_bytes(int64_t n);
 int gc_permutation(uint64_t key, int64_t n, const int64_t* d_pool, int64_t* d_out, void* d_temp,
                    size_t temp_bytes, void* stream);
+/* Same, with the shuffle key read from device memory at run time, so a CUDA graph
+ * captured once replays every epoch's shuffle (SampleGatherPipeline.run_epoch_graph). */
+int gc_permutation_dkey(const uint64_t* d_key, int64_t n, const int64_t* d_pool, int64_t* d_out, void* d_temp,
+                        size_t temp_bytes, void* stream);
 
 /* ---------------------------------------------------------- topology (graph.py) */
 

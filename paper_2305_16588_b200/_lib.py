@@ -103,6 +103,7 @@ SIGNATURES = {
     "gc_hash_pairs": (ctypes.c_int, [U64, V, V, V, I64, V]),
     "gc_permutation_temp_bytes": (SZ, [I64]),
     "gc_permutation": (ctypes.c_int, [U64, I64, V, V, V, SZ, V]),
+    "gc_permutation_dkey": (ctypes.c_int, [V, I64, V, V, V, SZ, V]),
     "gc_hop_expand_temp_bytes": (SZ, [U32, U32]),
     "gc_hop_expand": (
         ctypes.c_int,

@@ -45,7 +45,11 @@ __global__ void k_hash_pairs(uint64_t key, const int64_t* __restrict__ a, const 
 // keys[i] = hash_counters(i), vals[i] = i : the inputs of the stable argsort (rng.py:82)
 // The permutation sorts the high 32 bits of each key (4 radix passes instead of 8);
 // k_perm_ties then orders every run of equal high words by the full 64-bit key.
-__global__ void k_perm_keys(uint64_t key, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, int64_t n) {
+// key_ptr (device) overrides `key` when set: a CUDA graph replays with the key read
+// from memory, so one captured epoch serves every epoch's shuffle
+__global__ void k_perm_keys(uint64_t key, const uint64_t* __restrict__ key_ptr, uint32_t* __restrict__ keys,
+                            uint32_t* __restrict__ vals, int64_t n) {
+    if (key_ptr) key = *key_ptr;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         keys[i] = (uint32_t)(hash_counter(key, (uint64_t)i) >> 32);
         vals[i] = (uint32_t)i;
@@ -55,7 +59,9 @@ __global__ void k_perm_keys(uint64_t key, uint32_t* __restrict__ keys, uint32_t*
 // A run of equal high words (n^2 / 2^33 pairs expected, almost all of length 2) is in
 // ascending index order after the stable sort; its first thread insertion-sorts it by
 // (full key, index) — the order of argsort(kind="stable") on the 64-bit keys.
-__global__ void k_perm_ties(uint64_t key, const uint32_t* __restrict__ hi, uint32_t* __restrict__ perm, int64_t n) {
+__global__ void k_perm_ties(uint64_t key, const uint64_t* __restrict__ key_ptr, const uint32_t* __restrict__ hi,
+                            uint32_t* __restrict__ perm, int64_t n) {
+    if (key_ptr) key = *key_ptr;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i + 1 < n; i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t h = hi[i];
         if (hi[i + 1] != h || (i > 0 && hi[i - 1] == h)) continue;  // not the start of a run
@@ -152,8 +158,8 @@ size_t gc_permutation_temp_bytes(int64_t n) {
     return perm_layout(n).total;
 }
 
-int gc_permutation(uint64_t key, int64_t n, const int64_t* d_pool, int64_t* d_out, void* d_temp,
-                   size_t temp_bytes, void* stream) {
+static int permutation_impl(uint64_t key, const uint64_t* d_key, int64_t n, const int64_t* d_pool, int64_t* d_out,
+                            void* d_temp, size_t temp_bytes, void* stream) {
     GC_REQUIRE(n >= 0 && n < (1ll << 31), GC_ERR_VALUE, "gc_permutation: n must be in [0, 2^31)");
     if (n == 0) return GC_OK;
     PermLayout L = perm_layout(n);
@@ -164,7 +170,7 @@ int gc_permutation(uint64_t key, int64_t n, const int64_t* d_pool, int64_t* d_ou
     auto* k1 = reinterpret_cast<uint32_t*>(t + L.keys1);
     auto* v0 = reinterpret_cast<uint32_t*>(t + L.vals0);
     auto* v1 = reinterpret_cast<uint32_t*>(t + L.vals1);
-    k_perm_keys<<<grid_for(n, 256), 256, 0, s>>>(key, k0, v0, n);
+    k_perm_keys<<<grid_for(n, 256), 256, 0, s>>>(key, d_key, k0, v0, n);
     GC_CHECK_LAUNCH("gc_permutation keys");
     // LSD radix sort is stable: equal keys keep ascending index, matching
     // np.argsort(kind="stable") (rng.py:82); ties of the high words are then ordered
@@ -173,11 +179,22 @@ int gc_permutation(uint64_t key, int64_t n, const int64_t* d_pool, int64_t* d_ou
     cub::DoubleBuffer<uint32_t> vb(v0, v1);
     size_t cub_bytes = L.cub_bytes;
     GC_TRY(cub::DeviceRadixSort::SortPairs(t + L.cub, cub_bytes, kb, vb, (int)n, 0, 32, s), "gc_permutation sort");
-    k_perm_ties<<<grid_for(n, 256), 256, 0, s>>>(key, kb.Current(), vb.Current(), n);
+    k_perm_ties<<<grid_for(n, 256), 256, 0, s>>>(key, d_key, kb.Current(), vb.Current(), n);
     GC_CHECK_LAUNCH("gc_permutation ties");
     k_perm_emit<<<grid_for(n, 256), 256, 0, s>>>(vb.Current(), d_pool, d_out, n);
     GC_CHECK_LAUNCH("gc_permutation emit");
     return GC_OK;
+}
+
+int gc_permutation(uint64_t key, int64_t n, const int64_t* d_pool, int64_t* d_out, void* d_temp,
+                   size_t temp_bytes, void* stream) {
+    return permutation_impl(key, nullptr, n, d_pool, d_out, d_temp, temp_bytes, stream);
+}
+
+int gc_permutation_dkey(const uint64_t* d_key, int64_t n, const int64_t* d_pool, int64_t* d_out, void* d_temp,
+                        size_t temp_bytes, void* stream) {
+    GC_REQUIRE(d_key, GC_ERR_VALUE, "gc_permutation_dkey: key pointer is null");
+    return permutation_impl(0, d_key, n, d_pool, d_out, d_temp, temp_bytes, stream);
 }
 
 int gc_host_register(void* host_ptr, size_t bytes, void** d_alias) {

@@ -28,6 +28,12 @@ from .sampling import DeviceHotness, SamplingConfig, WindowSampler, batch_hop_ke
 LAUNCHES_PERMUTATION = 3 + 6
 
 
+def _as_i64(key: int) -> int:
+    """uint64 bit pattern -> the int64 a torch tensor stores."""
+    key = int(key) & 0xFFFFFFFFFFFFFFFF
+    return key - (1 << 64) if key >= 1 << 63 else key
+
+
 @dataclass
 class EpochPlan:
     pool: torch.Tensor  # int64 [L] device
@@ -35,6 +41,7 @@ class EpochPlan:
     keys: torch.Tensor  # int64 [nb, H] device (uint64 bit patterns)
     counts: torch.Tensor  # int32 [nb] device
     num_batches: int
+    shuffle_key_dev: torch.Tensor | None = None  # int64 [1] device: the key read at run time (graphs)
 
 
 class StageTimer:
@@ -103,6 +110,7 @@ class SampleGatherPipeline:
         self.feat_cap = self.sampler.ucap
         self.timer: StageTimer | None = None
         self.launches = 0
+        self._graph = None  # run_epoch_graph: (CUDA graph, static plan, launches per replay)
 
     @property
     def lanes(self) -> int:
@@ -137,7 +145,8 @@ class SampleGatherPipeline:
         On return the caller's stream is ordered after every window."""
         B, H = self.cfg.batch_size, len(self.cfg.fanouts)
         end = self._stage("shuffle")
-        shuffled = KeyedRng(plan.shuffle_key).permutation_device(plan.pool.numel(), plan.pool)
+        shuffled = KeyedRng(plan.shuffle_key).permutation_device(plan.pool.numel(), plan.pool,
+                                                                 key_tensor=plan.shuffle_key_dev)
         self.launches += LAUNCHES_PERMUTATION
         if end is not None:
             end.record()
@@ -164,6 +173,36 @@ class SampleGatherPipeline:
             # `shuffled` and the plan's tensors were used on the lane streams
             for st in self.lane_streams:
                 shuffled.record_stream(st)
+
+    def run_epoch_graph(self, plan: EpochPlan) -> None:
+        """run_epoch as one CUDA-graph launch: the epoch's ~20 kernels (and the lanes'
+        and relabel stream's fork/join) are captured on the first call and replayed
+        after copying this epoch's inputs — pool, hop keys, batch sizes, shuffle key —
+        into the captured static buffers. Same results as run_epoch; no host work or
+        launch gaps between the kernels. The pool size must stay the same."""
+        shape = (plan.pool.numel(), plan.num_batches)
+        if self._graph is None or self._graph[1].pool.numel() != shape[0] \
+                or self._graph[1].num_batches != shape[1]:
+            static = EpochPlan(plan.pool.clone(), plan.shuffle_key, plan.keys.clone(), plan.counts.clone(),
+                               plan.num_batches, torch.zeros(1, dtype=torch.int64, device="cuda"))
+            static.shuffle_key_dev.fill_(_as_i64(plan.shuffle_key))
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):  # warm-up outside the capture (allocations, lazy init)
+                self.run_epoch(static)
+            torch.cuda.current_stream().wait_stream(side)
+            before = self.launches
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.run_epoch(static)
+            self._graph = (g, static, self.launches - before)
+        g, static, per_replay = self._graph
+        static.pool.copy_(plan.pool)
+        static.keys.copy_(plan.keys)
+        static.counts.copy_(plan.counts)
+        static.shuffle_key_dev.fill_(_as_i64(plan.shuffle_key))
+        g.replay()
+        self.launches += per_replay
 
     def _window(self, plan: EpochPlan, shuffled: torch.Tensor, w0: int, on_window, hot) -> None:
         sp = self.sampler

@@ -93,9 +93,12 @@ class KeyedRng:
     def uniform(self, counters) -> np.ndarray:
         return (self.hash_counters(counters) >> np.uint64(11)) * (2.0**-53)
 
-    def permutation_device(self, n: int, pool: torch.Tensor | None = None) -> torch.Tensor:
+    def permutation_device(self, n: int, pool: torch.Tensor | None = None,
+                           key_tensor: torch.Tensor | None = None) -> torch.Tensor:
         """K1: stable argsort of hash_counters(0..n-1) on the device, optionally fused
-        with the gather pool[perm] (run_sampling_epoch, sampling.py:231). int64 out."""
+        with the gather pool[perm] (run_sampling_epoch, sampling.py:231). int64 out.
+        key_tensor: a one-element int64 CUDA tensor holding the key (its bit pattern),
+        read at run time instead of self.key — what a captured CUDA graph needs."""
         lib = _lib.lib()
         out = torch.empty(n, dtype=torch.int64, device="cuda")
         if n == 0:
@@ -106,12 +109,16 @@ class KeyedRng:
             pool = pool.contiguous()
         tmp_bytes = lib.gc_permutation_temp_bytes(n)
         tmp = torch.empty(tmp_bytes, dtype=torch.uint8, device="cuda")
-        _lib.check(
-            lib.gc_permutation(
-                self.key, n, _lib.ptr(pool), out.data_ptr(), tmp.data_ptr(), tmp_bytes, _lib.stream_handle()
-            ),
-            "permutation",
-        )
+        if key_tensor is not None:
+            _lib.check(lib.gc_permutation_dkey(key_tensor.data_ptr(), n, _lib.ptr(pool), out.data_ptr(),
+                                               tmp.data_ptr(), tmp_bytes, _lib.stream_handle()), "permutation")
+        else:
+            _lib.check(
+                lib.gc_permutation(
+                    self.key, n, _lib.ptr(pool), out.data_ptr(), tmp.data_ptr(), tmp_bytes, _lib.stream_handle()
+                ),
+                "permutation",
+            )
         return out
 
     def permutation(self, n: int) -> np.ndarray:

@@ -245,3 +245,42 @@ def test_lanes_overlap_matches_sequential(lanes):
             for h in range(len(fanouts)):
                 t = int(a[5][h + 1, bi])
                 assert torch.equal(a[4][h][bi, :t], b[4][h][bi, :t])
+
+
+@pytest.mark.parametrize("lanes", [1, 2])
+def test_epoch_graph_replay_matches_eager(lanes):
+    """run_epoch_graph (one CUDA-graph launch per epoch, inputs copied into the captured
+    buffers) gives run_epoch's results for several epochs with different shuffle and
+    hop keys."""
+    import paper_2305_16588_b200 as P
+    from paper_2305_16588_b200.cache import FeatureStore
+    from paper_2305_16588_b200.graph import synthetic_features_device
+    from paper_2305_16588_b200.pipeline import SampleGatherPipeline
+
+    n, dim, batch, fanouts = 30_000, 32, 128, (8, 4)
+    g = P.generate_synthetic(n, 12, 1.2, seed=6)
+    pool = np.sort(np.random.default_rng(5).choice(n, 2000, replace=False)).astype(np.int64)
+    cfg = P.SamplingConfig(fanouts=fanouts, batch_size=batch)
+    store = FeatureStore.resident(synthetic_features_device(0, n, dim))
+    eager = SampleGatherPipeline(g, cfg, store, len(pool), window=8 if lanes > 1 else None, lanes=lanes)
+    graph = SampleGatherPipeline(g, cfg, store, len(pool), window=8 if lanes > 1 else None, lanes=lanes)
+    root = P.KeyedRng(77)
+
+    def snapshot(p):
+        out = []
+        for sp, feats in zip(p.lane_samplers, p.lane_features):
+            out.append([t.clone() for t in (sp.counts, sp.ucount, sp.unique, feats, *sp.local_nbrs)])
+        return out
+
+    for e in range(3):
+        gs = root.derive(e, 0, 0)
+        eager.run_epoch(eager.plan_epoch(pool, gs))
+        graph.run_epoch_graph(graph.plan_epoch(pool, gs))
+        torch.cuda.synchronize()
+        a, b = snapshot(eager), snapshot(graph)
+        for la, lb in zip(a, b):
+            cnt = la[1].cpu().numpy()
+            assert torch.equal(la[0], lb[0]) and torch.equal(la[1], lb[1])
+            for bi, u in enumerate(cnt):
+                assert torch.equal(la[2][bi, :u], lb[2][bi, :u])
+                assert torch.equal(la[3][bi, :u], lb[3][bi, :u])
