@@ -45,6 +45,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--window", type=int, default=256)
     ap.add_argument("--lanes", type=int, default=2, help="concurrent window lanes (inter-batch pipeline)")
+    ap.add_argument("--graph", type=int, default=1, help="1: each timed epoch is one CUDA-graph launch")
     ap.add_argument("--sweep-lanes", default="", help="extra schedules to time after the main run, e.g. 1,3,2d,2w64 (d: host rows deferred, wN: window)")
     ap.add_argument("--alpha-sweep", type=int, default=0,
                     help="validate the cost model: time one epoch at this many alpha points (+ both objectives' picks)")
@@ -106,7 +107,7 @@ def main():
     plans = [pipe.plan_epoch(pool, root.derive(e, 0, 0)) for e in range(a.warmup + a.steps)]
     setup_s = time.perf_counter() - t_setup
     for e in range(a.warmup):
-        pipe.run_epoch(plans[e])
+        (pipe.run_epoch_graph if a.graph else pipe.run_epoch)(plans[e])
     torch.cuda.synchronize()
     topo.reset_counters()
     fstore.reset_counters()
@@ -114,7 +115,7 @@ def main():
     for s in range(a.steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        pipe.run_epoch(plans[a.warmup + s])
+        (pipe.run_epoch_graph if a.graph else pipe.run_epoch)(plans[a.warmup + s])
         e1.record()
         torch.cuda.synchronize()
         ms.append(e0.elapsed_time(e1))
@@ -136,11 +137,11 @@ def main():
         torch.cuda.empty_cache()
         pipe = SampleGatherPipeline(g, cfg, fstore, len(pool), window=min(wsize, nb), feat_rows_cap=60_000,
                                     topology=topo, lanes=lanes, defer_host=defer)
-        pipe.run_epoch(plans[0])
+        (pipe.run_epoch_graph if a.graph else pipe.run_epoch)(plans[0])
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for s in range(a.steps):
-            pipe.run_epoch(plans[a.warmup + s])
+            (pipe.run_epoch_graph if a.graph else pipe.run_epoch)(plans[a.warmup + s])
         e1.record()
         torch.cuda.synchronize()
         sweep[tag] = nb * a.steps / (e0.elapsed_time(e1) / 1000.0)
@@ -211,6 +212,7 @@ def main():
             "measured_us_per_batch": t_meas * 1e6, "frac": t_roof / t_meas,
         },
         "lanes": a.lanes,
+        "cuda_graph": bool(a.graph),
         "lane_sweep_batches_per_s": sweep,
         "tiers_per_batch": {**{k: v / batches for k, v in t.items()}, **{f"rows_{k}": v / batches for k, v in f.items()}},
         "stages_ms_per_epoch": stages,
