@@ -118,7 +118,12 @@ __global__ void __launch_bounds__(kUniqThreads) k_unique(UniqueParams p) {
 // persistent CTAs every chunk's look-back walks back through the whole wave; a
 // chunk-granular two-pass version at 16 ms.)
 constexpr int kBlockWarps = kUniqThreads / 32;
-constexpr int kBlocksInFlight = 4;  // listed blocks per warp per step (independent load chains)
+#ifndef GC_BLOCKS_IN_FLIGHT
+#define GC_BLOCKS_IN_FLIGHT 4
+#endif
+// listed blocks per warp per step (independent load chains): C3's touched blocks hold
+// ~1 id each, so the passes are latency-bound and want many chains per warp
+constexpr int kBlocksInFlight = GC_BLOCKS_IN_FLIGHT;
 
 __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, uint32_t& total) {
     const int lane = threadIdx.x & 31;
@@ -237,17 +242,17 @@ __global__ void __launch_bounds__(kUniqThreads) k_block_emit(SparseParams p) {
     const uint32_t warps = gridDim.x * kBlockWarps;
     for (uint32_t i0 = (blockIdx.x * kBlockWarps + (threadIdx.x >> 5)) * kBlocksInFlight; i0 < nb;
          i0 += warps * kBlocksInFlight) {
-        uint32_t x[kBlocksInFlight], base[kBlocksInFlight];
-        uint64_t wi[kBlocksInFlight];
+        uint32_t x[kBlocksInFlight], base[kBlocksInFlight], blk[kBlocksInFlight];
 #pragma unroll
         for (int k = 0; k < kBlocksInFlight; ++k) {
             x[k] = 0u;
-            wi[k] = 0;
+            blk[k] = 0;
             base[k] = 0;
             if (i0 + k < nb) {
-                wi[k] = (uint64_t)list[i0 + k] * 32 + lane;
+                blk[k] = list[i0 + k];
                 base[k] = pre[i0 + k];
-                if (wi[k] < p.bwords) x[k] = row[wi[k]];
+                const uint64_t w = (uint64_t)blk[k] * 32 + lane;
+                if (w < p.bwords) x[k] = row[w];
             }
         }
 #pragma unroll
@@ -255,14 +260,15 @@ __global__ void __launch_bounds__(kUniqThreads) k_block_emit(SparseParams p) {
             uint32_t tot;
             uint32_t pos = base[k] + warp_excl_scan((uint32_t)__popc(x[k]), tot);
             if (x[k]) {
-                if (rt) rt[wi[k]] = make_uint2(pos, x[k]);
-                const uint32_t vbase = (uint32_t)(wi[k] * 32);
+                const uint64_t wik = (uint64_t)blk[k] * 32 + lane;
+                if (rt) rt[wik] = make_uint2(pos, x[k]);
+                const uint32_t vbase = (uint32_t)(wik * 32);
                 for (uint32_t w = x[k]; w; w &= w - 1u) {
                     const uint32_t u = vbase + (__ffs(w) - 1);
                     out[pos++] = u;
                     if (p.feat) atomicAdd((unsigned long long*)(p.feat + u), 1ull);
                 }
-                if (p.clear) row[wi[k]] = 0u;
+                if (p.clear) row[wik] = 0u;
             }
         }
     }
