@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(kUniqThreads) k_unique(UniqueParams p) {
 // chunk-granular two-pass version at 16 ms.)
 constexpr int kBlockWarps = kUniqThreads / 32;
 #ifndef GC_BLOCKS_IN_FLIGHT
-#define GC_BLOCKS_IN_FLIGHT 4
+#define GC_BLOCKS_IN_FLIGHT 8  // C3 dedup+relabel 15.1 -> 13.6 ms per epoch (16: 14.7)
 #endif
 // listed blocks per warp per step (independent load chains): C3's touched blocks hold
 // ~1 id each, so the passes are latency-bound and want many chains per warp
