@@ -34,10 +34,11 @@ constexpr int kItemCap = 16 * kHopThreads;  // staged output items per round (u6
 // emission items in flight per thread: a full tile of 256 positions with take =
 // fanout stages exactly `fanout` items per thread, so for the small networks S - 1
 // (the largest fanout of the network) covers it in one pass (C2 hop 3: 1.68 -> 1.60
-// ms); wider fanouts keep 4 (measured faster than 8-12 for S = 11 and 16)
+// ms); S = 11 (fanouts 8-10) takes two passes of 5 (C2 hop 2: 0.246 -> 0.235 ms);
+// wider fanouts keep 4 (measured faster than 8-12 for S = 16)
 template <int S>
 __host__ __device__ constexpr int emit_items() {
-    return S > 1 && S <= 8 ? S - 1 : 4;
+    return S > 1 && S <= 8 ? S - 1 : (S == 11 ? 5 : 4);
 }
 // resident CTAs per SM the register budget targets: 6 (40 registers, no spills) for
 // S <= 8, 5 up to S = 16 (C3 hop 2, S = 11: 15.0 ms at 5 vs 16.1 at 6), 4 (64 registers) above and for the
