@@ -300,3 +300,32 @@ def test_heavy_tailed_out_degrees_match_oracle(fanouts):
         assert np.array_equal(hop.offsets, off)
         assert np.array_equal(hop.neighbors, nbr)
     assert np.array_equal(got.distinct_vertices(), O.distinct_vertices(seeds, want))
+
+
+_RAND_CASES = [
+    (int(n), int(d), tuple(int(f) for f in fs), int(s))
+    for n, d, fs, s in [
+        (np.random.default_rng(i).integers(500, 30_000), np.random.default_rng(i + 100).integers(1, 70),
+         np.random.default_rng(i + 200).integers(1, 40, np.random.default_rng(i + 300).integers(1, 4)),
+         np.random.default_rng(i + 400).integers(1, 2**62))
+        for i in range(8)
+    ]
+]
+
+
+@pytest.mark.parametrize("n,deg,fanouts,seed", _RAND_CASES)
+def test_randomized_shapes_match_oracle(n, deg, fanouts, seed):
+    """Seeded random (graph size, degree, 1-3 hop fanouts, stream key) — every network
+    size S, copy and choice paths mixed within a hop."""
+    P = _pkg()
+    g = P.generate_synthetic(n, deg, 1.1, seed=seed % 1000)
+    seeds = np.random.default_rng(seed % 997).integers(0, n, 200)
+    stream = P.KeyedRng(seed).derive(1, 0, 3).derive(2, 7)
+    cfg = P.SamplingConfig(fanouts=fanouts, batch_size=len(seeds))
+    got = P.sample_batch(g, seeds, cfg, stream)
+    want = O.sample_batch(g.row_offsets, g.col_indices, n, seeds, fanouts, stream.key)
+    for hop, (s, off, nbr) in zip(got.hops, want):
+        assert np.array_equal(hop.sources, s)
+        assert np.array_equal(hop.offsets, off)
+        assert np.array_equal(hop.neighbors, nbr)
+    assert np.array_equal(got.distinct_vertices(), O.distinct_vertices(seeds, want))
