@@ -45,6 +45,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--window", type=int, default=256)
     ap.add_argument("--lanes", type=int, default=2, help="concurrent window lanes (inter-batch pipeline)")
+    ap.add_argument("--presample-epochs", type=int, default=4,
+                    help="presampling epochs behind the plan (more: less optimistic estimate, better cache)")
     ap.add_argument("--graph", type=int, default=1, help="1: each timed epoch is one CUDA-graph launch")
     ap.add_argument("--sweep-lanes", default="", help="extra schedules to time after the main run, e.g. 1,3,2d,2w64 (d: host rows deferred, wN: window)")
     ap.add_argument("--alpha-sweep", type=int, default=0,
@@ -75,7 +77,8 @@ def main():
     total_bytes = g.num_edges * 4 + 8 * n + n * feat.row_bytes
     budget = int(a.budget_frac * total_bytes) * K
     spec = P.HardwareSpec(layout, clique_budget_bytes=budget)
-    cfg = P.SamplingConfig(fanouts=fanouts, batch_size=bs, presample_epochs=1, seed=P.derive_seed(7, 4))
+    cfg = P.SamplingConfig(fanouts=fanouts, batch_size=bs, presample_epochs=a.presample_epochs,
+                           seed=P.derive_seed(7, 4))
 
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -168,7 +171,8 @@ def main():
         seq.run_epoch(plans[a.warmup + s], on_window=account)
     torch.cuda.synchronize()
     batches = nb * a.steps
-    clique_batches = sum(math.ceil(len(pl) / bs) for pl in pools)  # the presampling epoch's batches
+    # the presampling epochs' batches: the plan's N_total counts all of them
+    clique_batches = a.presample_epochs * sum(math.ceil(len(pl) / bs) for pl in pools)
     row_txns = PL.feature_row_transactions(feat, spec)
     cls = spec.cache_line_bytes
     measured_txn = t["host_txn"] + f["host"] * row_txns
@@ -194,7 +198,7 @@ def main():
                    "num_edges": g.num_edges, "feature_dim": dim, "fanouts": list(fanouts), "batch_size": bs,
                    "budget_bytes": budget, "budget_frac_per_gpu": a.budget_frac, "batches_per_epoch": nb,
                    "clique": K, "peers": "emulated in local HBM" if K > 1 else None},
-        "plan": {"alpha": plan.alpha, "topo_prefix_len": est.topo_prefix_len, "feat_prefix_len": est.feat_prefix_len,
+        "plan": {"presample_epochs": a.presample_epochs, "alpha": plan.alpha, "topo_prefix_len": est.topo_prefix_len, "feat_prefix_len": est.feat_prefix_len,
                  "predicted_txn_per_epoch": pred_txn, "presample_txn_total": hot.sampling_txn_total},
         "pcie": {
             "measured_gb_per_batch": measured_txn * cls / batches / 1e9,
