@@ -239,6 +239,11 @@ int gc_synth_features(uint64_t first_row, uint64_t rows, uint32_t dim, float* d_
 /* ---------------------------------------------- K5: hotness scatter (sampling.py:164-174) */
 
 /* accumulate_hotness's bincount: d_counter[d_ids[k]] += (d_weights ? d_weights[k] : 1). */
+/* Trainer helper (not in the reference): out[i] = mean of x[idx[k]] over
+ * k in [offsets[i], offsets[i+1]) (0 for an empty segment), fp32, x row-major [*, dim].
+ * The first GraphSAGE layer's neighbour mean taken straight from the gathered rows. */
+int gc_segment_mean_gather(const float* d_x, int dim, const int64_t* d_idx, const int64_t* d_offsets, int64_t segs,
+                           float* d_out, void* stream);
 int gc_scatter_add(const uint32_t* d_ids, const uint32_t* d_weights, int64_t count, uint64_t* d_counter,
                    void* stream);
 

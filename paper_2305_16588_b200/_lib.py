@@ -121,6 +121,7 @@ SIGNATURES = {
     "gc_bitmap_clear": (ctypes.c_int, [ctypes.POINTER(GcVisited), U32, V, U64, V, U32, V]),
     "gc_gather": (ctypes.c_int, [ctypes.POINTER(GcFeatureStore), V, U64, V, U32, U32, V, U64, V, V]),
     "gc_scatter_add": (ctypes.c_int, [V, V, I64, V, V]),
+    "gc_segment_mean_gather": (ctypes.c_int, [V, ctypes.c_int, V, V, I64, V, V]),
     "gc_colsum_argmax": (ctypes.c_int, [V, U32, I64, V, V, V]),
     "gc_descending_order_temp_bytes": (SZ, [I64]),
     "gc_descending_order": (ctypes.c_int, [V, I64, V, V, SZ, V]),

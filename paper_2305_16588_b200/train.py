@@ -56,14 +56,34 @@ def segment_mean(x: torch.Tensor, offsets: torch.Tensor) -> torch.Tensor:
     return torch.segment_reduce(x, "mean", lengths=lengths, unsafe=True, initial=0.0)
 
 
+def segment_mean_gather(x: torch.Tensor, idx: torch.Tensor, offsets: torch.Tensor) -> torch.Tensor:
+    """segment_mean(x[idx], offsets) without materialising x[idx]: on the device one
+    kernel (gc_segment_mean_gather) reads the rows straight from x. No gradient flows
+    to x (the gathered feature rows are inputs)."""
+    segs = offsets.shape[0] - 1
+    if not x.is_cuda:
+        return segment_mean(x[idx], offsets)
+    from . import _lib
+
+    x = x.detach().contiguous()
+    idx = idx.to(torch.int64).contiguous()
+    offsets = offsets.to(torch.int64).contiguous()
+    out = torch.empty((segs, x.shape[1]), dtype=torch.float32, device=x.device)
+    _lib.check(_lib.lib().gc_segment_mean_gather(x.data_ptr(), x.shape[1], idx.data_ptr(), offsets.data_ptr(), segs,
+                                                 out.data_ptr(), _lib.stream_handle()), "segment_mean_gather")
+    return out
+
+
 class SAGELayer(nn.Module):
     def __init__(self, d_in: int, d_out: int):
         super().__init__()
         self.lin_self = nn.Linear(d_in, d_out)
         self.lin_neigh = nn.Linear(d_in, d_out, bias=False)
 
-    def forward(self, h_self, h_children, offsets):
-        return self.lin_self(h_self) + self.lin_neigh(segment_mean(h_children, offsets))
+    def forward(self, h_self, h_children, offsets, x=None, idx=None):
+        """h_children = None with (x, idx): the children are rows x[idx] (first layer)."""
+        agg = segment_mean(h_children, offsets) if h_children is not None else segment_mean_gather(x, idx, offsets)
+        return self.lin_self(h_self) + self.lin_neigh(agg)
 
 
 class GCNLayer(nn.Module):
@@ -74,9 +94,10 @@ class GCNLayer(nn.Module):
         super().__init__()
         self.lin = nn.Linear(d_in, d_out)
 
-    def forward(self, h_self, h_children, offsets):
+    def forward(self, h_self, h_children, offsets, x=None, idx=None):
         deg = (offsets[1:] - offsets[:-1]).to(h_self.dtype).unsqueeze(1)
-        agg = segment_mean(h_children, offsets) * deg  # segment sum (0 for empty segments)
+        mean = segment_mean(h_children, offsets) if h_children is not None else segment_mean_gather(x, idx, offsets)
+        agg = mean * deg  # segment sum (0 for empty segments)
         return self.lin((h_self + agg) / (deg + 1.0))
 
 
@@ -93,8 +114,13 @@ class GraphSAGE(nn.Module):
 
     def forward(self, batch: TreeBatch) -> torch.Tensor:
         L = len(self.layers)
-        h = [batch.features[idx] for idx in batch.local[: L + 1]]
-        for li, layer in enumerate(self.layers):
+        x = batch.features
+        # first layer: the children's mean is taken straight from the gathered rows
+        # (the leaf level, 5x the positions of the level above, is never materialised)
+        h = [F.relu(self.layers[0](x[batch.local[lvl]], None, batch.offsets[lvl], x=x, idx=batch.local[lvl + 1]))
+             for lvl in range(L)]
+        for li in range(1, L):
+            layer = self.layers[li]
             h = [F.relu(layer(h[lvl], h[lvl + 1], batch.offsets[lvl])) for lvl in range(L - li)]
         return self.classifier(h[0])
 

@@ -61,3 +61,20 @@ def test_graphsage_loss_parity_fp32(layer):
     rel = np.abs(np.array(losses_g) - np.array(losses_c)) / np.abs(np.array(losses_c))
     assert rel.max() < 1e-3, (losses_g, losses_c)
     assert losses_g[-1] < losses_g[0] * 1.5  # training runs (SGD on random labels need not drop fast)
+
+
+@pytest.mark.parametrize("dim", [100, 7])
+def test_segment_mean_gather_matches_torch(dim):
+    """The fused first-layer aggregation == segment_mean(x[idx]) (fp32, ragged segments
+    including empty ones; float4 and scalar paths)."""
+    from paper_2305_16588_b200.train import segment_mean, segment_mean_gather
+
+    rng = np.random.default_rng(dim)
+    U, P = 3000, 5000
+    deg = rng.integers(0, 9, P)
+    off = torch.from_numpy(np.concatenate([[0], np.cumsum(deg)])).cuda()
+    idx = torch.from_numpy(rng.integers(0, U, int(deg.sum()))).cuda()
+    x = torch.randn(U, dim, device="cuda")
+    got = segment_mean_gather(x, idx, off)
+    want = segment_mean(x[idx], off)
+    assert torch.allclose(got, want, rtol=1e-6, atol=1e-6)
