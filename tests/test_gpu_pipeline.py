@@ -284,3 +284,55 @@ def test_epoch_graph_replay_matches_eager(lanes):
             for bi, u in enumerate(cnt):
                 assert torch.equal(la[2][bi, :u], lb[2][bi, :u])
                 assert torch.equal(la[3][bi, :u], lb[3][bi, :u])
+
+
+@pytest.mark.parametrize("lanes", [1, 2])
+def test_epoch_graph_replay_tiered_matches_eager(lanes):
+    """Graph replay through the tiered path (neighbour lists from local slab / peer
+    slabs / host CSR, features from HBM / peers / pinned host rows over UVA): same
+    results and same per-tier counters as eager run_epoch, epoch after epoch."""
+    import paper_2305_16588_b200 as P
+    from paper_2305_16588_b200.cache import FeatureStore, TopologyStore
+    from paper_2305_16588_b200.graph import synthetic_features_device
+    from paper_2305_16588_b200.pipeline import SampleGatherPipeline
+
+    n, dim, batch, fanouts = 40_000, 32, 128, (10, 5)
+    g = P.generate_synthetic(n, 14, 1.2, seed=8)
+    rng = np.random.default_rng(9)
+    pool = np.sort(rng.choice(n, 2000, replace=False)).astype(np.int64)
+    perm = rng.permutation(n)
+    topo_parts = [np.sort(perm[i * 6000 : (i + 1) * 6000]) for i in range(4)]
+    feat_parts = [np.sort(perm[24_000 + i * 3000 : 24_000 + (i + 1) * 3000]) for i in range(4)]
+    host_table = synthetic_features_device(0, n, dim).cpu()
+    cfg = P.SamplingConfig(fanouts=fanouts, batch_size=batch)
+
+    def make():
+        topo = TopologyStore(g, topo_parts, self_rank=1, host_full=True)
+        fs = FeatureStore.from_assignment(host_table, feat_parts, 1)
+        pipe = SampleGatherPipeline(g, cfg, fs, len(pool), window=8 if lanes > 1 else None, topology=topo,
+                                    lanes=lanes)
+        return pipe, topo, fs
+
+    (eager, te, fe), (graph, tg, fg) = make(), make()
+    root = P.KeyedRng(31)
+    for e in range(3):
+        for s in (te, fe, tg, fg):
+            s.reset_counters()
+        gs = root.derive(e, 0, 0)
+        eager.run_epoch(eager.plan_epoch(pool, gs))
+        graph.run_epoch_graph(graph.plan_epoch(pool, gs))
+        torch.cuda.synchronize()
+        # replayed kernels keep counting; the first call also ran one uncaptured warm-up epoch
+        mult = 2 if e == 0 else 1
+        ct, cg = te.tier_counts(), tg.tier_counts()
+        assert all(cg[k] == mult * ct[k] for k in ct), (e, ct, cg)
+        assert all(fg.tier_counts()[k] == mult * fe.tier_counts()[k] for k in ("local", "peer", "host"))
+        assert min(fe.tier_counts()[k] for k in ("local", "peer", "host")) > 0
+        assert min(ct[f"reads_{k}"] for k in ("local", "peer", "host")) > 0
+        for pa, pb in zip(zip(eager.lane_samplers, eager.lane_features), zip(graph.lane_samplers, graph.lane_features)):
+            (sa, xa), (sb, xb) = pa, pb
+            assert torch.equal(sa.counts, sb.counts) and torch.equal(sa.ucount, sb.ucount)
+            for bi, u in enumerate(sa.ucount.cpu().numpy()):
+                assert torch.equal(sa.unique[bi, :u], sb.unique[bi, :u])
+                assert torch.equal(xa[bi, :u], xb[bi, :u])
+                assert torch.equal(xa[bi, :u].cpu(), host_table[sa.unique[bi, :u].cpu().long() & 0xFFFFFFFF])
