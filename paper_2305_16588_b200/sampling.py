@@ -448,7 +448,10 @@ class EpochRunner:
     def run(self, pool: np.ndarray, gpu_stream: KeyedRng, hot: DeviceHotness) -> int:
         B = self.cfg.batch_size
         L = len(pool)
-        pool_dev = torch.from_numpy(np.ascontiguousarray(pool, dtype=np.int64)).cuda()
+        pool_np = np.ascontiguousarray(pool, dtype=np.int64)
+        if not pool_np.flags.writeable:  # read-only pools (reference dataclasses) — torch needs a writable view
+            pool_np = pool_np.copy()
+        pool_dev = torch.from_numpy(pool_np).cuda()
         shuffled = gpu_stream.derive(ROLE_SHUFFLE).permutation_device(L, pool_dev).to(torch.int32)
         nb = math.ceil(L / B)
         H = len(self.cfg.fanouts)
