@@ -466,31 +466,20 @@ def e2e_run(args, g, cfg, store, pool, root, clique, local_idx, world, results_t
     host_pool = torch.from_numpy(np.asarray(pool, dtype=np.int64)).pin_memory()
     sp = pipe.sampler
     H = len(cfg.fanouts)
-    pinned = {
-        "feat": torch.empty(pipe.features.shape, dtype=torch.float32).pin_memory(),
-        "uniq": torch.empty(sp.unique.shape, dtype=torch.int32).pin_memory(),
-        "local": [torch.empty(t.shape, dtype=torch.int32).pin_memory() for t in sp.local_nbrs],
-        "offs": [torch.empty(t.shape, dtype=torch.int32).pin_memory() for t in sp.offsets],
-    }
+    staging = {}  # pinned host buffers reused across windows
     moved = {"h2d": 0, "d2h": 0}
 
     def drain(p, w0, nbw):
-        counts = sp.counts[:, :nbw].cpu()  # sync point: sizes of this window
-        ucnt = sp.ucount[:nbw].cpu()
-        moved["d2h"] += 4 * (counts.numel() + ucnt.numel())
         if not results_to_host:
+            counts = sp.counts[:, :nbw].cpu()  # sync point: sizes of this window
+            ucnt = sp.ucount[:nbw].cpu()
+            moved["d2h"] += 4 * (counts.numel() + ucnt.numel())
             return
-        for b in range(nbw):
-            u = int(ucnt[b])
-            pinned["feat"][b, :u].copy_(pipe.features[b, :u], non_blocking=True)
-            pinned["uniq"][b, :u].copy_(sp.unique[b, :u], non_blocking=True)
-            moved["d2h"] += u * (store.spec.row_bytes + 4)
-            for h in range(H):
-                f, t = int(counts[h, b]), int(counts[h + 1, b])
-                pinned["offs"][h][b, : f + 1].copy_(sp.offsets[h][b, : f + 1], non_blocking=True)
-                pinned["local"][h][b, :t].copy_(sp.local_nbrs[h][b, :t], non_blocking=True)
-                moved["d2h"] += 4 * (f + 1 + t)
-        torch.cuda.current_stream().synchronize()
+        # sizes (one sync), then one packed D2H copy per array into pinned memory
+        moved["d2h"] += 4 * (H + 2) * nbw
+        out = p.window_to_host(nbw, staging)
+        moved["d2h"] += sum(t.numel() * t.element_size() for t in (out["unique"], out["features"],
+                                                                     *out["offsets"], *out["local"]))
 
     def step(e):
         dev_pool = host_pool.to("cuda", non_blocking=True)
@@ -518,9 +507,26 @@ def e2e_run(args, g, cfg, store, pool, root, clique, local_idx, world, results_t
         from paper_2305_16588_b200.distributed import max_over_ranks
 
         el = max_over_ranks(el)
-    return {"value": nb * world * steps / el, "unit": UNIT, "h2d_bytes_per_step": moved["h2d"] // steps,
-            "d2h_bytes_per_step": moved["d2h"] // steps, "steps": steps,
-            "api": "SampleGatherPipeline.plan_epoch/run_epoch (ctypes -> libgnncache_b200.so)"}
+    out = {"value": nb * world * steps / el, "unit": UNIT, "h2d_bytes_per_step": moved["h2d"] // steps,
+           "d2h_bytes_per_step": moved["d2h"] // steps, "steps": steps,
+           "api": "SampleGatherPipeline.plan_epoch/run_epoch + window_to_host (ctypes -> libgnncache_b200.so)"}
+    if results_to_host:
+        # the link the host-buffer arm is bound by: one large device -> pinned copy
+        src = torch.empty(1 << 28, dtype=torch.float32, device="cuda")
+        dst = staging["features"].view(-1)[: 1 << 28] if staging["features"].numel() >= 1 << 28 else \
+            torch.empty(1 << 28, dtype=torch.float32).pin_memory()
+        dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record()
+        for _ in range(3):
+            dst.copy_(src, non_blocking=True)
+        c1.record()
+        torch.cuda.synchronize()
+        link = 3 * src.numel() * 4 / (c0.elapsed_time(c1) / 1000.0) / 1e9
+        out["d2h_link_gbs"] = link
+        out["d2h_floor_per_s"] = nb * world / (out["d2h_bytes_per_step"] / (link * 1e9))
+    return out
 
 
 def main():

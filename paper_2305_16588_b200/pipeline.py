@@ -240,6 +240,72 @@ class SampleGatherPipeline:
         if on_window is not None:
             on_window(self, w0, nb)
 
+    # ------------------------------------------------------------------ host delivery
+    def window_to_host(self, nb: int, staging: dict | None = None) -> dict:
+        """The last window's results in pinned host memory, packed batch after batch.
+
+        The device buffers are padded [batch, capacity]; each array's per-batch
+        segments are first packed on the device (a masked gather, HBM-speed), so the
+        PCIe link carries one large copy per array instead of 2 + 2H small copies per
+        batch. Returns host tensors (views into `staging`, valid until the next call):
+        'unique' int32 [sum U], 'features' f32 [sum U, D], 'offsets'[h] int32
+        [sum (F_h + 1)], 'local'[h] int32 [sum T_h], and the batch boundaries
+        'unique_ptr', 'offsets_ptr'[h], 'local_ptr'[h] (int64 numpy [nb + 1]).
+        The packing is sync-free (segment rows from the host-side sizes) and each
+        array's D2H copy runs on a copy stream while the next array is packed. Reads
+        the sizes once (a sync) and returns after the copies have landed."""
+        sp = self.sampler
+        counts = sp.counts[:, :nb].cpu().numpy().astype(np.int64)
+        ucount = sp.ucount[:nb].cpu().numpy().astype(np.int64)
+        st = {} if staging is None else staging
+        main = torch.cuda.current_stream()
+        copy = st.get("_copy_stream")
+        if copy is None:
+            copy = st["_copy_stream"] = torch.cuda.Stream()
+        keep = []  # packed device arrays, alive until the copies finish
+
+        def ptr(sizes):
+            return np.concatenate(([0], np.cumsum(sizes))).astype(np.int64)
+
+        def pack(name, buf, sizes):
+            # sync-free segment pack: flat row of packed element k = b * cap + (k - ptr[b])
+            total = int(sizes.sum())
+            cap = buf.shape[1]
+            if total:
+                sz = torch.from_numpy(sizes).to(buf.device, non_blocking=True)
+                shift = torch.from_numpy(np.arange(nb, dtype=np.int64) * cap - ptr(sizes)[:-1]).to(
+                    buf.device, non_blocking=True)
+                rows = torch.arange(total, device=buf.device) + torch.repeat_interleave(shift, sz, output_size=total)
+                packed = buf[:nb].reshape((nb * cap,) + tuple(buf.shape[2:])).index_select(0, rows)
+            else:
+                packed = buf.new_empty((0,) + tuple(buf.shape[2:]))
+            host = st.get(name)
+            if host is None or host.shape[0] < total or host.shape[1:] != packed.shape[1:] or host.dtype != packed.dtype:
+                host = torch.empty((max(total, 1),) + tuple(packed.shape[1:]), dtype=packed.dtype).pin_memory()
+                st[name] = host
+            # the copy stream moves this array over PCIe while the next one is packed
+            ev = torch.cuda.Event()
+            ev.record(main)
+            copy.wait_event(ev)
+            with torch.cuda.stream(copy):
+                host[:total].copy_(packed, non_blocking=True)
+            keep.append(packed)
+            return host[:total]
+
+        out = {"unique_ptr": ptr(ucount), "offsets_ptr": [], "local_ptr": [], "offsets": [], "local": []}
+        out["unique"] = pack("unique", sp.unique, ucount)
+        if self.store is not None:
+            out["features"] = pack("features", self.features, ucount)
+        for h in range(sp.H):
+            f, t = counts[h] + 1, counts[h + 1]
+            out["offsets_ptr"].append(ptr(f))
+            out["local_ptr"].append(ptr(t))
+            out["offsets"].append(pack(f"offsets{h}", sp.offsets[h], f))
+            out["local"].append(pack(f"local{h}", sp.local_nbrs[h], t))
+        copy.synchronize()
+        main.wait_stream(copy)  # later kernels may overwrite the window's buffers only after the copies
+        return out
+
     # ------------------------------------------------------------------ accounting
     def window_bytes(self, nb: int) -> dict[str, int]:
         """Algorithmic bytes of the last window by kernel stage; syncs.

@@ -336,3 +336,41 @@ def test_epoch_graph_replay_tiered_matches_eager(lanes):
                 assert torch.equal(sa.unique[bi, :u], sb.unique[bi, :u])
                 assert torch.equal(xa[bi, :u], xb[bi, :u])
                 assert torch.equal(xa[bi, :u].cpu(), host_table[sa.unique[bi, :u].cpu().long() & 0xFFFFFFFF])
+
+
+def test_window_to_host_packs_every_batch():
+    """window_to_host: one packed pinned copy per array equals the per-batch slices of
+    the padded device buffers, batch boundaries included; staging is reused."""
+    import paper_2305_16588_b200 as P
+    from paper_2305_16588_b200.cache import FeatureStore
+    from paper_2305_16588_b200.graph import synthetic_features_device
+    from paper_2305_16588_b200.pipeline import SampleGatherPipeline
+
+    n, dim, batch, fanouts = 30_000, 100, 96, (7, 3)
+    g = P.generate_synthetic(n, 12, 1.2, seed=12)
+    pool = np.sort(np.random.default_rng(13).choice(n, 1000, replace=False)).astype(np.int64)  # last batch partial
+    store = FeatureStore.resident(synthetic_features_device(0, n, dim))
+    pipe = SampleGatherPipeline(g, P.SamplingConfig(fanouts=fanouts, batch_size=batch), store, len(pool), window=4)
+    staging, seen = {}, []
+
+    def check(p, w0, nbw):
+        out = p.window_to_host(nbw, staging)
+        sp = p.sampler
+        for b in range(nbw):
+            u0, u1 = out["unique_ptr"][b : b + 2]
+            u = int(sp.ucount[b])
+            assert u1 - u0 == u
+            assert torch.equal(out["unique"][u0:u1], sp.unique[b, :u].cpu())
+            assert torch.equal(out["features"][u0:u1], p.features[b, :u].cpu())
+            for h in range(len(fanouts)):
+                f, t = int(sp.counts[h, b]), int(sp.counts[h + 1, b])
+                o0, o1 = out["offsets_ptr"][h][b : b + 2]
+                l0, l1 = out["local_ptr"][h][b : b + 2]
+                assert o1 - o0 == f + 1 and l1 - l0 == t
+                assert torch.equal(out["offsets"][h][o0:o1], sp.offsets[h][b, : f + 1].cpu())
+                assert torch.equal(out["local"][h][l0:l1], sp.local_nbrs[h][b, :t].cpu())
+        seen.append(nbw)
+
+    pipe.run_epoch(pipe.plan_epoch(pool, P.KeyedRng(3).derive(0, 0, 0)), on_window=check)
+    assert sum(seen) == -(-len(pool) // batch) and len(seen) == 3
+    assert staging["features"].is_pinned()
