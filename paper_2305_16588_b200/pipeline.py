@@ -248,8 +248,9 @@ class SampleGatherPipeline:
         segments are first packed on the device (a masked gather, HBM-speed), so the
         PCIe link carries one large copy per array instead of 2 + 2H small copies per
         batch. Returns host tensors (views into `staging`, valid until the next call):
-        'unique' int32 [sum U], 'features' f32 [sum U, D], 'offsets'[h] int32
-        [sum (F_h + 1)], 'local'[h] int32 [sum T_h], and the batch boundaries
+        'unique' int32 [sum U], 'features' f32 [sum U, D] (with a feature store),
+        'offsets'[h] int32 [sum (F_h + 1)], 'local'[h] int32 [sum T_h] (global
+        neighbour ids when the pipeline does not relabel), and the batch boundaries
         'unique_ptr', 'offsets_ptr'[h], 'local_ptr'[h] (int64 numpy [nb + 1]).
         The packing is sync-free (segment rows from the host-side sizes) and each
         array's D2H copy runs on a copy stream while the next array is packed. Reads
@@ -301,7 +302,8 @@ class SampleGatherPipeline:
             out["offsets_ptr"].append(ptr(f))
             out["local_ptr"].append(ptr(t))
             out["offsets"].append(pack(f"offsets{h}", sp.offsets[h], f))
-            out["local"].append(pack(f"local{h}", sp.local_nbrs[h], t))
+            ids = sp.local_nbrs[h] if sp.local_nbrs is not None else sp.nbrs[h]  # relabel=False: global ids
+            out["local"].append(pack(f"local{h}", ids, t))
         copy.synchronize()
         main.wait_stream(copy)  # later kernels may overwrite the window's buffers only after the copies
         return out

@@ -338,7 +338,8 @@ def test_epoch_graph_replay_tiered_matches_eager(lanes):
                 assert torch.equal(xa[bi, :u].cpu(), host_table[sa.unique[bi, :u].cpu().long() & 0xFFFFFFFF])
 
 
-def test_window_to_host_packs_every_batch():
+@pytest.mark.parametrize("relabel", [True, False])
+def test_window_to_host_packs_every_batch(relabel):
     """window_to_host: one packed pinned copy per array equals the per-batch slices of
     the padded device buffers, batch boundaries included; staging is reused."""
     import paper_2305_16588_b200 as P
@@ -350,7 +351,8 @@ def test_window_to_host_packs_every_batch():
     g = P.generate_synthetic(n, 12, 1.2, seed=12)
     pool = np.sort(np.random.default_rng(13).choice(n, 1000, replace=False)).astype(np.int64)  # last batch partial
     store = FeatureStore.resident(synthetic_features_device(0, n, dim))
-    pipe = SampleGatherPipeline(g, P.SamplingConfig(fanouts=fanouts, batch_size=batch), store, len(pool), window=4)
+    pipe = SampleGatherPipeline(g, P.SamplingConfig(fanouts=fanouts, batch_size=batch), store, len(pool), window=4,
+                                relabel=relabel)
     staging, seen = {}, []
 
     def check(p, w0, nbw):
@@ -368,7 +370,8 @@ def test_window_to_host_packs_every_batch():
                 l0, l1 = out["local_ptr"][h][b : b + 2]
                 assert o1 - o0 == f + 1 and l1 - l0 == t
                 assert torch.equal(out["offsets"][h][o0:o1], sp.offsets[h][b, : f + 1].cpu())
-                assert torch.equal(out["local"][h][l0:l1], sp.local_nbrs[h][b, :t].cpu())
+                ids = sp.local_nbrs[h] if relabel else sp.nbrs[h]
+                assert torch.equal(out["local"][h][l0:l1], ids[b, :t].cpu())
         seen.append(nbw)
 
     pipe.run_epoch(pipe.plan_epoch(pool, P.KeyedRng(3).derive(0, 0, 0)), on_window=check)
