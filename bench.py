@@ -427,26 +427,34 @@ def train_run(args, g, cfg, pipe, pool, root, clique, local_idx, world):
     from paper_2305_16588_b200.train import GraphSAGE, synthetic_labels, train_epoch
 
     classes = 47
-    torch.manual_seed(0)
-    model = GraphSAGE(CONFIG["feature_dim"], 256, classes, len(cfg.fanouts)).cuda()
-    opt = torch.optim.SGD(model.parameters(), lr=0.1)
     labels = torch.from_numpy(synthetic_labels(np.arange(g.num_vertices), classes)).cuda()
     plans = [pipe.plan_epoch(pool, root.derive(1000 + e, clique, local_idx)) for e in range(args.train_epochs + 1)]
-    train_epoch(pipe, plans[0], model, opt, labels, max_batches=8)  # warm-up (allocator, kernels)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    losses = []
-    for e in range(args.train_epochs):
-        losses += train_epoch(pipe, plans[1 + e], model, opt, labels)
-    e1.record()
-    torch.cuda.synchronize()
-    sec = e0.elapsed_time(e1) / 1000.0 / args.train_epochs
-    if world > 1:
-        sec = max_over_ranks(sec)
-    return {"seconds": sec, "batches_per_gpu": len(losses) // args.train_epochs, "epochs": args.train_epochs,
-            "model": "GraphSAGE mean, 3 layers, hidden 256, 47 classes, fp32, SGD",
-            "first_loss": float(losses[0]), "last_loss": float(losses[-1])}
+    out = {}
+    for precision in ("fp32", "bf16"):
+        torch.manual_seed(0)
+        model = GraphSAGE(CONFIG["feature_dim"], 256, classes, len(cfg.fanouts)).cuda()
+        opt = torch.optim.SGD(model.parameters(), lr=0.1)
+        train_epoch(pipe, plans[0], model, opt, labels, max_batches=8, precision=precision)  # warm-up
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        losses = []
+        for e in range(args.train_epochs):
+            losses += train_epoch(pipe, plans[1 + e], model, opt, labels, precision=precision)
+        e1.record()
+        torch.cuda.synchronize()
+        sec = e0.elapsed_time(e1) / 1000.0 / args.train_epochs
+        if world > 1:
+            sec = max_over_ranks(sec)
+        gemm = "fp32 (SIMT GEMMs)" if precision == "fp32" else "bf16 autocast GEMMs (fp32 weights, means, loss)"
+        res = {"seconds": sec, "batches_per_gpu": len(losses) // args.train_epochs, "epochs": args.train_epochs,
+               "model": f"GraphSAGE mean, 3 layers, hidden 256, 47 classes, {gemm}, SGD",
+               "first_loss": float(losses[0]), "last_loss": float(losses[-1])}
+        if precision == "fp32":
+            out.update(res)
+        else:
+            out["bf16"] = res
+    return out
 
 
 def e2e_run(args, g, cfg, store, pool, root, clique, local_idx, world, results_to_host: bool = True):

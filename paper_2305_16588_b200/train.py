@@ -51,6 +51,7 @@ def synthetic_labels(ids, num_classes: int) -> np.ndarray:
 def segment_mean(x: torch.Tensor, offsets: torch.Tensor) -> torch.Tensor:
     """Mean of x over consecutive segments [offsets[i], offsets[i+1]); empty -> 0."""
     lengths = offsets[1:] - offsets[:-1]
+    x = x.float()  # bf16 activations under autocast: the mean accumulates in fp32
     if x.shape[0] == 0:
         return x.new_zeros((lengths.shape[0], x.shape[1]))
     return torch.segment_reduce(x, "mean", lengths=lengths, unsafe=True, initial=0.0)
@@ -113,16 +114,25 @@ class GraphSAGE(nn.Module):
         self.classifier = nn.Linear(hidden, num_classes)
 
     def forward(self, batch: TreeBatch) -> torch.Tensor:
+        """Levels are stacked row-wise (level 0, 1, ...), so each layer is one segment
+        mean and one GEMM pair over all the levels it updates: layer l's outputs for
+        levels 0..L-1-l are a row prefix of the stack and their children (levels
+        1..L-l) a contiguous row range; the children offsets of every level are
+        rebased into that range once per batch."""
         L = len(self.layers)
         x = batch.features
+        c = [0]
+        for t in batch.local:
+            c.append(c[-1] + t.numel())  # c[k] = positions in levels < k
+        offs = torch.cat([batch.offsets[lvl][:-1] + (c[lvl + 1] - c[1]) for lvl in range(L)] +
+                         [batch.offsets[L - 1][-1:] + (c[L] - c[1])])
         # first layer: the children's mean is taken straight from the gathered rows
         # (the leaf level, 5x the positions of the level above, is never materialised)
-        h = [F.relu(self.layers[0](x[batch.local[lvl]], None, batch.offsets[lvl], x=x, idx=batch.local[lvl + 1]))
-             for lvl in range(L)]
+        h = F.relu(self.layers[0](x[torch.cat(batch.local[:L])], None, offs, x=x, idx=torch.cat(batch.local[1:])))
         for li in range(1, L):
-            layer = self.layers[li]
-            h = [F.relu(layer(h[lvl], h[lvl + 1], batch.offsets[lvl])) for lvl in range(L - li)]
-        return self.classifier(h[0])
+            top = c[L - li]  # rows updated by this layer: levels 0 .. L-1-li
+            h = F.relu(self.layers[li](h[:top], h[c[1] : c[L - li + 1]], offs[: top + 1]))
+        return self.classifier(h[: c[1]])
 
 
 def tree_batch_from_window(pipe, b: int, labels: torch.Tensor, counts=None, ucount=None) -> TreeBatch:
@@ -142,15 +152,28 @@ def tree_batch_from_window(pipe, b: int, labels: torch.Tensor, counts=None, ucou
     return TreeBatch(feats, local, offsets, labels[seeds])
 
 
-def train_step(model: GraphSAGE, opt: torch.optim.Optimizer, batch: TreeBatch) -> torch.Tensor:
+PRECISIONS = ("fp32", "bf16")
+
+
+def train_step(model: GraphSAGE, opt: torch.optim.Optimizer, batch: TreeBatch, precision: str = "fp32") -> torch.Tensor:
+    """One SGD step. precision="bf16": the layer GEMMs run under bf16 autocast on the
+    tensor cores (weights, gathered rows, the neighbour means and the loss stay fp32)."""
+    if precision not in PRECISIONS:
+        raise ValueError(f"precision must be one of {PRECISIONS}")
     opt.zero_grad(set_to_none=True)
-    loss = F.cross_entropy(model(batch), batch.labels)
+    if precision == "bf16" and batch.features.is_cuda:
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            logits = model(batch)
+        loss = F.cross_entropy(logits.float(), batch.labels)
+    else:
+        loss = F.cross_entropy(model(batch), batch.labels)
     loss.backward()
     opt.step()
     return loss.detach()
 
 
-def train_epoch(pipe, plan, model: GraphSAGE, opt, labels: torch.Tensor, max_batches: int | None = None) -> list:
+def train_epoch(pipe, plan, model: GraphSAGE, opt, labels: torch.Tensor, max_batches: int | None = None,
+                precision: str = "fp32") -> list:
     """Sample the epoch window by window on the device and train on every batch in
     order; returns the per-batch losses (device scalars)."""
     losses = []
@@ -161,7 +184,7 @@ def train_epoch(pipe, plan, model: GraphSAGE, opt, labels: torch.Tensor, max_bat
         for b in range(nbw):
             if max_batches is not None and len(losses) >= max_batches:
                 return
-            losses.append(train_step(model, opt, tree_batch_from_window(p, b, labels, counts, ucount)))
+            losses.append(train_step(model, opt, tree_batch_from_window(p, b, labels, counts, ucount), precision))
 
     pipe.run_epoch(plan, on_window=consume)
     return losses

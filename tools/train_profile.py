@@ -1,4 +1,5 @@
-"""Where the GraphSAGE step's time goes (torch.profiler, C2 shape, 20 batches)."""
+"""Where the GraphSAGE step's time goes (torch.profiler, C2 shape, 20 batches).
+Usage: python tools/train_profile.py [fp32|bf16]"""
 import math
 import sys
 from pathlib import Path
@@ -27,9 +28,10 @@ plan = pipe.plan_epoch(pool, KeyedRng(cfg.seed).derive(0, 0, 0))
 model = GraphSAGE(C["feature_dim"], 256, 47, 3).cuda()
 opt = torch.optim.SGD(model.parameters(), lr=0.1)
 labels = torch.from_numpy(synthetic_labels(np.arange(g.num_vertices), 47)).cuda()
-train_epoch(pipe, plan, model, opt, labels, max_batches=5)
+prec = sys.argv[1] if len(sys.argv) > 1 else "fp32"
+train_epoch(pipe, plan, model, opt, labels, max_batches=5, precision=prec)
 torch.cuda.synchronize()
 with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA, torch.profiler.ProfilerActivity.CPU]) as prof:
-    train_epoch(pipe, plan, model, opt, labels, max_batches=20)
+    train_epoch(pipe, plan, model, opt, labels, max_batches=20, precision=prec)
     torch.cuda.synchronize()
 print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=25, max_name_column_width=70))
