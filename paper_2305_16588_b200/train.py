@@ -51,7 +51,6 @@ def synthetic_labels(ids, num_classes: int) -> np.ndarray:
 def segment_mean(x: torch.Tensor, offsets: torch.Tensor) -> torch.Tensor:
     """Mean of x over consecutive segments [offsets[i], offsets[i+1]); empty -> 0."""
     lengths = offsets[1:] - offsets[:-1]
-    x = x.float()  # bf16 activations under autocast: the mean accumulates in fp32
     if x.shape[0] == 0:
         return x.new_zeros((lengths.shape[0], x.shape[1]))
     return torch.segment_reduce(x, "mean", lengths=lengths, unsafe=True, initial=0.0)
@@ -128,7 +127,9 @@ class GraphSAGE(nn.Module):
                          [batch.offsets[L - 1][-1:] + (c[L] - c[1])])
         # first layer: the children's mean is taken straight from the gathered rows
         # (the leaf level, 5x the positions of the level above, is never materialised)
-        h = F.relu(self.layers[0](x[torch.cat(batch.local[:L])], None, offs, x=x, idx=torch.cat(batch.local[1:])))
+        # under autocast the distinct rows are cast once (U rows), not per position
+        xs = x.to(torch.get_autocast_dtype("cuda")) if x.is_cuda and torch.is_autocast_enabled("cuda") else x
+        h = F.relu(self.layers[0](xs[torch.cat(batch.local[:L])], None, offs, x=x, idx=torch.cat(batch.local[1:])))
         for li in range(1, L):
             top = c[L - li]  # rows updated by this layer: levels 0 .. L-1-li
             h = F.relu(self.layers[li](h[:top], h[c[1] : c[L - li + 1]], offs[: top + 1]))
