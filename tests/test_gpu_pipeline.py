@@ -338,8 +338,8 @@ def test_epoch_graph_replay_tiered_matches_eager(lanes):
                 assert torch.equal(xa[bi, :u].cpu(), host_table[sa.unique[bi, :u].cpu().long() & 0xFFFFFFFF])
 
 
-@pytest.mark.parametrize("relabel", [True, False])
-def test_window_to_host_packs_every_batch(relabel):
+@pytest.mark.parametrize("relabel,lanes", [(True, 1), (False, 1), (True, 2)])
+def test_window_to_host_packs_every_batch(relabel, lanes):
     """window_to_host: one packed pinned copy per array equals the per-batch slices of
     the padded device buffers, batch boundaries included; staging is reused."""
     import paper_2305_16588_b200 as P
@@ -352,7 +352,7 @@ def test_window_to_host_packs_every_batch(relabel):
     pool = np.sort(np.random.default_rng(13).choice(n, 1000, replace=False)).astype(np.int64)  # last batch partial
     store = FeatureStore.resident(synthetic_features_device(0, n, dim))
     pipe = SampleGatherPipeline(g, P.SamplingConfig(fanouts=fanouts, batch_size=batch), store, len(pool), window=4,
-                                relabel=relabel)
+                                relabel=relabel, lanes=lanes)
     staging, seen = {}, []
 
     def check(p, w0, nbw):
