@@ -310,6 +310,16 @@ int gc_ipc_close(void* d_ptr);
 /* Enable peer access from the current device to `peer` (same-process multi-GPU). */
 int gc_enable_peer(int peer);
 
+/* Inter-clique LDG partition, host preprocessing (replaces partition_inter_clique's
+ * placement + refinement, src/partition.py:85-152). All arrays are HOST memory:
+ * the CSR, the BFS root order (KeyedRng(seed).derive(0x5EED).permutation(n), computed
+ * by gc_permutation), capacity = the reference's int((1 + eps) * ceil(n / parts)).
+ * Writes h_assignment[n]; h_cuts (optional, 2 * refine_passes) receives the edge cut
+ * before/after each refinement pass run. GC_ERR_ASSERT if a pass raised the cut. */
+int gc_partition_ldg(const uint64_t* h_row_offsets, const uint32_t* h_cols, uint64_t num_vertices,
+                     uint64_t num_edges, const int64_t* h_root_order, uint32_t num_parts, int64_t capacity,
+                     int refine_passes, int32_t* h_assignment, uint64_t* h_cuts);
+
 #ifdef __cplusplus
 }
 #endif

@@ -144,6 +144,7 @@ SIGNATURES = {
     "gc_ipc_import": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]),
     "gc_ipc_close": (ctypes.c_int, [V]),
     "gc_enable_peer": (ctypes.c_int, [ctypes.c_int]),
+    "gc_partition_ldg": (ctypes.c_int, [V, V, U64, U64, V, U32, I64, ctypes.c_int, V, V]),
 }
 
 _LIB = None

@@ -1,19 +1,27 @@
-"""Training-vertex sharding across the GPUs of a clique (partition.py of the reference).
+"""Hierarchical partitioning (partition.py of the reference): the inter-clique LDG
+edge-cut split and the intra-clique training-vertex tablets.
 
-Host-side preprocessing that stays on the host (north star). On one 8xB200 NVSwitch
-clique the inter-clique LDG level collapses (num_parts == 1 returns all zeros,
-partition.py:100-101), so only the intra-clique tablet split and its binding to
-GPUs are needed to produce the per-GPU seed pools of the data path.
+Host-side preprocessing (north star). On one 8xB200 NVSwitch clique the
+inter-clique level collapses (num_parts == 1 returns all zeros, partition.py:100-101);
+for several cliques, and for the pagraph-plus comparison policy, the LDG placement
+runs natively in the library (gc_partition_ldg: sequential greedy + refinement in
+C++, BFS roots from the device permutation).
 """
 
 from __future__ import annotations
 
+import ctypes
+import math
 from dataclasses import dataclass
 
 import numpy as np
 
+from . import _lib
 from .graph import CsrGraph, TrainingSet
 from .hardware import CliqueLayout
+from .rng import KeyedRng
+
+ROLE_BFS_ROOTS = 0x5EED  # partition.py:53
 
 
 def _mix64_np(x: np.ndarray) -> np.ndarray:
@@ -46,6 +54,58 @@ class Partitioning:
 def single_clique_partitioning(graph: CsrGraph) -> Partitioning:
     """partition_inter_clique with num_parts == 1 (partition.py:100-101)."""
     return Partitioning(np.zeros(graph.num_vertices, dtype=np.int32), 1)
+
+
+def ldg_capacity(n: int, num_parts: int, epsilon: float) -> int:
+    """Per-part vertex cap, int((1 + eps) * ceil(n / k)) and at least ceil(n / k)
+    (partition.py:103-104)."""
+    even = math.ceil(n / num_parts)
+    return max(int((1.0 + epsilon) * even), even)
+
+
+def ldg_assign(graph: CsrGraph, num_parts: int, capacity: int, root_order: np.ndarray, refine_passes: int = 2,
+               lib: ctypes.CDLL | None = None) -> tuple[np.ndarray, np.ndarray]:
+    """gc_partition_ldg over host arrays: (assignments int32 [n], per-pass cuts
+    uint64 [passes, 2] before/after, zero rows for passes not run)."""
+    n = graph.num_vertices
+    roots = np.ascontiguousarray(root_order, dtype=np.int64)
+    if roots.shape != (n,):
+        raise ValueError("root_order must hold every vertex once")
+    out = np.empty(n, dtype=np.int32)
+    cuts = np.zeros((max(refine_passes, 1), 2), dtype=np.uint64)
+    L = lib if lib is not None else _lib.lib()
+    _lib.check(L.gc_partition_ldg(graph.row_offsets.ctypes.data, graph.col_indices.ctypes.data, n, graph.num_edges,
+                                  roots.ctypes.data, num_parts, capacity, refine_passes, out.ctypes.data,
+                                  cuts.ctypes.data), "partition_inter_clique")
+    return out, cuts[: max(refine_passes, 0)]
+
+
+def partition_inter_clique(graph: CsrGraph, num_parts: int, epsilon: float = 0.05, seed: int = 0,
+                           refine_passes: int = 2) -> Partitioning:
+    """Balanced edge-cut-minimising streaming partition, deterministic per seed
+    (partition.py:85-130): BFS stream order from KeyedRng(seed).derive(0x5EED)'s
+    permutation (device), then the native LDG placement + refinement."""
+    n = graph.num_vertices
+    if num_parts < 1:
+        raise ValueError("num_parts must be >= 1")
+    if num_parts > n:
+        raise ValueError(f"num_parts {num_parts} exceeds num_vertices {n}")
+    if epsilon < 0:
+        raise ValueError("epsilon must be >= 0")
+    if num_parts == 1:
+        return Partitioning(np.zeros(n, dtype=np.int32), 1)
+    roots = KeyedRng(seed).derive(ROLE_BFS_ROOTS).permutation(n)
+    assignments, _ = ldg_assign(graph, num_parts, ldg_capacity(n, num_parts, epsilon), roots, refine_passes)
+    return Partitioning(assignments, num_parts)
+
+
+def edge_cut_ratio(graph: CsrGraph, partitioning: Partitioning) -> float:
+    """Fraction of directed edges whose endpoints lie in different parts (partition.py:162-166)."""
+    if graph.num_edges == 0:
+        return 0.0
+    a = partitioning.assignments
+    src = np.repeat(np.arange(graph.num_vertices, dtype=np.int64), graph.out_degrees)
+    return int(np.count_nonzero(a[src] != a[graph.col_indices.astype(np.int64)])) / graph.num_edges
 
 
 @dataclass(frozen=True)

@@ -12,9 +12,10 @@ The comparison cache policies of the reference (gnnlab-replicated, quiver-plus,
 pagraph-plus next to legion-hierarchical; simulator.py:41-91, :259-402) run through the
 same device kernels: presampling (K2/K3/K5), hotness ranking and prefix split (K6/K8
 helpers), the plan search for the hierarchical policy (K7) and the epoch replay + tier
-accounting (K9). The LDG streaming partitioner they need for more than one clique or
-for pagraph-plus is host preprocessing outside this build: pass its result as
-`partitioning=`.
+accounting (K9). The LDG partition they need for more than one clique or for
+pagraph-plus is computed as the reference does (partition_inter_clique with seed
+derive_seed(seed, 0x52), simulator.py:273-276; native gc_partition_ldg) unless one
+is passed as `partitioning=`.
 """
 
 from __future__ import annotations
@@ -31,7 +32,7 @@ import warnings
 
 from .graph import TrainingSet
 from .hardware import block_layout
-from .partition import Partitioning, assign_tablets, split_intra_clique
+from .partition import Partitioning, assign_tablets, partition_inter_clique, split_intra_clique
 from .planner import (
     CacheAssignment,
     build_candidate_orders,
@@ -202,14 +203,15 @@ def effective_layout(policy: CachePolicy, layout: CliqueLayout) -> CliqueLayout:
     return block_layout(layout.num_gpus, 1) if policy.variant in _NO_NVLINK else layout
 
 
-def _need_partitioning(partitioning: Partitioning | None, parts: int, graph: CsrGraph) -> Partitioning:
-    if parts == 1:
-        return Partitioning(np.zeros(graph.num_vertices, dtype=np.int32), 1)
-    if partitioning is None or partitioning.num_parts != parts:
-        raise NotImplementedError(
-            f"this policy needs an LDG partition into {parts} parts (partition_inter_clique, host "
-            "preprocessing outside the B200 path); pass it as partitioning=")
-    return partitioning
+def _need_partitioning(partitioning: Partitioning | None, parts: int, graph: CsrGraph, epsilon: float,
+                       seed: int) -> Partitioning:
+    """The caller's partition, else partition_inter_clique(graph, parts, epsilon,
+    derive_seed(seed, 0x52)) as the reference computes it (simulator.py:273, :276)."""
+    if partitioning is not None:
+        if partitioning.num_parts != parts:
+            raise ValueError(f"partitioning has {partitioning.num_parts} parts, this policy needs {parts}")
+        return partitioning
+    return partition_inter_clique(graph, parts, epsilon, derive_seed(seed, 0x52))
 
 
 def policy_seed_pools(policy: CachePolicy, graph: CsrGraph, training: TrainingSet, layout: CliqueLayout, seed: int,
@@ -220,10 +222,10 @@ def policy_seed_pools(policy: CachePolicy, graph: CsrGraph, training: TrainingSe
         perm = np.random.default_rng(derive_seed(seed, 0x51)).permutation(training.vertex_ids)
         return [np.sort(perm[g::num_gpus]) for g in range(num_gpus)]
     if policy.variant == POLICY_PAGRAPH:
-        parts = _need_partitioning(partitioning, num_gpus, graph)
+        parts = _need_partitioning(partitioning, num_gpus, graph, epsilon, seed)
         ids = training.vertex_ids
         return [ids[parts.assignments[ids] == g] for g in range(num_gpus)]
-    parts = _need_partitioning(partitioning, layout.clique_count, graph)
+    parts = _need_partitioning(partitioning, layout.clique_count, graph, epsilon, seed)
     return assign_tablets(split_intra_clique(training, parts, layout), layout)
 
 

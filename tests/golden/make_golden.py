@@ -219,14 +219,50 @@ def policy_vectors():
     np.savez_compressed(OUT / "policies.npz", **d)
 
 
+def partition_vectors():
+    """partition_inter_clique (partition.py:85-130) over graphs with self loops,
+    duplicate edges, isolated vertices and several components, for a grid of part
+    counts, imbalance and refinement passes; edge_cut_ratio of each result."""
+    from gnncache.graph import CsrGraph
+    from gnncache.partition import edge_cut_ratio, partition_inter_clique
+
+    d = {}
+    rng = np.random.default_rng(77)
+    graphs = [generate_synthetic(3000, 8, 1.2, seed=3), random_graph(rng, 700, 6)]
+    # self loops + duplicates + isolated tail + a second component
+    src = np.array([0, 0, 1, 2, 2, 3, 5, 6, 6, 9, 9, 10, 11], dtype=np.int64)
+    dst = np.array([0, 1, 1, 3, 3, 2, 6, 5, 7, 10, 9, 11, 9], dtype=np.int64)
+    graphs.append(CsrGraph.from_edges(16, src, dst))
+    cases = []
+    for gi, g in enumerate(graphs):
+        d[f"g{gi}_ro"], d[f"g{gi}_ci"] = g.row_offsets, g.col_indices
+        for parts in (2, 3, 5, 8):
+            for eps in (0.0, 0.05, 0.3):
+                for passes in (0, 1, 2, 5):
+                    for seed in (0, 1234):
+                        if parts > g.num_vertices:
+                            continue
+                        part = partition_inter_clique(g, parts, eps, seed, passes)
+                        k = len(cases)
+                        d[f"c{k}"] = part.assignments
+                        d[f"c{k}_cut"] = np.array([edge_cut_ratio(g, part)])
+                        cases.append((gi, parts, int(eps * 100), passes, seed))
+    d["cases"] = np.array(cases, dtype=np.int64)
+    np.savez_compressed(OUT / "partition.npz", **d)
+
+
 if __name__ == "__main__":
     if "--policies" in sys.argv:
         policy_vectors()
+        raise SystemExit(0)
+    if "--partition" in sys.argv:
+        partition_vectors()
         raise SystemExit(0)
     rng_vectors()
     sampling_vectors()
     presampling_vectors()
     planner_vectors()
     policy_vectors()
+    partition_vectors()
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)

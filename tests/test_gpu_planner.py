@@ -176,11 +176,13 @@ def test_time_objective_prefers_the_slower_access_shape(golden):
     assert fast.alpha <= base.alpha <= slow.alpha
 
 
-def test_cache_policies_match_reference(golden):
+@pytest.mark.parametrize("supplied", [True, False])
+def test_cache_policies_match_reference(golden, supplied):
     """run_policy_pipeline for all four policies (simulator.py:259-402) on 4 GPUs as two
     cliques of 2 and one clique of 4, two size parameters each: seed pools, cache
     contents and the epoch's CPU transactions / traffic matrix equal the reference's
-    (the LDG partitions are the reference's own, recorded in the golden file)."""
+    (supplied: the reference's own LDG partitions from the golden file; else the
+    pipeline partitions the graph itself, device permutation + gc_partition_ldg)."""
     import warnings
 
     import paper_2305_16588_b200 as P
@@ -202,7 +204,7 @@ def test_cache_policies_match_reference(golden):
         with warnings.catch_warnings():
             warnings.simplefilter("ignore")
             run = S.run_policy_pipeline(policy, graph, train, layout, cfg, spec, feat, master_seed=5, epsilon=0.05,
-                                        partitioning=part)
+                                        partitioning=part if supplied else None)
         key = f"L{li}_v{vi}_r{ri}"
         assert run.layout.clique_size == int(g[f"{key}_csize"][0])
         for gi in range(ngpu):
@@ -213,14 +215,32 @@ def test_cache_policies_match_reference(golden):
         assert np.array_equal(run.report.traffic_matrix, g[f"{key}_matrix"]), key
 
 
-def test_policy_without_partition_raises_for_multi_clique():
+def test_partition_inter_clique_matches_reference(golden):
+    """partition_inter_clique on the device box (BFS roots by gc_permutation, LDG by
+    gc_partition_ldg) gives the reference's partitions; a partition with the wrong
+    part count is rejected by the policy pipeline."""
     import paper_2305_16588_b200 as P
     from paper_2305_16588_b200 import simulator as S
 
-    g = P.generate_synthetic(500, 6, 1.2, seed=1)
-    train = P.select_training_set(g, 0.2, seed=3)
-    with pytest.raises(NotImplementedError):
-        S.policy_seed_pools(S.CachePolicy(S.POLICY_PAGRAPH, cache_ratio=0.1), g, train, P.block_layout(4, 2), 5)
-    pools = S.policy_seed_pools(S.CachePolicy(S.POLICY_HIERARCHICAL, cache_ratio=0.1), g, train,
+    g = golden("partition")
+    for k, (gi, parts, eps100, passes, seed) in enumerate(g["cases"]):
+        if k % 7:  # every 7th case here; all of them run on CPU in test_partition_cpu.py
+            continue
+        graph = P.CsrGraph(len(g[f"g{gi}_ro"]) - 1, len(g[f"g{gi}_ci"]), g[f"g{gi}_ro"], g[f"g{gi}_ci"])
+        part = P.partition_inter_clique(graph, int(parts), eps100 / 100.0, int(seed), int(passes))
+        assert np.array_equal(part.assignments, g[f"c{k}"]), k
+        assert P.edge_cut_ratio(graph, part) == float(g[f"c{k}_cut"][0])
+    graph = P.generate_synthetic(500, 6, 1.2, seed=1)
+    train = P.select_training_set(graph, 0.2, seed=3)
+    with pytest.raises(ValueError):
+        S.policy_seed_pools(S.CachePolicy(S.POLICY_PAGRAPH, cache_ratio=0.1), graph, train, P.block_layout(4, 2), 5,
+                            partitioning=P.Partitioning(np.zeros(500, dtype=np.int32), 2))
+    with pytest.raises(ValueError):
+        P.partition_inter_clique(graph, 0)
+    with pytest.raises(ValueError):
+        P.partition_inter_clique(graph, 501)
+    with pytest.raises(ValueError):
+        P.partition_inter_clique(graph, 2, epsilon=-0.1)
+    pools = S.policy_seed_pools(S.CachePolicy(S.POLICY_HIERARCHICAL, cache_ratio=0.1), graph, train,
                                 P.block_layout(4, 4), 5)
     assert sorted(np.concatenate(pools).tolist()) == sorted(train.vertex_ids.tolist())
