@@ -153,3 +153,22 @@ def assign_tablets(tablets: TabletAssignment, layout: CliqueLayout) -> list[np.n
         for li, gpu in enumerate(members):
             pools[gpu] = tablets.tablets[ci][li]
     return pools
+
+
+def dump_partitioning(partitioning: Partitioning, path) -> None:
+    """One "vertex part" line per vertex (partition.py:221-224)."""
+    a = np.asarray(partitioning.assignments, dtype=np.int64)
+    with open(path, "w", encoding="utf-8") as fh:
+        np.savetxt(fh, np.stack([np.arange(len(a), dtype=np.int64), a], axis=1), fmt="%d")
+
+
+def dump_tablets(tablets: TabletAssignment, layout: CliqueLayout, path) -> None:
+    """One "vertex clique gpu_in_clique" line per training vertex, clique-major
+    (partition.py:227-232)."""
+    with open(path, "w", encoding="utf-8") as fh:
+        for ci in range(layout.clique_count):
+            for li in range(layout.clique_size):
+                v = np.asarray(tablets.tablets[ci][li], dtype=np.int64)
+                if len(v):
+                    rows = np.stack([v, np.full(len(v), ci, np.int64), np.full(len(v), li, np.int64)], axis=1)
+                    np.savetxt(fh, rows, fmt="%d")

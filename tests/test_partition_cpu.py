@@ -71,3 +71,18 @@ def test_ldg_argument_errors(lib):
         ldg_assign(graph, 2, 2, np.array([0, 0, 1]), lib=lib)  # not a permutation
     with pytest.raises(ValueError):
         ldg_assign(graph, 4, 2, np.arange(3), lib=lib)  # more parts than vertices
+
+
+def test_dump_formats(tmp_path):
+    """dump_partitioning / dump_tablets write the reference's text lines
+    (partition.py:221-232): "v p" per vertex; "v clique gpu" per training vertex."""
+    import paper_2305_16588_b200 as P
+
+    part = P.Partitioning(np.array([1, 0, 2, 2, 0], dtype=np.int32), 3)
+    P.dump_partitioning(part, tmp_path / "p.txt")
+    assert (tmp_path / "p.txt").read_text() == "".join(f"{v} {p}\n" for v, p in enumerate([1, 0, 2, 2, 0]))
+    layout = P.block_layout(4, 2)
+    tabs = P.TabletAssignment(((np.array([3, 9]), np.array([], dtype=np.int64)), (np.array([1]), np.array([4, 7]))))
+    P.dump_tablets(tabs, layout, tmp_path / "t.txt")
+    want = "".join(f"{v} {ci} {li}\n" for ci in range(2) for li in range(2) for v in tabs.tablets[ci][li])
+    assert (tmp_path / "t.txt").read_text() == want
