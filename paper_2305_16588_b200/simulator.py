@@ -308,3 +308,34 @@ def run_policy_pipeline(policy: CachePolicy, graph: CsrGraph, training: Training
     assignment = build_policy_cache(policy, hotness, lay, graph, feat, spec_eff)
     report = simulate_epoch(graph, pools, pcfg, assignment, lay, spec_eff, feat, seed=derive_seed(master_seed, 0x20))
     return PolicyRun(policy, lay, pools, hotness, assignment, report)
+
+
+@dataclass(frozen=True)
+class SweepPoint:
+    """One GPU count of a policy sweep (simulator.py:405-409)."""
+
+    gpu_count: int
+    total_cpu_txn: int
+    normalized: float
+
+
+def sweep_gpus(policy: CachePolicy, gpu_counts: list[int], graph: CsrGraph, training: TrainingSet,
+               cfg: SamplingConfig, feat: FeatureSpec, clique_size: int = 2, seed: int = 0, epsilon: float = 0.05,
+               cache_line_bytes: int = 64) -> list[SweepPoint]:
+    """Total host-tier PCIe transactions of one policy across GPU counts, normalised
+    to the smallest count (simulator.py:412-441): each count runs the whole policy
+    pipeline on the device with block cliques of min(clique_size, count) GPUs and a
+    clique budget of the policy's per-GPU bytes x clique size."""
+    counts = sorted(gpu_counts)
+    totals = []
+    for count in counts:
+        size = min(clique_size, count)
+        if count % size:
+            raise ValueError(f"gpu count {count} incompatible with clique size {size}")
+        layout = block_layout(count, size)
+        spec = HardwareSpec(layout=layout, clique_budget_bytes=policy.per_gpu_bytes(graph, feat) * size,
+                            cache_line_bytes=cache_line_bytes)
+        run = run_policy_pipeline(policy, graph, training, layout, cfg, spec, feat, derive_seed(seed, count), epsilon)
+        totals.append(run.report.total_cpu_txn)
+    anchor = totals[0] if totals and totals[0] else 1
+    return [SweepPoint(c, t, t / anchor) for c, t in zip(counts, totals)]

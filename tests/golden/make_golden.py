@@ -251,7 +251,71 @@ def partition_vectors():
     np.savez_compressed(OUT / "partition.npz", **d)
 
 
+def hardware_vectors():
+    """detect_cliques (hardware.py:109-139) on random symmetric NVLink matrices (some
+    decompose into unequal cliques and raise) and block matrices; save/load text."""
+    import tempfile
+
+    from gnncache.hardware import HeterogeneousTopologyError, NvlinkMatrix, detect_cliques, save_hardware_config
+
+    rng = np.random.default_rng(5)
+    d = {}
+    mats = []
+    for n in (1, 2, 3, 4, 6, 8, 8, 10, 12):
+        for p in (0.3, 0.6, 0.9):
+            a = rng.random((n, n)) < p
+            a = np.triu(a, 1)
+            mats.append(a | a.T | np.eye(n, dtype=bool))
+    for n, c in ((8, 2), (8, 4), (8, 8), (12, 3)):
+        blk = np.arange(n) // c
+        mats.append(blk[:, None] == blk[None, :])
+    # equal-size cliques with ties between several maximum cliques
+    ring = np.eye(6, dtype=bool)
+    for i in range(6):
+        ring[i, (i + 1) % 6] = ring[(i + 1) % 6, i] = True
+    mats.append(ring)
+    for k, a in enumerate(mats):
+        d[f"m{k}"] = a
+        try:
+            lay = detect_cliques(NvlinkMatrix(a))
+            d[f"m{k}_cliques"] = np.array([g for c in lay.cliques for g in c], dtype=np.int64)
+            d[f"m{k}_size"] = np.array([lay.clique_size])
+        except HeterogeneousTopologyError:
+            d[f"m{k}_size"] = np.array([-1])
+    d["count"] = np.array([len(mats)])
+    from gnncache.hardware import HardwareSpec, block_layout
+
+    with tempfile.TemporaryDirectory() as tmp:
+        path = Path(tmp) / "hw.txt"
+        save_hardware_config(HardwareSpec(block_layout(8, 4), 123456, 128), path)
+        d["saved_text"] = np.array([path.read_text()])
+    np.savez_compressed(OUT / "hardware.npz", **d)
+
+
+def sweep_vectors():
+    """sweep_gpus (simulator.py:412-441) for two policies over 1/2/4 GPUs."""
+    from gnncache.simulator import CachePolicy, sweep_gpus
+
+    g = generate_synthetic(2000, 8, 1.2, seed=43)
+    train = select_training_set(g, 0.1, seed=derive_seed(6, 2))
+    cfg = SamplingConfig(fanouts=(6, 3), batch_size=32, presample_epochs=1, seed=derive_seed(6, 4))
+    d = {"graph_ro": g.row_offsets, "graph_ci": g.col_indices, "train_ids": train.vertex_ids}
+    for name, policy in (("hier", CachePolicy("legion-hierarchical", cache_ratio=0.05)),
+                         ("pagraph", CachePolicy("pagraph-plus", budget_bytes=30_000))):
+        pts = sweep_gpus(policy, [4, 1, 2], g, train, cfg, FeatureSpec(32), clique_size=2, seed=9)
+        d[f"{name}_counts"] = np.array([p.gpu_count for p in pts])
+        d[f"{name}_txn"] = np.array([p.total_cpu_txn for p in pts])
+        d[f"{name}_norm"] = np.array([p.normalized for p in pts])
+    np.savez_compressed(OUT / "sweep.npz", **d)
+
+
 if __name__ == "__main__":
+    if "--sweep" in sys.argv:
+        sweep_vectors()
+        raise SystemExit(0)
+    if "--hardware" in sys.argv:
+        hardware_vectors()
+        raise SystemExit(0)
     if "--policies" in sys.argv:
         policy_vectors()
         raise SystemExit(0)
@@ -264,5 +328,7 @@ if __name__ == "__main__":
     planner_vectors()
     policy_vectors()
     partition_vectors()
+    hardware_vectors()
+    sweep_vectors()
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)

@@ -244,3 +244,33 @@ def test_partition_inter_clique_matches_reference(golden):
     pools = S.policy_seed_pools(S.CachePolicy(S.POLICY_HIERARCHICAL, cache_ratio=0.1), graph, train,
                                 P.block_layout(4, 4), 5)
     assert sorted(np.concatenate(pools).tolist()) == sorted(train.vertex_ids.tolist())
+
+
+def test_sweep_gpus_matches_reference(golden):
+    """sweep_gpus (simulator.py:412-441): per-GPU-count host transactions and their
+    normalisation equal the reference's, for the hierarchical policy and pagraph-plus
+    (which partitions the graph itself at every count)."""
+    import paper_2305_16588_b200 as P
+
+    g = golden("sweep")
+    graph = P.CsrGraph(len(g["graph_ro"]) - 1, len(g["graph_ci"]), g["graph_ro"], g["graph_ci"])
+    train = P.TrainingSet(g["train_ids"], 0.1)
+    cfg = P.SamplingConfig(fanouts=(6, 3), batch_size=32, presample_epochs=1, seed=P.derive_seed(6, 4))
+    for name, policy in (("hier", P.CachePolicy("legion-hierarchical", cache_ratio=0.05)),
+                         ("pagraph", P.CachePolicy("pagraph-plus", budget_bytes=30_000))):
+        pts = P.sweep_gpus(policy, [4, 1, 2], graph, train, cfg, P.FeatureSpec(32), clique_size=2, seed=9)
+        assert [p.gpu_count for p in pts] == list(g[f"{name}_counts"])
+        assert [p.total_cpu_txn for p in pts] == list(g[f"{name}_txn"]), name
+        assert [p.normalized for p in pts] == list(g[f"{name}_norm"])
+
+
+def test_probe_nvlink_matrix_layout():
+    """The visible GPUs' peer table gives a valid clique layout (one clique per box)."""
+    import torch
+
+    import paper_2305_16588_b200 as P
+
+    m = P.probe_nvlink_matrix()
+    assert m.size == torch.cuda.device_count()
+    lay = P.detect_cliques(m)
+    assert lay.num_gpus == m.size
