@@ -373,3 +373,19 @@ def materialize_assignment(orders_by_clique: list[CandidateOrders], plans: list[
         if total > plan.budget_bytes:
             raise AssertionError("materialized clique cache exceeds its budget")
     return out
+
+
+def plan_report(layout: CliqueLayout, plans: list[CachePlan], estimates: list[TrafficEstimate], delta_alpha: float,
+                tablet_sizes: list[list[int]] | None = None) -> dict:
+    """JSON-ready per-clique plan summary (planner.py:322-351)."""
+    cliques = []
+    for ci in range(layout.clique_count):
+        plan, est = plans[ci], estimates[ci]
+        entry = {"clique": ci, "alpha": plan.alpha, "topo_budget_bytes": plan.topo_budget,
+                 "feat_budget_bytes": plan.feat_budget, "topo_prefix_len": est.topo_prefix_len,
+                 "feat_prefix_len": est.feat_prefix_len, "sampling_txns": est.sampling_txns,
+                 "feature_txns": est.feature_txns, "total_txns": est.total_txns}
+        if tablet_sizes is not None:
+            entry["tablet_sizes"] = tablet_sizes[ci]
+        cliques.append(entry)
+    return {"delta_alpha": delta_alpha, "alpha_grid_points": len(alpha_grid(delta_alpha)), "cliques": cliques}

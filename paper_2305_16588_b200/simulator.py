@@ -339,3 +339,24 @@ def sweep_gpus(policy: CachePolicy, gpu_counts: list[int], graph: CsrGraph, trai
         totals.append(run.report.total_cpu_txn)
     anchor = totals[0] if totals and totals[0] else 1
     return [SweepPoint(c, t, t / anchor) for c, t in zip(counts, totals)]
+
+
+def write_report_csv(report: TrafficReport, path, provenance: str | None = None) -> None:
+    """Per-GPU hit rates and transactions as CSV (simulator.py:444-459)."""
+    topo, feats = report.topo_hit_rate, report.feat_hit_rate
+    lines = [f"# {provenance}\n"] if provenance else []
+    lines.append("gpu,topo_hit_rate,feat_hit_rate,sampling_cpu_txn,feature_cpu_txn,feature_peer_txn\n")
+    lines += [f"{g},{topo[g]:.6f},{feats[g]:.6f},{report.sampling_cpu_txn[g]},{report.feature_cpu_txn[g]},"
+              f"{report.feature_peer_txn[g]}\n" for g in range(report.num_gpus)]
+    with open(path, "w", encoding="utf-8") as fh:
+        fh.writelines(lines)
+
+
+def write_traffic_matrix_csv(report: TrafficReport, path, provenance: str | None = None) -> None:
+    """Traffic matrix rows dest_gpu x (from_gpu*, from_cpu) as CSV (simulator.py:462-470)."""
+    lines = [f"# {provenance}\n"] if provenance else []
+    cols = [f"from_gpu{g}" for g in range(report.num_gpus)] + ["from_cpu"]
+    lines.append("dest_gpu," + ",".join(cols) + "\n")
+    lines += [f"{g}," + ",".join(str(int(x)) for x in report.traffic_matrix[g]) + "\n" for g in range(report.num_gpus)]
+    with open(path, "w", encoding="utf-8") as fh:
+        fh.writelines(lines)

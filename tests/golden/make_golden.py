@@ -309,7 +309,40 @@ def sweep_vectors():
     np.savez_compressed(OUT / "sweep.npz", **d)
 
 
+def report_vectors():
+    """write_report_csv / write_traffic_matrix_csv (simulator.py:444-470) of one policy
+    run, and plan_report (planner.py:322-351) of the hierarchical plan."""
+    import json
+    import tempfile
+
+    from gnncache.planner import plan_report
+    from gnncache.simulator import CachePolicy, run_policy_pipeline, write_report_csv, write_traffic_matrix_csv
+
+    g = generate_synthetic(2000, 8, 1.2, seed=43)
+    train = select_training_set(g, 0.1, seed=derive_seed(6, 2))
+    cfg = SamplingConfig(fanouts=(6, 3), batch_size=32, presample_epochs=1, seed=derive_seed(6, 4))
+    layout = block_layout(4, 2)
+    spec = HardwareSpec(layout, clique_budget_bytes=50_000)
+    feat = FeatureSpec(32)
+    run = run_policy_pipeline(CachePolicy("legion-hierarchical"), g, train, layout, cfg, spec, feat, master_seed=3)
+    d = {"graph_ro": g.row_offsets, "graph_ci": g.col_indices, "train_ids": train.vertex_ids}
+    with tempfile.TemporaryDirectory() as tmp:
+        write_report_csv(run.report, Path(tmp) / "r.csv", provenance="seed 3")
+        write_traffic_matrix_csv(run.report, Path(tmp) / "m.csv")
+        d["report_csv"] = np.array([(Path(tmp) / "r.csv").read_text()])
+        d["matrix_csv"] = np.array([(Path(tmp) / "m.csv").read_text()])
+    orders = [build_candidate_orders(h) for h in run.hotness]
+    plans, ests = zip(*[search_optimal_plan(o, spec.clique_budget_bytes, 0.05, g, feat, spec, h.sampling_txn_total)
+                        for o, h in zip(orders, run.hotness)])
+    d["plan_report"] = np.array([json.dumps(plan_report(layout, list(plans), list(ests), 0.05, [[3, 4], [5, 6]]),
+                                            sort_keys=True)])
+    np.savez_compressed(OUT / "reports.npz", **d)
+
+
 if __name__ == "__main__":
+    if "--reports" in sys.argv:
+        report_vectors()
+        raise SystemExit(0)
     if "--sweep" in sys.argv:
         sweep_vectors()
         raise SystemExit(0)
@@ -330,5 +363,6 @@ if __name__ == "__main__":
     partition_vectors()
     hardware_vectors()
     sweep_vectors()
+    report_vectors()
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)

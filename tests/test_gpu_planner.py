@@ -274,3 +274,32 @@ def test_probe_nvlink_matrix_layout():
     assert m.size == torch.cuda.device_count()
     lay = P.detect_cliques(m)
     assert lay.num_gpus == m.size
+
+
+def test_reports_match_reference(golden, tmp_path):
+    """write_report_csv / write_traffic_matrix_csv / plan_report produce the reference's
+    text for the same policy run and plans (simulator.py:444-470, planner.py:322-351)."""
+    import json
+
+    import paper_2305_16588_b200 as P
+    from paper_2305_16588_b200 import simulator as S
+    from paper_2305_16588_b200.planner import plan_report
+
+    g = golden("reports")
+    graph = P.CsrGraph(len(g["graph_ro"]) - 1, len(g["graph_ci"]), g["graph_ro"], g["graph_ci"])
+    train = P.TrainingSet(g["train_ids"], 0.1)
+    cfg = P.SamplingConfig(fanouts=(6, 3), batch_size=32, presample_epochs=1, seed=P.derive_seed(6, 4))
+    layout = P.block_layout(4, 2)
+    spec = P.HardwareSpec(layout, clique_budget_bytes=50_000)
+    feat = P.FeatureSpec(32)
+    run = S.run_policy_pipeline(P.CachePolicy("legion-hierarchical"), graph, train, layout, cfg, spec, feat,
+                                master_seed=3)
+    S.write_report_csv(run.report, tmp_path / "r.csv", provenance="seed 3")
+    S.write_traffic_matrix_csv(run.report, tmp_path / "m.csv")
+    assert (tmp_path / "r.csv").read_text() == str(g["report_csv"][0])
+    assert (tmp_path / "m.csv").read_text() == str(g["matrix_csv"][0])
+    orders = [P.build_candidate_orders(h) for h in run.hotness]
+    plans, ests = zip(*[P.search_optimal_plan(o, spec.clique_budget_bytes, 0.05, graph, feat, spec,
+                                              h.sampling_txn_total) for o, h in zip(orders, run.hotness)])
+    got = json.dumps(plan_report(layout, list(plans), list(ests), 0.05, [[3, 4], [5, 6]]), sort_keys=True)
+    assert got == str(g["plan_report"][0])
