@@ -177,7 +177,10 @@ uint64_t gc_summary_words(int64_t num_vertices);
  * sorted distinct ids of batch b -> d_unique + b*unique_stride, count -> d_unique_count[b];
  * d_rank_table (optional, 2*bitmap_words u32 per batch) receives {exclusive popcount
  * prefix, bitmap word} per word for gc_relabel. feat_lookups (optional) += 1 per
- * distinct id (sampling.py:242). clear_bitmap zeroes the bitmap as it is consumed. */
+ * distinct id (sampling.py:242). clear_bitmap zeroes the bitmap as it is consumed.
+ * At most unique_stride ids are written per batch; d_unique_count[b] always holds the
+ * true distinct count, so d_unique_count[b] > unique_stride reports an overflow (the
+ * caller raises; the bitmap is still cleared in full). */
 size_t gc_unique_temp_bytes(uint32_t num_batches, const gc_visited_t* visited);
 int gc_unique_compact(const gc_visited_t* visited, uint32_t num_batches, uint32_t* d_unique,
                       uint64_t unique_stride, uint32_t* d_unique_count, uint32_t* d_rank_table,
@@ -303,8 +306,20 @@ int gc_host_unregister(void* host_ptr);
  * `*mapped_bytes` (bytes rounded up to the granularity) must be passed to the free. */
 int gc_host_alloc_numa(size_t bytes, int numa_node, void** ptr, size_t* mapped_bytes);
 int gc_host_free_numa(void* ptr, size_t mapped_bytes);
-/* Cross-process NVLink peer slabs: 64-byte cudaIpcMemHandle_t export/import. */
-int gc_ipc_export(void* d_ptr, uint8_t* handle64);
+/* Synthetic graph targets (generate_synthetic, graph.py:144-177) on the device: edge
+ * e in [first_edge, first_edge + count) gets searchsorted(cdf, u_e, side="right")
+ * with u_e the e-th numpy Generator.random() double of the PCG64 stream whose 128-bit
+ * state/increment the caller passes (Generator.bit_generator.state), self-loops
+ * redirected to (t + 1) % n. d_cdf: the reference's float64 Zipf cdf (host-computed).
+ * Bit-identical to the reference's column array. */
+int gc_synth_zipf_targets(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                          const double* d_cdf, uint64_t num_vertices, uint64_t degree, uint64_t first_edge,
+                          uint64_t count, uint32_t* d_out, void* stream);
+/* Cross-process NVLink peer slabs: 64-byte cudaIpcMemHandle_t of the allocation
+ * holding d_ptr, plus d_ptr's byte offset from that allocation's base (caching
+ * allocators sub-allocate). gc_ipc_import maps the allocation and returns its base;
+ * the peer address of the exported pointer is base + offset. */
+int gc_ipc_export(void* d_ptr, uint8_t* handle64, uint64_t* offset);
 int gc_ipc_import(const uint8_t* handle64, void** d_ptr);
 int gc_ipc_close(void* d_ptr);
 /* Enable peer access from the current device to `peer` (same-process multi-GPU). */

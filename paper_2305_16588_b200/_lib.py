@@ -140,7 +140,8 @@ SIGNATURES = {
     "gc_host_unregister": (ctypes.c_int, [V]),
     "gc_host_alloc_numa": (ctypes.c_int, [SZ, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(SZ)]),
     "gc_host_free_numa": (ctypes.c_int, [V, SZ]),
-    "gc_ipc_export": (ctypes.c_int, [V, ctypes.c_char_p]),
+    "gc_synth_zipf_targets": (ctypes.c_int, [U64, U64, U64, U64, V, U64, U64, U64, U64, V, V]),
+    "gc_ipc_export": (ctypes.c_int, [V, ctypes.c_char_p, ctypes.POINTER(U64)]),
     "gc_ipc_import": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]),
     "gc_ipc_close": (ctypes.c_int, [V]),
     "gc_enable_peer": (ctypes.c_int, [ctypes.c_int]),

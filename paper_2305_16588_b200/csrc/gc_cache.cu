@@ -28,7 +28,7 @@ extern "C" int gc_csr_extract(const gc_csr_t* src, const int64_t* d_ids, int64_t
     GC_REQUIRE(src && src->row_offsets, GC_ERR_VALUE, "gc_csr_extract: source CSR is null");
     if (count <= 0) return GC_OK;
     int64_t g = (count * 32 + 255) / 256;
-    if (g > 148 * 32) g = 148 * 32;
+    if (g > (int64_t)sm_count() * 32) g = (int64_t)sm_count() * 32;
     k_csr_extract<<<(unsigned)g, 256, 0, as_stream(stream)>>>(src->row_offsets, src->col_indices, d_ids, count,
                                                               d_slab_offsets, d_slab_cols);
     GC_CHECK_LAUNCH("gc_csr_extract");

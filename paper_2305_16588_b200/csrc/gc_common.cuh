@@ -120,6 +120,9 @@ __device__ __forceinline__ void mark_visited(uint32_t* bm, uint32_t* sm, uint32_
 }
 
 void set_error(const std::string& msg);
+// streaming multiprocessors of the current device (cudaDevAttrMultiProcessorCount,
+// cached per device; 148 on a B200): grids are sized in multiples of it
+unsigned sm_count();
 void set_defer_ctas(int ctas);  // gc_gather.cu
 void set_gather_ctas_per_sm(int v);  // gc_gather.cu
 int cuda_status(cudaError_t err, const char* what);
@@ -152,8 +155,9 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 // Decoupled look-back for segmented single-pass scans. Tile status words pack a
 // 2-bit flag (1 = aggregate available, 2 = inclusive prefix available) over a
 // 62-bit value; an aligned 64-bit store publishes both atomically, so no fence is
-// needed between value and flag. Tiles are claimed in launch order from a
-// counter, so every predecessor a tile waits on is already resident (no deadlock).
+// needed between value and flag. Callers claim tile ids from an atomic counter
+// (not blockIdx), so every predecessor a tile waits on already belongs to a running
+// or finished CTA whatever order CTAs are dispatched in (no deadlock).
 // ------------------------------------------------------------------------------
 constexpr uint64_t kFlagAgg = 1ull << 62;
 constexpr uint64_t kFlagPre = 2ull << 62;

@@ -95,7 +95,10 @@ __global__ void __launch_bounds__(kUniqThreads) k_unique(UniqueParams p) {
             const uint32_t vbase = (uint32_t)((w0 + k) * 32);
             while (w) {
                 const uint32_t u = vbase + (__ffs(w) - 1);
-                out[pos++] = u;
+                // capacity guard: ucount still reports the true count, so the caller
+                // sees ucount > unique_stride and raises (rows past the cap are dropped)
+                if (pos < p.ustride) out[pos] = u;
+                ++pos;
                 if (p.feat) atomicAdd((unsigned long long*)(p.feat + u), 1ull);
                 w &= w - 1;
             }
@@ -265,7 +268,8 @@ __global__ void __launch_bounds__(kUniqThreads) k_block_emit(SparseParams p) {
                 const uint32_t vbase = (uint32_t)(wik * 32);
                 for (uint32_t w = x[k]; w; w &= w - 1u) {
                     const uint32_t u = vbase + (__ffs(w) - 1);
-                    out[pos++] = u;
+                    if (pos < p.ustride) out[pos] = u;  // capacity guard (see k_unique)
+                    ++pos;
                     if (p.feat) atomicAdd((unsigned long long*)(p.feat + u), 1ull);
                 }
                 if (p.clear) row[wik] = 0u;
@@ -344,7 +348,8 @@ __global__ void k_relabel(const uint32_t* __restrict__ ids, uint64_t stride, con
 __global__ void k_bitmap_clear(uint32_t* bm, uint64_t bwords, uint32_t* sm, uint64_t swords,
                                const uint32_t* __restrict__ uniq, uint64_t ustride, const uint32_t* __restrict__ ucount) {
     const uint32_t b = blockIdx.y;
-    const uint32_t c = ucount[b];
+    // only the first unique_stride ids were written (capacity guard of the compaction)
+    const uint32_t c = (uint64_t)ucount[b] < ustride ? ucount[b] : (uint32_t)ustride;
     uint32_t* row = bm + b * bwords;
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < c; k += gridDim.x * blockDim.x) {
         const uint32_t u = uniq[b * ustride + k];
@@ -433,7 +438,7 @@ int gc_unique_compact(const gc_visited_t* visited, uint32_t num_batches, uint32_
         k_block_lists<<<num_batches, kUniqThreads, 0, s>>>(q);
         GC_CHECK_LAUNCH("gc_unique_compact lists");
         // ~8 CTAs per SM over the whole window
-        unsigned gx = (unsigned)((148u * 8u + num_batches - 1) / num_batches);
+        unsigned gx = (unsigned)((sm_count() * 8u + num_batches - 1) / num_batches);
         if (gx < 1) gx = 1;
         const dim3 grid(gx, num_batches);
         k_block_counts<<<grid, kUniqThreads, 0, s>>>(q);

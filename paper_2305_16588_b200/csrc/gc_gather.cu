@@ -317,8 +317,8 @@ static int gather_impl(const gc_feature_store_t* store, const uint32_t* d_ids, u
     }
     uint64_t work = (uint64_t)max_count * per_row;
     uint64_t gx = (work + 255) / 256;
-    // enough CTAs to fill 148 SMs for the whole window; grid-stride beyond that
-    const uint64_t cap = (uint64_t)148 * 16 / num_batches;
+    // enough CTAs to fill every SM for the whole window; grid-stride beyond that
+    const uint64_t cap = (uint64_t)sm_count() * 16 / num_batches;
     if (gx > cap) gx = cap;
     if (gx < 1) gx = 1;
     dim3 grid((unsigned)gx, num_batches);
@@ -326,7 +326,7 @@ static int gather_impl(const gc_feature_store_t* store, const uint32_t* d_ids, u
         // warp per row, 32-row chunks per warp, 4 rows in flight; ~16 resident warps per
         // SM per batch slice
         uint64_t wx = ((uint64_t)max_count + 32 * 8 - 1) / (32 * 8);
-        uint64_t wcap = (uint64_t)148 * g_gather_ctas_per_sm / num_batches;
+        uint64_t wcap = (uint64_t)sm_count() * g_gather_ctas_per_sm / num_batches;
         if (wcap < 1) wcap = 1;
         if (wx > wcap) wx = wcap;
         if (wx < 1) wx = 1;
@@ -387,7 +387,7 @@ int gc_synth_features(uint64_t first_row, uint64_t rows, uint32_t dim, float* d_
     GC_REQUIRE(dim >= 1, GC_ERR_VALUE, "feature dimension must be >= 1");
     if (rows == 0) return GC_OK;
     uint64_t g = (rows * dim + 255) / 256;
-    if (g > 148 * 64) g = 148 * 64;
+    if (g > (uint64_t)sm_count() * 64) g = (uint64_t)sm_count() * 64;
     k_synth_features<<<(unsigned)g, 256, 0, as_stream(stream)>>>(first_row, rows, dim, d_out);
     GC_CHECK_LAUNCH("gc_synth_features");
     return GC_OK;
@@ -398,7 +398,7 @@ int gc_scatter_add(const uint32_t* d_ids, const uint32_t* d_weights, int64_t cou
     GC_REQUIRE(count >= 0, GC_ERR_VALUE, "gc_scatter_add: count must be >= 0");
     if (count == 0) return GC_OK;
     int64_t g = (count + 255) / 256;
-    if (g > 148 * 32) g = 148 * 32;
+    if (g > (int64_t)sm_count() * 32) g = (int64_t)sm_count() * 32;
     k_scatter_add<<<(unsigned)g, 256, 0, as_stream(stream)>>>(d_ids, d_weights, count, d_counter);
     GC_CHECK_LAUNCH("gc_scatter_add");
     return GC_OK;

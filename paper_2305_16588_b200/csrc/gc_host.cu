@@ -10,6 +10,7 @@
 // link-time dependency on libcuda (it still loads on a CPU-only host).
 #include <cuda.h>
 
+#include <cstring>
 #include <mutex>
 
 #include "gc_common.cuh"
@@ -26,6 +27,7 @@ struct DriverVmm {
     decltype(&cuMemRelease) release = nullptr;
     decltype(&cuMemAddressFree) free_va = nullptr;
     decltype(&cuMemRetainAllocationHandle) retain = nullptr;
+    decltype(&cuMemGetAddressRange) address_range = nullptr;
     bool ok = false;
 };
 
@@ -43,6 +45,7 @@ static DriverVmm& vmm() {
                get("cuMemSetAccess", (void**)&d.access) && get("cuMemUnmap", (void**)&d.unmap) &&
                get("cuMemRelease", (void**)&d.release) && get("cuMemAddressFree", (void**)&d.free_va) &&
                get("cuMemRetainAllocationHandle", (void**)&d.retain);
+        if (!get("cuMemGetAddressRange", (void**)&d.address_range)) d.address_range = nullptr;
     });
     return d;
 }
@@ -111,6 +114,40 @@ int gc_host_alloc_numa(size_t bytes, int numa_node, void** ptr, size_t* mapped_b
     }
     *ptr = reinterpret_cast<void*>(va);
     *mapped_bytes = size;
+    return GC_OK;
+}
+
+// CUDA IPC of cache slabs across the clique's processes. cudaIpcOpenMemHandle maps
+// the whole cudaMalloc allocation and returns its base, while torch's caching
+// allocator sub-allocates tensors inside larger blocks: the exporter therefore also
+// returns the tensor's offset from its allocation base (cuMemGetAddressRange), which
+// the importer adds to the mapped base.
+int gc_ipc_export(void* d_ptr, uint8_t* handle64, uint64_t* offset) {
+    GC_REQUIRE(d_ptr && handle64 && offset, GC_ERR_VALUE, "gc_ipc_export: null argument");
+    DriverVmm& d = vmm();
+    GC_REQUIRE(d.address_range, GC_ERR_UNSUPPORTED, "gc_ipc_export: cuMemGetAddressRange unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (int e = drv(d.address_range(&base, &size, reinterpret_cast<CUdeviceptr>(d_ptr)), "cuMemGetAddressRange"))
+        return e;
+    cudaIpcMemHandle_t h;
+    GC_TRY(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)), "cudaIpcGetMemHandle");
+    static_assert(sizeof(h) == 64, "ipc handle size");
+    memcpy(handle64, &h, 64);
+    *offset = (uint64_t)(reinterpret_cast<CUdeviceptr>(d_ptr) - base);
+    return GC_OK;
+}
+
+int gc_ipc_import(const uint8_t* handle64, void** d_ptr) {
+    GC_REQUIRE(handle64 && d_ptr, GC_ERR_VALUE, "gc_ipc_import: null argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, 64);
+    GC_TRY(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    return GC_OK;
+}
+
+int gc_ipc_close(void* d_ptr) {
+    GC_TRY(cudaIpcCloseMemHandle(d_ptr), "cudaIpcCloseMemHandle");
     return GC_OK;
 }
 

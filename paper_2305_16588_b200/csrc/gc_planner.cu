@@ -16,7 +16,7 @@ namespace gc {
 static unsigned grid1d(int64_t n, int block) {
     int64_t g = (n + block - 1) / block;
     if (g < 1) g = 1;
-    if (g > 148 * 32) g = 148 * 32;
+    if (g > (int64_t)sm_count() * 32) g = (int64_t)sm_count() * 32;
     return (unsigned)g;
 }
 

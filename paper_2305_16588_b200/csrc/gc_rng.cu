@@ -19,10 +19,22 @@ int cuda_status(cudaError_t err, const char* what) {
     return GC_ERR_CUDA;
 }
 
+unsigned sm_count() {
+    static int cached[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    if (cached[dev] == 0) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+        cached[dev] = v;
+    }
+    return (unsigned)cached[dev];
+}
+
 static unsigned grid_for(int64_t n, int block) {
     int64_t g = (n + block - 1) / block;
     if (g < 1) g = 1;
-    if (g > 148 * 64) g = 148 * 64;  // grid-stride beyond 64 CTAs per SM
+    if (g > (int64_t)sm_count() * 64) g = (int64_t)sm_count() * 64;  // grid-stride beyond 64 CTAs per SM
     return (unsigned)g;
 }
 
@@ -207,26 +219,6 @@ int gc_host_register(void* host_ptr, size_t bytes, void** d_alias) {
 
 int gc_host_unregister(void* host_ptr) {
     GC_TRY(cudaHostUnregister(host_ptr), "cudaHostUnregister");
-    return GC_OK;
-}
-
-int gc_ipc_export(void* d_ptr, uint8_t* handle64) {
-    cudaIpcMemHandle_t h;
-    GC_TRY(cudaIpcGetMemHandle(&h, d_ptr), "cudaIpcGetMemHandle");
-    static_assert(sizeof(h) == 64, "ipc handle size");
-    memcpy(handle64, &h, 64);
-    return GC_OK;
-}
-
-int gc_ipc_import(const uint8_t* handle64, void** d_ptr) {
-    cudaIpcMemHandle_t h;
-    memcpy(&h, handle64, 64);
-    GC_TRY(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
-    return GC_OK;
-}
-
-int gc_ipc_close(void* d_ptr) {
-    GC_TRY(cudaIpcCloseMemHandle(d_ptr), "cudaIpcCloseMemHandle");
     return GC_OK;
 }
 

@@ -1,7 +1,7 @@
 // K2 hop_expand: one hop of the reference's L-hop sampler (_expand_frontier,
 // sampling.py:84-117) for a window of W independent mini-batches in one launch.
 //
-// Per CTA tile of up to 256 frontier positions (tile id = blockIdx.x):
+// Per CTA tile of up to 256 frontier positions (tile ids claimed from a counter):
 //   phase 1  thread-per-position: v, row offsets, deg, take = min(deg, fanout);
 //            presampling counters (warp-aggregated), seed marking; CTA scan of take;
 //            the tile aggregate is published for the decoupled look-back.
@@ -89,6 +89,7 @@ struct HopParams {
     uint32_t cls;
     uint32_t u32b;
     uint64_t* tile_state;
+    uint32_t* tile_counter;  // tile ids are claimed from it in dispatch order (zeroed per launch)
     int exact_only;  // test hook: always take the 64-bit extraction path
     uint32_t k32;    // == 32, opaque to the compiler (see PairHashHigh::hi_counter)
 };
@@ -381,13 +382,16 @@ __global__ void __launch_bounds__(kHopThreads, hop_min_blocks<S>()) k_hop_expand
     using Item = typename std::conditional<TIERED, uint64_t, uint32_t>::type;
     __shared__ Item s_items[kItemCap];
     __shared__ uint64_t s_prefix;
+    __shared__ uint32_t s_vid;
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
-    // tile id = blockIdx.x: CTAs are dispatched in increasing index order, so every
-    // predecessor a tile's look-back waits on is resident or done (as in CUB's
-    // single-pass scans)
-    const uint32_t vid = blockIdx.x;
+    // tile id claimed from a counter, not blockIdx.x: a tile only starts after every
+    // lower tile id has been handed to a running CTA, so each predecessor its look-back
+    // waits on is resident or done whatever order the hardware dispatches CTAs in
+    if (tid == 0) s_vid = atomicAdd(p.tile_counter, 1u);
+    __syncthreads();
+    const uint32_t vid = s_vid;
     const uint32_t b = vid / p.tiles_per_batch;
     const uint32_t t = vid % p.tiles_per_batch;
     const uint32_t F = p.fcount[b];
@@ -421,14 +425,16 @@ __global__ void __launch_bounds__(kHopThreads, hop_min_blocks<S>()) k_hop_expand
             }
         }
         take = min(deg, p.fanout);
-        if (p.mark_frontier && p.bitmap)
+        if (p.mark_frontier && p.bitmap && v < p.n)
             mark_visited(p.bitmap + b * p.bwords, p.summary ? p.summary + b * p.swords : nullptr, v);
         // hash_counters(position), position = index in this batch's frontier (rng.py:64-66)
         if (deg > p.fanout) hc = hash_counter(p.hop_keys[b], p0 + tid);
     }
     if (p.topo_reads || p.edge_trav) {
-        unsigned act = __ballot_sync(kFull, valid);
-        if (valid) {
+        // ids outside [0, n) are rejected on the host; never let one index a counter
+        const bool counted = valid && v < p.n;
+        unsigned act = __ballot_sync(kFull, counted);
+        if (counted) {
             // vertex 0 of a Zipf graph fills ~1/5 of a frontier: one atomic per
             // distinct vertex per warp (take depends on v only)
             unsigned peers = __match_any_sync(act, v);
@@ -695,7 +701,8 @@ int gc_hop_expand(const gc_topology_t* topo, const uint32_t* d_frontier, uint64_
     }
     const size_t state_bytes = align_up((size_t)num_batches * tiles * sizeof(uint64_t), 256);
     p.tile_state = static_cast<uint64_t*>(d_temp);
-    GC_TRY(cudaMemsetAsync(d_temp, 0, state_bytes, s), "gc_hop_expand memset");
+    p.tile_counter = reinterpret_cast<uint32_t*>(static_cast<char*>(d_temp) + state_bytes);
+    GC_TRY(cudaMemsetAsync(d_temp, 0, state_bytes + 256, s), "gc_hop_expand memset");
     const uint64_t grid = (uint64_t)num_batches * tiles;
     GC_REQUIRE(grid < (1ull << 31), GC_ERR_VALUE, "gc_hop_expand: window too large");
     // the plain-CSR kernel stages 32-bit edge indices; a CSR with 2^32 or more edges

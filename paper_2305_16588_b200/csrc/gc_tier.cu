@@ -110,7 +110,7 @@ int gc_mark_holders(const int64_t* d_ids, int64_t count, uint32_t local_gpu, uin
     GC_REQUIRE(((uintptr_t)d_holders & 3) == 0, GC_ERR_VALUE, "gc_mark_holders: holders must be 4-byte aligned");
     if (count <= 0) return GC_OK;
     int64_t g = (count + 255) / 256;
-    if (g > 148 * 32) g = 148 * 32;
+    if (g > (int64_t)sm_count() * 32) g = (int64_t)sm_count() * 32;
     k_mark_holders<<<(unsigned)g, 256, 0, as_stream(stream)>>>(d_ids, count, (uint8_t)(1u << local_gpu), d_holders);
     GC_CHECK_LAUNCH("gc_mark_holders");
     return GC_OK;
@@ -129,7 +129,7 @@ int gc_tier_account(const uint64_t* d_row_offsets, int64_t n, const uint64_t* d_
     TierParams p{d_row_offsets, n, d_topo_reads, d_feat_lookups, d_topo_holders, d_feat_holders, local_gpu,
                  clique_size, cache_line_bytes, uint32_bytes, row_txns, reinterpret_cast<unsigned long long*>(d_out)};
     int64_t g = (n + 255) / 256;
-    if (g > 148 * 8) g = 148 * 8;
+    if (g > (int64_t)sm_count() * 8) g = (int64_t)sm_count() * 8;
     k_tier_account<<<(unsigned)g, 256, 0, s>>>(p);
     GC_CHECK_LAUNCH("gc_tier_account");
     return GC_OK;

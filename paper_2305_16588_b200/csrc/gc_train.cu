@@ -53,7 +53,7 @@ int gc_segment_mean_gather(const float* d_x, int dim, const int64_t* d_idx, cons
     GC_REQUIRE(dim >= 1 && segs >= 0, GC_ERR_VALUE, "gc_segment_mean_gather: bad sizes");
     if (segs == 0) return GC_OK;
     int64_t g = (segs + 7) / 8;
-    if (g > 148 * 64) g = 148 * 64;
+    if (g > (int64_t)sm_count() * 64) g = (int64_t)sm_count() * 64;
     const bool vec4 = dim % 4 == 0 && (uintptr_t)d_x % 16 == 0 && (uintptr_t)d_out % 16 == 0;
     if (vec4)
         k_segment_mean_gather<true><<<(unsigned)g, 256, 0, as_stream(stream)>>>(d_x, dim, d_idx, d_offsets, segs, d_out);

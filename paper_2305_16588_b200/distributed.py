@@ -65,12 +65,16 @@ def candidate_orders_from_rows(topo_row: torch.Tensor, feat_row: torch.Tensor, l
 
 
 def ipc_export(t: torch.Tensor) -> bytes:
-    """64-byte CUDA IPC handle of the allocation holding tensor t, plus its offset."""
+    """64-byte CUDA IPC handle of the cudaMalloc allocation holding tensor t, plus t's
+    byte offset from that allocation's base (torch's caching allocator places many
+    tensors inside one allocation; cudaIpcOpenMemHandle maps the allocation base)."""
+    import ctypes
+
     lib = _lib.lib()
-    base = t.untyped_storage().data_ptr()
     buf = ctypes_buffer()
-    _lib.check(lib.gc_ipc_export(base, buf), "ipc_export")
-    return bytes(buf.raw[:64]) + int(t.data_ptr() - base).to_bytes(8, "little")
+    off = ctypes.c_uint64(0)
+    _lib.check(lib.gc_ipc_export(t.data_ptr(), buf, ctypes.byref(off)), "ipc_export")
+    return bytes(buf.raw[:64]) + int(off.value).to_bytes(8, "little")
 
 
 def ipc_import(blob: bytes) -> int:

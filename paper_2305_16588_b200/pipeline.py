@@ -21,7 +21,7 @@ from . import _lib
 from .cache import FeatureStore
 from .graph import CsrGraph
 from .rng import ROLE_SHUFFLE, KeyedRng
-from .sampling import DeviceHotness, SamplingConfig, WindowSampler, batch_hop_keys
+from .sampling import DeviceHotness, SamplingConfig, WindowSampler, batch_hop_keys, check_seed_pool
 
 # kernels each stage launches (for the bench's gpu_launches count): CUB's onesweep
 # radix sort of the keys' high 32 bits is 1 histogram + 1 scan + 4 digit passes, plus keys, ties, emit
@@ -105,8 +105,10 @@ class SampleGatherPipeline:
         self.host_stream = torch.cuda.Stream(priority=-1) if self.defer_host and lanes > 1 else None
         self.sampler = self.lane_samplers[0]
         self.features = self.lane_features[0]
-        # relabel overlaps the gather on a side stream (None: run them back to back)
-        self._relabel_side = torch.cuda.Stream() if overlap_relabel else None
+        # relabel overlaps the gather on a side stream per lane (None: back to back), so
+        # one lane's relabel never queues behind another lane's compaction
+        self._relabel_sides = [torch.cuda.Stream() for _ in range(lanes)] if overlap_relabel else None
+        self._lane = 0
         self.feat_cap = self.sampler.ucap
         self.timer: StageTimer | None = None
         self.launches = 0
@@ -119,6 +121,7 @@ class SampleGatherPipeline:
     # ------------------------------------------------------------------ host prep
     def plan_epoch(self, pool, gpu_stream: KeyedRng) -> EpochPlan:
         B = self.cfg.batch_size
+        check_seed_pool(pool, self.graph.num_vertices)
         pool_dev = pool if isinstance(pool, torch.Tensor) else torch.from_numpy(np.asarray(pool, np.int64)).cuda()
         L = pool_dev.numel()
         nb = math.ceil(L / B)
@@ -158,6 +161,7 @@ class SampleGatherPipeline:
                 st.wait_event(ready)
         for i, w0 in enumerate(range(0, plan.num_batches, self.window)):
             lane = i % self.lanes
+            self._lane = lane
             self.sampler = self.lane_samplers[lane]
             self.features = self.lane_features[lane]
             if self.lane_streams:
@@ -220,7 +224,8 @@ class SampleGatherPipeline:
         end = self._stage("unique_relabel")
         # relabel and gather both only need the compaction: with the side stream the two
         # HBM-bound passes share the GPU instead of running back to back
-        side = self._relabel_side if (self.store is not None and self.timer is None) else None
+        side = self._relabel_sides[self._lane] if (self._relabel_sides and self.store is not None
+                                                   and self.timer is None) else None
         sp.dedup(hot, relabel_stream=side)
         # compaction: tile counts, scan, emit (+ block lists when sparse); one relabel per level
         self.launches += (4 if sp.summary is not None else 3) + (H + 1 if sp.relabel else 0)
@@ -240,6 +245,11 @@ class SampleGatherPipeline:
         if on_window is not None:
             on_window(self, w0, nb)
 
+    def check_capacity(self, reset: bool = False) -> int:
+        """Raise OverflowError if any batch since the last reset had more distinct
+        vertices than feat_rows_cap (its rows would have been truncated); one sync."""
+        return max(sp.check_capacity(reset) for sp in self.lane_samplers)
+
     # ------------------------------------------------------------------ host delivery
     def window_to_host(self, nb: int, staging: dict | None = None) -> dict:
         """The last window's results in pinned host memory, packed batch after batch.
@@ -258,6 +268,9 @@ class SampleGatherPipeline:
         sp = self.sampler
         counts = sp.counts[:, :nb].cpu().numpy().astype(np.int64)
         ucount = sp.ucount[:nb].cpu().numpy().astype(np.int64)
+        if nb and int(ucount.max()) > sp.ucap:
+            raise OverflowError(f"a batch has {int(ucount.max())} distinct vertices but the unique/gather "
+                                f"capacity is {sp.ucap}: raise feat_rows_cap")
         st = {} if staging is None else staging
         main = torch.cuda.current_stream()
         copy = st.get("_copy_stream")

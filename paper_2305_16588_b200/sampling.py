@@ -194,6 +194,10 @@ class WindowSampler:
         self.visited = _lib.GcVisited(self.bitmap.data_ptr(), self.words, _lib.ptr(self.summary), self.swords)
         bound = min(self.n, sum(caps))
         self.ucap = max(1, bound if unique_cap is None else min(bound, int(unique_cap)))
+        # capped unique buffers can overflow: the compaction writes at most ucap ids and
+        # still reports the true count, whose running maximum is kept on the device
+        # (no sync per window) and checked by check_capacity()
+        self.peak_ucount = torch.zeros((), dtype=i32, device=dev) if self.ucap < bound else None
         self.unique = torch.empty((W, self.ucap), dtype=i32, device=dev)
         self.ucount = torch.zeros(W, dtype=i32, device=dev)
         # relabel rank table: {exclusive popcount prefix, bitmap word} per word
@@ -264,6 +268,9 @@ class WindowSampler:
             ),
             "unique_compact",
         )
+        if self.peak_ucount is not None and self.active:
+            with torch.cuda.stream(stream) if stream is not None else _nullcontext():
+                torch.maximum(self.peak_ucount, self.ucount[: self.active].amax(), out=self.peak_ucount)
         if self.relabel:
             if relabel_stream is not None:
                 ready = torch.cuda.Event()
@@ -279,6 +286,20 @@ class WindowSampler:
                                         self.rank.data_ptr(), self.words, loc.data_ptr(), s),
                     "relabel",
                 )
+
+    def check_capacity(self, reset: bool = False) -> int:
+        """Largest distinct count of any batch since the last reset (one sync); raises
+        OverflowError when it exceeded the unique-row capacity, i.e. some batch's
+        distinct ids (and gathered rows) were truncated."""
+        if self.peak_ucount is None:
+            return -1
+        peak = int(self.peak_ucount.item())
+        if reset:
+            self.peak_ucount.zero_()
+        if peak > self.ucap:
+            raise OverflowError(f"a batch has {peak} distinct vertices but the unique/gather capacity is "
+                                f"{self.ucap}: raise feat_rows_cap")
+        return peak
 
     def run(self, hot: DeviceHotness | None = None, stream=None) -> None:
         self.expand(hot, stream)
@@ -304,6 +325,32 @@ class WindowSampler:
         u = int(self.ucount[b].item())
         object.__setattr__(out, "_distinct", self.unique[b, :u].cpu().numpy().view(np.uint32).astype(np.int64))
         return out
+
+
+class _nullcontext:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
+def check_seed_pool(pool, num_vertices: int) -> None:
+    """sample_batch's seed check (sampling.py:128-131) for a whole pool: ValueError
+    before any id reaches a kernel (numpy pools on the host; device pools with one
+    min/max reduction)."""
+    if isinstance(pool, torch.Tensor):
+        if pool.numel() == 0:
+            return
+        lo, hi = torch.aminmax(pool)
+        lo, hi = int(lo.item()), int(hi.item())
+    else:
+        arr = np.asarray(pool)
+        if arr.size == 0:
+            return
+        lo, hi = int(arr.min()), int(arr.max())
+    if lo < 0 or hi >= num_vertices:
+        raise ValueError("invalid seed vertex id")
 
 
 def device_unique(ids: np.ndarray, n: int) -> np.ndarray:
@@ -448,6 +495,7 @@ class EpochRunner:
     def run(self, pool: np.ndarray, gpu_stream: KeyedRng, hot: DeviceHotness) -> int:
         B = self.cfg.batch_size
         L = len(pool)
+        check_seed_pool(pool, self.graph.num_vertices)
         pool_np = np.ascontiguousarray(pool, dtype=np.int64)
         if not pool_np.flags.writeable:  # read-only pools (reference dataclasses) — torch needs a writable view
             pool_np = pool_np.copy()

@@ -182,6 +182,9 @@ def train_epoch(pipe, plan, model: GraphSAGE, opt, labels: torch.Tensor, max_bat
     def consume(p, w0, nbw):
         counts = p.sampler.counts[:, :nbw].cpu().numpy()  # one sync per window for the sizes
         ucount = p.sampler.ucount[:nbw].cpu().numpy()
+        if nbw and int(ucount.max()) > p.sampler.ucap:
+            raise OverflowError(f"a batch has {int(ucount.max())} distinct vertices but the gather capacity "
+                                f"is {p.sampler.ucap}: raise feat_rows_cap")
         for b in range(nbw):
             if max_batches is not None and len(losses) >= max_batches:
                 return

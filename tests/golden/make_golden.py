@@ -339,7 +339,43 @@ def report_vectors():
     np.savez_compressed(OUT / "reports.npz", **d)
 
 
+def format_vectors():
+    """Files the reference itself writes: an LGCSR1 graph (save_csr, graph.py:112-117)
+    and the u32 hotness dump of a 2-clique presampling (write_hotness,
+    sampling.py:292-303), stored byte for byte, plus what load_csr/read_hotness return."""
+    import tempfile
+
+    from gnncache.graph import load_csr, save_csr
+    from gnncache.sampling import read_hotness, write_hotness
+
+    g = generate_synthetic(600, 7, 1.1, seed=21)
+    train = select_training_set(g, 0.2, seed=5)
+    layout = block_layout(4, 2)
+    spec = HardwareSpec(layout, clique_budget_bytes=10_000)
+    tablets = split_intra_clique(train, Partitioning(np.array([v % 2 for v in range(600)]), 2), layout)
+    cfg = SamplingConfig(fanouts=(5, 3), batch_size=16, presample_epochs=2, seed=17)
+    hot = run_presampling(g, tablets, layout, cfg, spec)
+    d = {"graph_ro": g.row_offsets, "graph_ci": g.col_indices}
+    with tempfile.TemporaryDirectory() as tmp:
+        save_csr(g, Path(tmp) / "g.lgcsr")
+        write_hotness(Path(tmp) / "h.bin", hot)
+        d["lgcsr1_bytes"] = np.frombuffer((Path(tmp) / "g.lgcsr").read_bytes(), dtype=np.uint8)
+        d["hotness_bytes"] = np.frombuffer((Path(tmp) / "h.bin").read_bytes(), dtype=np.uint8)
+        back = read_hotness(Path(tmp) / "h.bin")
+        assert np.array_equal(load_csr(Path(tmp) / "g.lgcsr").col_indices, g.col_indices)
+    for ci, h in enumerate(back):
+        d[f"hot{ci}_topo"] = h.topo_hotness
+        d[f"hot{ci}_feat"] = h.feat_hotness
+        d[f"hot{ci}_txn"] = np.array([h.sampling_txn_total], dtype=np.int64)
+        d[f"hot{ci}_id"] = np.array([h.clique_id], dtype=np.int64)
+    d["num_cliques"] = np.array([len(back)])
+    np.savez_compressed(OUT / "formats.npz", **d)
+
+
 if __name__ == "__main__":
+    if "--formats" in sys.argv:
+        format_vectors()
+        raise SystemExit(0)
     if "--reports" in sys.argv:
         report_vectors()
         raise SystemExit(0)
@@ -364,5 +400,6 @@ if __name__ == "__main__":
     hardware_vectors()
     sweep_vectors()
     report_vectors()
+    format_vectors()
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)
