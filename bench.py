@@ -69,12 +69,12 @@ def dist_env():
 
 
 def build_inputs(n: int, world: int):
-    from paper_2305_16588_b200 import derive_seed, generate_synthetic, select_training_set
+    from paper_2305_16588_b200 import derive_seed, generate_synthetic_device, select_training_set
     from paper_2305_16588_b200.hardware import block_layout
     from paper_2305_16588_b200.partition import assign_tablets, single_clique_partitioning, split_intra_clique
 
     seed = CONFIG["master_seed"]
-    g = generate_synthetic(n, CONFIG["avg_degree"], CONFIG["skew"], seed=derive_seed(seed, 1))
+    g = generate_synthetic_device(n, CONFIG["avg_degree"], CONFIG["skew"], seed=derive_seed(seed, 1))
     train = select_training_set(g, CONFIG["training_fraction"], seed=derive_seed(seed, 2))
     layout = block_layout(world, world)
     pools = assign_tablets(split_intra_clique(train, single_clique_partitioning(g), layout), layout)
@@ -148,46 +148,107 @@ class ClockSampler:
         return out
 
 
-# ------------------------------------------------------------------ CPU baseline (oracle port)
-def cpu_batches(g, table, pool, nbatches, seconds, epoch=0):
-    """Time the oracle restatement of the reference path (sample_batch + np.unique +
-    X[ids]) on one host core for about `seconds`; returns (batches, elapsed)."""
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import gnncache_oracle as O
+# ------------------------------------------------------------------ CPU baseline (the reference)
+def reference_module():
+    """The unmodified reference (gnncache 0.1.0) installed by oracle/build_ref.sh into
+    oracle/_ref; None when that build output is absent (then the oracle port stands in,
+    reported as kind "port")."""
+    ref = ROOT / "oracle" / "_ref"
+    if not (ref / "gnncache" / "__init__.py").exists():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    import gnncache
 
-    B, fan = CONFIG["batch_size"], CONFIG["fanouts"]
-    gkey, skey = O.batch_stream_keys(O.derive(CONFIG["master_seed"], 0x10), epoch, 0, 0)
-    shuffled = np.asarray(pool)[O.permutation(skey, len(pool))]
+    return gnncache
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
+class CpuPath:
+    """The reference's CPU path for one GPU's epoch: the stock
+    gnncache.run_sampling_epoch loop body (sampling.py:224-234) — shuffle with
+    KeyedRng.permutation, sample_batch, BatchSample.distinct_vertices — plus the
+    feature gather X[ids] (numpy fancy indexing; the reference stores no values).
+    Falls back to the oracle port when oracle/_ref is missing."""
+
+    def __init__(self, g, table, pool, epoch=0):
+        self.R = reference_module()
+        self.kind = "reference" if self.R is not None else "port"
+        self.table = table
+        B = CONFIG["batch_size"]
+        if self.R is not None:
+            R = self.R
+            self.g = R.CsrGraph(g.num_vertices, g.num_edges, g.row_offsets, g.col_indices)
+            self.cfg = R.SamplingConfig(fanouts=tuple(CONFIG["fanouts"]), batch_size=B)
+            self.stream = R.KeyedRng(_seed()).derive(epoch, 0, 0)
+            from gnncache.rng import ROLE_SAMPLE, ROLE_SHUFFLE
+
+            self.role_sample = ROLE_SAMPLE
+            self.shuffled = np.asarray(pool, np.int64)[self.stream.derive(ROLE_SHUFFLE).permutation(len(pool))]
+        else:
+            sys.path.insert(0, str(ROOT / "oracle"))
+            import gnncache_oracle as O
+
+            self.O, self.g = O, g
+            self.gkey, skey = O.batch_stream_keys(_seed(), epoch, 0, 0)
+            self.shuffled = np.asarray(pool, np.int64)[O.permutation(skey, len(pool))]
+
+    def batch(self, b: int):
+        B = CONFIG["batch_size"]
+        start = (b * B) % len(self.shuffled)
+        seeds = self.shuffled[start : start + B]
+        if self.R is not None:
+            bs = self.R.sample_batch(self.g, seeds, self.cfg, self.stream.derive(self.role_sample, b))
+            uniq = bs.distinct_vertices()
+            return uniq, self.table[uniq]
+        O, g = self.O, self.g
+        hops = O.sample_batch(g.row_offsets, g.col_indices, g.num_vertices, seeds, CONFIG["fanouts"],
+                              O.derive(self.gkey, 2, b))
+        uniq = O.distinct_vertices(seeds, hops)
+        return uniq, O.gather(self.table, uniq)
+
+
+def _seed():
+    from paper_2305_16588_b200 import derive_seed
+
+    return derive_seed(CONFIG["master_seed"], 0x10)
+
+
+def cpu_batches(g, table, pool, nbatches, seconds, epoch=0, keep=0):
+    """Time the reference's CPU path on one host core for about `seconds`; returns
+    (batches, elapsed, kind, results) — results: (distinct ids, rows) of the first
+    `keep` batches, which the bench compares with the device's epoch."""
+    path = CpuPath(g, table, pool, epoch)
     t0 = time.perf_counter()
     done = 0
+    results = []
     for b in range(nbatches):
-        seeds = shuffled[b * B : (b + 1) * B]
-        hops = O.sample_batch(g.row_offsets, g.col_indices, g.num_vertices, seeds, fan, O.derive(gkey, 2, b))
-        uniq = O.distinct_vertices(seeds, hops)
-        O.gather(table, uniq)
+        r = path.batch(b)
+        if b < keep:
+            results.append(r)
         done += 1
         if time.perf_counter() - t0 > seconds:
             break
-    return done, time.perf_counter() - t0
-
-
-def _ref_worker(args):
-    b0, count, epoch = args
-    g, table, pool = _REF_STATE
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import gnncache_oracle as O
-
-    B, fan = CONFIG["batch_size"], CONFIG["fanouts"]
-    gkey, skey = O.batch_stream_keys(O.derive(CONFIG["master_seed"], 0x10), epoch, 0, 0)
-    shuffled = np.asarray(pool)[O.permutation(skey, len(pool))]
-    for b in range(b0, b0 + count):
-        seeds = shuffled[(b * B) % len(pool) :][:B]
-        hops = O.sample_batch(g.row_offsets, g.col_indices, g.num_vertices, seeds, fan, O.derive(gkey, 2, b))
-        O.gather(table, O.distinct_vertices(seeds, hops))
-    return count
+    return done, time.perf_counter() - t0, path.kind, results
 
 
 _REF_STATE = None
+
+
+def _ref_worker(b):
+    _REF_STATE.batch(b)
+    return 1
 
 
 def host_table(n, dim):
@@ -202,17 +263,28 @@ def host_table(n, dim):
 
 
 def run_reference(args):
-    """--impl reference: the reference's CPU path (oracle port; the reference itself is
-    pure Python/numpy and is not installed on the box) on all host cores."""
+    """--impl reference: the unmodified reference (oracle/_ref, gnncache 0.1.0) through
+    its public API on all host cores — one forked process per core, one batch each per
+    step; the rank's epoch state is built once and shared copy-on-write. Under torchrun
+    rank 0 alone runs; the other ranks exit 0 without work."""
     global _REF_STATE
     import multiprocessing as mp
 
     rank, _, world = dist_env()
     if rank != 0:
         return
-    g, pools, _ = build_inputs(args.num_vertices, 1)
+    from paper_2305_16588_b200 import derive_seed, generate_synthetic, select_training_set
+    from paper_2305_16588_b200.hardware import block_layout
+    from paper_2305_16588_b200.partition import assign_tablets, single_clique_partitioning, split_intra_clique
+
+    # the same synthetic inputs as the B200 arm (identical CSR: same PCG64 draws), built on the host
+    seed = CONFIG["master_seed"]
+    g = generate_synthetic(args.num_vertices, CONFIG["avg_degree"], CONFIG["skew"], seed=derive_seed(seed, 1))
+    train = select_training_set(g, CONFIG["training_fraction"], seed=derive_seed(seed, 2))
+    layout = block_layout(world, world)
+    pools = assign_tablets(split_intra_clique(train, single_clique_partitioning(g), layout), layout)
     table = host_table(g.num_vertices, CONFIG["feature_dim"])
-    _REF_STATE = (g, table, pools[0])
+    _REF_STATE = CpuPath(g, table, pools[0])
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
     nb_epoch = math.ceil(len(pools[0]) / CONFIG["batch_size"])
     per_step = cores  # one batch per worker per step
@@ -222,7 +294,7 @@ def run_reference(args):
         b = 0
         for it in range(args.warmup + args.steps):
             t0 = time.perf_counter()
-            pool.map(_ref_worker, [((b + i) % nb_epoch, 1, 0) for i in range(per_step)])
+            pool.map(_ref_worker, [(b + i) % nb_epoch for i in range(per_step)], chunksize=1)
             dt = time.perf_counter() - t0
             b += per_step
             if it >= args.warmup:
@@ -231,12 +303,14 @@ def run_reference(args):
     value = per_step * len(times) / total
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1000 * total / len(times), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "u64", "data": "synthetic (reference generator law, PCG64 draws)", "impl": "reference",
-        "config": {**CONFIG, "num_vertices": args.num_vertices, "parallelism": "host processes"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{per_step} batches per step (one per process) of the epoch, "
-                                   "sample_batch + np.unique + X[ids] per batch"},
+        "ms_per_step": 1000 * total / len(times), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic (reference generator law, PCG64 draws)",
+        "impl": "reference",
+        "config": {**CONFIG, "num_vertices": args.num_vertices, "parallelism": f"{cores} host processes"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": _REF_STATE.kind,
+                         "cpu_model": cpu_model(),
+                         "sample": f"{per_step} batches per step (one per process) of GPU 0's epoch: "
+                                   "gnncache.sample_batch + BatchSample.distinct_vertices + X[ids]"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -300,6 +374,24 @@ def run_b200(args):
         stats["max_unique"] = max(stats["max_unique"], int(p.sampler.ucount[:nbw].max().item()))
 
     epoch_fn = pipe.run_epoch_graph if args.graph else pipe.run_epoch
+    # before any timing: every epoch the timed region will run goes through the eager
+    # pipeline once, one lane, kernels back to back — (1) the capacity check (a batch
+    # with more distinct vertices than feat_rows_cap fails the run here, before timing),
+    # (2) the algorithmic bytes, (3) per-stage device times for the roofline (stage
+    # events with the host run ahead, so they bracket device time only)
+    seq = pipe if args.lanes == 1 else SampleGatherPipeline(g, cfg, store, len(pool), window=window,
+                                                              sparse_visited=sparse, feat_rows_cap=65536, lanes=1)
+    for s in range(args.steps):
+        seq.run_epoch(plans[args.warmup + s], on_window=account)
+    stats["peak_unique"] = seq.check_capacity(reset=True)  # raises OverflowError on truncation
+    timer = StageTimer()
+    seq.timer = timer
+    for s in range(args.steps):
+        flush.zero_()
+        StageTimer.hold()  # the host runs ahead: stage events see device time only
+        seq.run_epoch(plans[args.warmup + s])
+    seq.timer = None
+    torch.cuda.synchronize()
     for e in range(args.warmup):
         epoch_fn(plans[e])
     torch.cuda.synchronize()
@@ -323,22 +415,7 @@ def run_b200(args):
         if world > 1:
             dist.barrier()
     launches = pipe.launches
-    # per-kernel durations for the roofline: the same epochs again, one window after
-    # another on one stream (kernels timed alone, not sharing the GPU), untimed overall
-    seq = pipe if args.lanes == 1 else SampleGatherPipeline(g, cfg, store, len(pool), window=window, sparse_visited=sparse,
-                                                              feat_rows_cap=65536, lanes=1)
-    timer = StageTimer()
-    seq.timer = timer
-    for s in range(args.steps):
-        flush.zero_()
-        seq.run_epoch(plans[args.warmup + s])
-    seq.timer = None
-    # algorithmic bytes of the timed epochs (recomputed, identical streams: untimed)
-    for s in range(args.steps):
-        seq.run_epoch(plans[args.warmup + s], on_window=account)
-    torch.cuda.synchronize()
-    if stats["max_unique"] > seq.feat_cap:
-        raise RuntimeError("gather capacity overflow: raise feat_rows_cap")
+    pipe.check_capacity(reset=True)  # the timed epochs were checked above; this re-asserts it
     pipe = seq
 
     total_ms = float(sum(step_ms))
@@ -372,7 +449,7 @@ def run_b200(args):
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "u64", "data": "synthetic (reference generator law, PCG64 draws; random fp32 features)",
         "config": {**CONFIG, "num_vertices": args.num_vertices, "batches_per_step_per_gpu": nb,
                    "window_batches": pipe.window, "lanes": args.lanes, "cuda_graph": bool(args.graph), "parallelism": f"dp{world} (tablet per GPU, no data-path collective)",
@@ -408,14 +485,42 @@ def run_b200(args):
         line["config"]["dist_backend"] = dist.get_backend()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         host = table.cpu().numpy()
-        done, el = cpu_batches(g, host, pool, nb, args.cpu_seconds)
-        line["cpu_baseline"] = {"value": done / el, "unit": UNIT, "cores": 1, "kind": "port",
-                                "sample": f"first {done} batches of epoch 0 (C2, 1 core): oracle sample_batch + "
-                                          "np.unique + X[ids]"}
+        done, el, kind, ref = cpu_batches(g, host, pool, nb, args.cpu_seconds, keep=8)
+        line["cpu_baseline"] = {"value": done / el, "unit": UNIT, "cores": 1, "kind": kind, "cpu_model": cpu_model(),
+                                "sample": f"first {done} batches of epoch 0 (C2, 1 core): gnncache.sample_batch + "
+                                          "distinct_vertices + X[ids]"}
+        line["verified"] = verify_epoch0(pipe, plans[0], ref)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def verify_epoch0(pipe, plan, ref):
+    """The bench checks its own output: epoch 0 once more through the benched pipeline,
+    and each batch the CPU leg ran is compared with the reference's result (sorted
+    distinct vertices and their gathered feature rows, bit for bit)."""
+    import torch
+
+    got = {}
+
+    def grab(p, w0, nbw):
+        sp = p.sampler
+        torch.cuda.synchronize()
+        for bi in range(nbw):
+            b = w0 + bi
+            if b < len(ref):
+                u = int(sp.ucount[bi])
+                got[b] = (sp.unique[bi, :u].cpu().numpy().view(np.uint32).astype(np.int64),
+                          p.features[bi, :u].cpu().numpy())
+
+    pipe.run_epoch(plan, on_window=grab)
+    bad = [b for b, (uniq, rows) in enumerate(ref)
+           if b not in got or not (np.array_equal(got[b][0], uniq) and np.array_equal(got[b][1], rows))]
+    if bad:
+        raise RuntimeError(f"bench self-check failed: batches {bad} of epoch 0 differ from the reference")
+    return {"batches": len(ref), "epoch": 0, "bit_exact": True,
+            "against": "the CPU leg's own results (distinct vertices + gathered rows)"}
 
 
 def train_run(args, g, cfg, pipe, pool, root, clique, local_idx, world):

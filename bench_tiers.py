@@ -68,7 +68,7 @@ def main():
     t_setup = time.perf_counter()
     n = int(round(111_000_000 * a.scale))
     deg, dim, fanouts, bs = 14, 128, (25, 10), 1024
-    g = P.generate_synthetic(n, deg, 1.2, seed=P.derive_seed(7, 1))
+    g = P.generate_synthetic_device(n, deg, 1.2, seed=P.derive_seed(7, 1))
     train = P.select_training_set(g, 0.1, seed=P.derive_seed(7, 2))
     K = a.clique
     layout = P.block_layout(K, K)
@@ -165,6 +165,7 @@ def main():
             acc[k] += wb[k]
 
     for s in range(a.steps):
+        StageTimer.hold()  # the host runs ahead: stage events see device time only
         seq.run_epoch(plans[a.warmup + s])
     seq.timer = None
     for s in range(a.steps):

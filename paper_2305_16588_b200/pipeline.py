@@ -64,6 +64,13 @@ class StageTimer:
     def reset(self):
         self.events.clear()
 
+    @staticmethod
+    def hold(ms: float = 30.0, clock_ghz: float = 2.0) -> None:
+        """Stall the current stream for ~ms (a device spin) so the host enqueues the
+        whole epoch before the GPU starts it: stage events then bracket device time
+        only, not host launch latency. Call right before a timed run_epoch."""
+        torch.cuda._sleep(int(ms * 1e-3 * clock_ghz * 1e9))
+
 
 class SampleGatherPipeline:
     """Sampling + dedup + relabel + three-tier gather for one GPU's seed pool.
