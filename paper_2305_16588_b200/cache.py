@@ -48,7 +48,6 @@ class TopologyStore:
             raise ValueError("self_rank must index the clique (at most 8 GPUs)")
         self.full = graph.device("host" if host_full else "hbm")
         loc = np.full(n, _lib.GC_TIER_HOST, dtype=np.uint32)
-        deg = graph.out_degrees
         self.slabs: list = []
         for g, verts in enumerate(topo_vertices):
             verts = np.asarray(verts, dtype=np.int64)
@@ -57,17 +56,10 @@ class TopologyStore:
             if len(verts) and (loc[verts] != _lib.GC_TIER_HOST).any():
                 raise ValueError("a vertex's topology is cached on two GPUs; the clique cache is partitioned")
             loc[verts] = (np.uint32(g) << np.uint32(28)) | np.arange(len(verts), dtype=np.uint32)
-            if peer_slabs is not None and g != self_rank:
-                self.slabs.append(peer_slabs[g])
+            if peer_slabs is not None and (g != self_rank or peer_slabs[g] is not None):
+                self.slabs.append(peer_slabs[g])  # mapped peer slab, or this GPU's prebuilt one
                 continue
-            offs = np.zeros(len(verts) + 1, dtype=np.uint64)
-            np.cumsum(deg[verts], out=offs[1:])
-            d_offs = torch.from_numpy(offs.view(np.int64)).cuda()
-            d_cols = torch.empty(max(int(offs[-1]), 1), dtype=torch.int32, device="cuda")
-            d_ids = torch.from_numpy(verts).cuda()
-            _lib.check(lib.gc_csr_extract(self.full.c_struct, d_ids.data_ptr(), len(verts), d_offs.data_ptr(),
-                                          d_cols.data_ptr(), _lib.stream_handle()), "csr_extract")
-            self.slabs.append((d_offs, d_cols))
+            self.slabs.append(self.build_slab(graph, verts, host_full))
         self.location = torch.from_numpy(loc.view(np.int32)).cuda()
         self.tier_reads = torch.zeros(7, dtype=torch.int64, device="cuda")
         t = _lib.GcTopology()
@@ -82,6 +74,22 @@ class TopologyStore:
         t.tier_reads = self.tier_reads.data_ptr()
         self.c_struct = t
         self.self_rank = self_rank
+
+    @staticmethod
+    def build_slab(graph: CsrGraph, verts: np.ndarray, host_full: bool = True) -> tuple:
+        """This GPU's compact CSR of the lists in `verts` (priority order), filled on the
+        device by K8 from the full CSR (pinned host or HBM): (offsets u64 as int64
+        [len+1], cols int32 [max(1, edges)])."""
+        verts = np.asarray(verts, dtype=np.int64)
+        full = graph.device("host" if host_full else "hbm")
+        offs = np.zeros(len(verts) + 1, dtype=np.uint64)
+        np.cumsum(graph.out_degrees[verts], out=offs[1:])
+        d_offs = torch.from_numpy(offs.view(np.int64)).cuda()
+        d_cols = torch.empty(max(int(offs[-1]), 1), dtype=torch.int32, device="cuda")
+        d_ids = torch.from_numpy(verts).cuda()
+        _lib.check(_lib.lib().gc_csr_extract(full.c_struct, d_ids.data_ptr(), len(verts), d_offs.data_ptr(),
+                                             d_cols.data_ptr(), _lib.stream_handle()), "csr_extract")
+        return d_offs, d_cols
 
     def tier_counts(self) -> dict:
         v = self.tier_reads.cpu().numpy()
@@ -162,13 +170,33 @@ class FeatureStore:
         pinned = host.contiguous().pin_memory() if not host.is_pinned() else host
         slabs: list = []
         for g, verts in enumerate(feat_vertices):
-            if peer_slabs is not None and g != self_rank:
-                slabs.append(int(peer_slabs[g]))
+            if peer_slabs is not None and (g != self_rank or peer_slabs[g] is not None):
+                slab = peer_slabs[g]  # mapped peer slab (address), or this GPU's prebuilt one
+                slabs.append(slab if isinstance(slab, torch.Tensor) else int(slab))
                 continue
-            idx = torch.from_numpy(np.asarray(verts, dtype=np.int64))
-            slabs.append(pinned.index_select(0, idx).cuda() if len(idx) else torch.empty((0, dim), device="cuda"))
+            slabs.append(cls.build_slab(pinned, verts))
         location = torch.from_numpy(loc.view(np.int32)).cuda()
         return cls(FeatureSpec(dim), self_rank, k, location, slabs, pinned)
+
+    @staticmethod
+    def build_slab(host_table: torch.Tensor, verts: np.ndarray, chunk: int = 1 << 20) -> torch.Tensor:
+        """This GPU's feature slab: rows X[verts] (priority order) pulled from the pinned,
+        mapped host table by the K4 gather itself (the table read as a resident tier
+        through UVA), so a multi-GB fill moves at PCIe speed with no host-side copy."""
+        verts = np.asarray(verts, dtype=np.int64)
+        dim = host_table.shape[1]
+        slab = torch.empty((max(len(verts), 1), dim), dtype=torch.float32, device="cuda")
+        if not len(verts):
+            return slab
+        if not host_table.is_pinned():
+            raise ValueError("host_table must be pinned (mapped) memory")
+        src = FeatureStore(FeatureSpec(dim), 0, 1, None, [int(host_table.data_ptr())])
+        ids = torch.from_numpy(verts.astype(np.uint32).view(np.int32)).cuda()
+        for c0 in range(0, len(verts), chunk):
+            c1 = min(len(verts), c0 + chunk)
+            cnt = torch.tensor([c1 - c0], dtype=torch.int32, device="cuda")
+            src.gather(ids[c0:c1].view(1, -1), cnt, slab[c0:c1].view(1, c1 - c0, dim))
+        return slab
 
     # ---------------------------------------------------------------- gather
     def gather(self, ids: torch.Tensor, counts: torch.Tensor, out: torch.Tensor, num_batches: int | None = None,

@@ -112,17 +112,18 @@ __global__ void __launch_bounds__(256) k_gather(GatherParams p) {
     }
 }
 
-// Warp-per-row gather for 16-byte-aligned rows of at most 32 vectors (D <= 128 fp32):
-// lane l moves vector l of a row. Each warp keeps ROWS rows in flight — their ids and
+// Warp-per-row gather for 16-byte-aligned rows of at most 32*VPL vectors (VPL = 1:
+// D <= 128 fp32; 2: D <= 256, C5's 1024-byte rows; 4: D <= 512): lane l moves vectors
+// l, l+32, ... of a row. Each warp keeps ROWS rows in flight — their ids and
 // locations are fetched by ROWS lanes at once and broadcast, then ROWS independent
 // 16-byte loads per lane are issued before any store — so HBM, NVLink and PCIe
 // latency overlap instead of serialising per row.
-template <int ROWS>
-__global__ void __launch_bounds__(256, GC_GATHER_MIN_BLOCKS) k_gather_rows(GatherParams p) {
+template <int ROWS, int VPL>
+__global__ void __launch_bounds__(256, VPL == 1 ? GC_GATHER_MIN_BLOCKS : 4) k_gather_rows(GatherParams p) {
     __shared__ unsigned long long s_tier[3];
     const uint32_t b = blockIdx.y;
     const uint32_t rows = min(p.count[b], p.max_rows);
-    const uint32_t per_row = p.fs.row_bytes / 16;  // <= 32
+    const uint32_t per_row = p.fs.row_bytes / 16;  // <= 32 * VPL
     const uint32_t* ids = p.ids + b * p.ids_stride;
     char* out = p.out + b * p.out_stride_rows * p.fs.row_bytes;
     const int lane = threadIdx.x & 31;
@@ -165,19 +166,44 @@ __global__ void __launch_bounds__(256, GC_GATHER_MIN_BLOCKS) k_gather_rows(Gathe
             }
         }
         const uint32_t n = min(32u, rows - c0);
+        if constexpr (VPL == 1) {
+            for (uint32_t j0 = 0; j0 < n; j0 += ROWS) {
+                uint4 v[ROWS];
+#pragma unroll
+                for (int j = 0; j < ROWS; ++j) {
+                    const char* src = (const char*)__shfl_sync(kFull, (unsigned long long)my_src, (j0 + j) & 31);
+                    v[j] = (j0 + j < n && src && (uint32_t)lane < per_row) ? ld_stream16(src + 16 * lane)
+                                                                             : make_uint4(0, 0, 0, 0);
+                }
+#pragma unroll
+                for (int j = 0; j < ROWS; ++j) {
+                    const bool have = __shfl_sync(kFull, my_src != nullptr, (j0 + j) & 31);
+                    if (j0 + j < n && have && (uint32_t)lane < per_row)
+                        st_stream16(out + (uint64_t)(c0 + j0 + j) * p.fs.row_bytes + 16 * lane, v[j]);
+                }
+            }
+            continue;
+        }
         for (uint32_t j0 = 0; j0 < n; j0 += ROWS) {
-            uint4 v[ROWS];
+            uint4 v[ROWS][VPL];
 #pragma unroll
             for (int j = 0; j < ROWS; ++j) {
                 const char* src = (const char*)__shfl_sync(kFull, (unsigned long long)my_src, (j0 + j) & 31);
-                v[j] = (j0 + j < n && src && (uint32_t)lane < per_row) ? ld_stream16(src + 16 * lane)
-                                                                         : make_uint4(0, 0, 0, 0);
+#pragma unroll
+                for (int q = 0; q < VPL; ++q) {
+                    const uint32_t c = (uint32_t)lane + 32u * q;
+                    v[j][q] = (j0 + j < n && src && c < per_row) ? ld_stream16(src + 16 * c) : make_uint4(0, 0, 0, 0);
+                }
             }
 #pragma unroll
             for (int j = 0; j < ROWS; ++j) {
                 const bool have = __shfl_sync(kFull, my_src != nullptr, (j0 + j) & 31);
-                if (j0 + j < n && have && (uint32_t)lane < per_row)
-                    st_stream16(out + (uint64_t)(c0 + j0 + j) * p.fs.row_bytes + 16 * lane, v[j]);
+                char* dst = out + (uint64_t)(c0 + j0 + j) * p.fs.row_bytes;
+#pragma unroll
+                for (int q = 0; q < VPL; ++q) {
+                    const uint32_t c = (uint32_t)lane + 32u * q;
+                    if (j0 + j < n && have && c < per_row) st_stream16(dst + 16 * c, v[j][q]);
+                }
             }
         }
     }
@@ -322,15 +348,22 @@ static int gather_impl(const gc_feature_store_t* store, const uint32_t* d_ids, u
     if (gx > cap) gx = cap;
     if (gx < 1) gx = 1;
     dim3 grid((unsigned)gx, num_batches);
-    if (vec16 && per_row <= 32) {
-        // warp per row, 32-row chunks per warp, 4 rows in flight; ~16 resident warps per
-        // SM per batch slice
+    if (vec16 && per_row <= 128) {
+        // warp per row, 32-row chunks per warp, 4 rows in flight (2 for 2 KB rows); ~16
+        // resident warps per SM per batch slice
         uint64_t wx = ((uint64_t)max_count + 32 * 8 - 1) / (32 * 8);
         uint64_t wcap = (uint64_t)sm_count() * g_gather_ctas_per_sm / num_batches;
         if (wcap < 1) wcap = 1;
         if (wx > wcap) wx = wcap;
         if (wx < 1) wx = 1;
-        k_gather_rows<GC_GATHER_ROWS><<<dim3((unsigned)wx, num_batches), 256, 0, s>>>(p);
+        const dim3 wg((unsigned)wx, num_batches);
+        if (per_row <= 32) {
+            k_gather_rows<GC_GATHER_ROWS, 1><<<wg, 256, 0, s>>>(p);
+        } else if (per_row <= 64) {
+            k_gather_rows<4, 2><<<wg, 256, 0, s>>>(p);
+        } else {
+            k_gather_rows<2, 4><<<wg, 256, 0, s>>>(p);
+        }
     } else if (vec16) {
         k_gather<16><<<grid, 256, 0, s>>>(p);
     } else {

@@ -181,8 +181,10 @@ def test_accumulate_hotness_matches_oracle():
 
 
 # ------------------------------------------------------------------ K4 gather
-@pytest.mark.parametrize("dim", [100, 128])
+@pytest.mark.parametrize("dim", [33, 100, 128, 256, 512, 600])
 def test_gather_three_tiers_bit_exact(dim):
+    """Every row width path: 4-byte vectors (D=33), warp per row with 1/2/4 16-byte
+    vectors per lane (D <= 128 / C5's D=256 / 512), thread per vector (D=600)."""
     from paper_2305_16588_b200.cache import FeatureStore, gather_rows
 
     n = 50_000
@@ -201,7 +203,7 @@ def test_gather_three_tiers_bit_exact(dim):
     assert tiers == {"local": want_local, "peer": want_peer, "host": len(ids) - want_local - want_peer}
 
 
-@pytest.mark.parametrize("dim", [64, 100, 128])
+@pytest.mark.parametrize("dim", [64, 100, 128, 256])
 def test_gather_deferred_host_rows_bit_exact(dim):
     """gc_gather_deferred (host rows by a second small-grid kernel) == gc_gather, over a
     window of batches with ragged counts and a capacity clamp."""
