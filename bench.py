@@ -30,6 +30,20 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "GraphSAGE epoch time, sampled+gathered batches/s at 1/2/4/8 B200; PCIe GB/batch"
 UNIT = "batches/s"
+C3 = {
+    "workload": "C3 ogbn-papers100M-shaped synthetic; cache partitioned over the clique (one owner per vertex, "
+                "peers read over NVLink) + host tier (UVA over PCIe)",
+    "num_vertices": 111_000_000,
+    "avg_degree": 14,
+    "skew": 1.2,
+    "feature_dim": 128,
+    "fanouts": [25, 10],
+    "batch_size": 1024,
+    "training_fraction": 0.1,
+    "master_seed": 7,
+}
+PCIE_NOMINAL_GBS = 64.0  # PCIe Gen5 x16, north_star's tier roofline
+NVLINK_GBS = 900.0  # NVLink 5 per direction
 CONFIG = {
     "workload": "C2 ogbn-products-shaped synthetic, fully HBM-cached",
     "num_vertices": 2_400_000,
@@ -61,6 +75,13 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--train-epochs", type=int, default=1, help="GraphSAGE epochs timed after the data-path bench")
+    ap.add_argument("--c3-scale", type=float, default=1.0,
+                    help="C3 three-tier section (papers100M shape x scale; 0 skips it)")
+    ap.add_argument("--c3-steps", type=int, default=3)
+    ap.add_argument("--c3-warmup", type=int, default=3)
+    ap.add_argument("--c3-presample-epochs", type=int, default=4)
+    ap.add_argument("--c3-budget-frac", type=float, default=0.1,
+                    help="per-GPU cache budget / (topology + feature bytes); the clique's is world x this")
     return ap.parse_args()
 
 
@@ -182,16 +203,18 @@ class CpuPath:
     feature gather X[ids] (numpy fancy indexing; the reference stores no values).
     Falls back to the oracle port when oracle/_ref is missing."""
 
-    def __init__(self, g, table, pool, epoch=0):
+    def __init__(self, g, table, pool, epoch=0, conf=None, seed=None):
         self.R = reference_module()
         self.kind = "reference" if self.R is not None else "port"
         self.table = table
-        B = CONFIG["batch_size"]
+        self.conf = conf or CONFIG
+        seed = _seed() if seed is None else seed
+        B = self.conf["batch_size"]
         if self.R is not None:
             R = self.R
             self.g = R.CsrGraph(g.num_vertices, g.num_edges, g.row_offsets, g.col_indices)
-            self.cfg = R.SamplingConfig(fanouts=tuple(CONFIG["fanouts"]), batch_size=B)
-            self.stream = R.KeyedRng(_seed()).derive(epoch, 0, 0)
+            self.cfg = R.SamplingConfig(fanouts=tuple(self.conf["fanouts"]), batch_size=B)
+            self.stream = R.KeyedRng(seed).derive(epoch, 0, 0)
             from gnncache.rng import ROLE_SAMPLE, ROLE_SHUFFLE
 
             self.role_sample = ROLE_SAMPLE
@@ -201,11 +224,11 @@ class CpuPath:
             import gnncache_oracle as O
 
             self.O, self.g = O, g
-            self.gkey, skey = O.batch_stream_keys(_seed(), epoch, 0, 0)
+            self.gkey, skey = O.batch_stream_keys(seed, epoch, 0, 0)
             self.shuffled = np.asarray(pool, np.int64)[O.permutation(skey, len(pool))]
 
     def batch(self, b: int):
-        B = CONFIG["batch_size"]
+        B = self.conf["batch_size"]
         start = (b * B) % len(self.shuffled)
         seeds = self.shuffled[start : start + B]
         if self.R is not None:
@@ -213,7 +236,7 @@ class CpuPath:
             uniq = bs.distinct_vertices()
             return uniq, self.table[uniq]
         O, g = self.O, self.g
-        hops = O.sample_batch(g.row_offsets, g.col_indices, g.num_vertices, seeds, CONFIG["fanouts"],
+        hops = O.sample_batch(g.row_offsets, g.col_indices, g.num_vertices, seeds, self.conf["fanouts"],
                               O.derive(self.gkey, 2, b))
         uniq = O.distinct_vertices(seeds, hops)
         return uniq, O.gather(self.table, uniq)
@@ -225,11 +248,11 @@ def _seed():
     return derive_seed(CONFIG["master_seed"], 0x10)
 
 
-def cpu_batches(g, table, pool, nbatches, seconds, epoch=0, keep=0):
+def cpu_batches(g, table, pool, nbatches, seconds, epoch=0, keep=0, conf=None, seed=None):
     """Time the reference's CPU path on one host core for about `seconds`; returns
     (batches, elapsed, kind, results) — results: (distinct ids, rows) of the first
     `keep` batches, which the bench compares with the device's epoch."""
-    path = CpuPath(g, table, pool, epoch)
+    path = CpuPath(g, table, pool, epoch, conf, seed)
     t0 = time.perf_counter()
     done = 0
     results = []
@@ -490,10 +513,179 @@ def run_b200(args):
                                 "sample": f"first {done} batches of epoch 0 (C2, 1 core): gnncache.sample_batch + "
                                           "distinct_vertices + X[ids]"}
         line["verified"] = verify_epoch0(pipe, plans[0], ref)
+    if args.c3_scale > 0:
+        del pipe, seq, store, table
+        torch.cuda.empty_cache()
+        line["c3_three_tier"] = c3_run(args, rank, local, world)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def c3_run(args, rank, local, world):
+    """C3 (BASELINE configs[2]) through Legion's full flow, one process per GPU of one
+    NVSwitch clique: per-rank presampling -> hotness merge -> CSLP plan -> each rank fills
+    its own slabs -> CUDA IPC peer slabs (clique.build_clique_cache), the host tier one
+    node-shared pinned table; then timed epochs through the three tiers. Reports
+    batches/s over all ranks (device time, max over ranks), measured PCIe per batch
+    against the reference plan's prediction N_total x CLS / batches (planner.py:142-169),
+    and the north-star tier roofline max(B_HBM/HBM, B_NVL/NVLink, B_PCIe/PCIe) per batch."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2305_16588_b200 as P
+    from paper_2305_16588_b200 import planner as PL
+    from paper_2305_16588_b200.clique import build_clique_cache
+    from paper_2305_16588_b200.distributed import max_over_ranks, sum_over_ranks
+    from paper_2305_16588_b200.graph import synthetic_features_device
+    from paper_2305_16588_b200.hostmem import shared_host_table
+    from paper_2305_16588_b200.partition import single_clique_partitioning
+    from paper_2305_16588_b200.pipeline import SampleGatherPipeline, StageTimer
+
+    t_setup = time.perf_counter()
+    multi = world > 1
+    barrier = dist.barrier if multi else (lambda: None)
+    n = int(round(C3["num_vertices"] * args.c3_scale))
+    dim, B = C3["feature_dim"], C3["batch_size"]
+    seed = C3["master_seed"]
+    g = P.generate_synthetic_device(n, C3["avg_degree"], C3["skew"], seed=P.derive_seed(seed, 1))
+    train = P.select_training_set(g, C3["training_fraction"], seed=P.derive_seed(seed, 2))
+    layout = P.block_layout(world, world)
+    pools = P.assign_tablets(P.split_intra_clique(train, single_clique_partitioning(g), layout), layout)
+    pool = pools[rank]
+    feat = P.FeatureSpec(dim)
+    total_bytes = g.num_edges * 4 + 8 * n + n * feat.row_bytes
+    budget = int(args.c3_budget_frac * total_bytes) * world
+    spec = P.HardwareSpec(layout, clique_budget_bytes=budget)
+    cfg = P.SamplingConfig(fanouts=tuple(C3["fanouts"]), batch_size=B, presample_epochs=args.c3_presample_epochs,
+                           seed=P.derive_seed(seed, 4))
+
+    def fill(t):  # the host tier, written from the device in 64 MB pieces
+        step = 1 << 17
+        for r0 in range(0, n, step):
+            rows = min(step, n - r0)
+            t[r0 : r0 + rows].copy_(synthetic_features_device(r0, rows, dim))
+        torch.cuda.synchronize()
+
+    run_id = os.environ.get("TORCHELASTIC_RUN_ID", "") + os.environ.get("MASTER_PORT", str(os.getpid()))
+    host = shared_host_table(f"gc_c3_{run_id}", (n, dim), torch.float32, local, fill=fill, barrier=barrier)
+    t0 = time.perf_counter()
+    cr = build_clique_cache(g, pool, layout, cfg, feat, spec, host.tensor, rank=rank, world=world)
+    torch.cuda.synchronize()
+    t_cache = time.perf_counter() - t0
+    nb = math.ceil(len(pool) / B)
+    pipe = SampleGatherPipeline(g, cfg, cr.features, len(pool), window=min(256, nb), feat_rows_cap=60_000,
+                                topology=cr.topology, lanes=2)
+    root = P.KeyedRng(P.derive_seed(seed, 5))
+    plans = [pipe.plan_epoch(pool, root.derive(e, 0, rank)) for e in range(args.c3_warmup + args.c3_steps)]
+    timed = plans[args.c3_warmup :]
+    # untimed passes over the timed epochs, one lane: algorithmic bytes, the capacity
+    # check (before timing), per-stage device times
+    seq = SampleGatherPipeline(g, cfg, cr.features, len(pool), window=min(256, nb), feat_rows_cap=60_000,
+                               topology=cr.topology, lanes=1)
+    acc = {"sampling": 0, "dedup": 0, "gather": 0}
+
+    def account(p, w0, nbw):
+        wb = p.window_bytes(nbw)
+        for k in acc:
+            acc[k] += wb[k]
+
+    for pl in timed:
+        seq.run_epoch(pl, on_window=account)
+    seq.check_capacity(reset=True)
+    timer = StageTimer()
+    seq.timer = timer
+    for pl in timed:
+        StageTimer.hold()
+        seq.run_epoch(pl)
+    seq.timer = None
+    torch.cuda.synchronize()
+    stages = {k: v[1] / len(timed) for k, v in timer.summary().items()}
+    del seq
+    for pl in plans[: args.c3_warmup]:
+        pipe.run_epoch_graph(pl)
+    torch.cuda.synchronize()
+    cr.topology.reset_counters()
+    cr.features.reset_counters()
+    setup_s = time.perf_counter() - t_setup
+    barrier()
+    ms = []
+    for pl in timed:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        pipe.run_epoch_graph(pl)
+        e1.record()
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    barrier()
+    pipe.check_capacity(reset=True)
+    t, f = cr.topology.tier_counts(), cr.features.tier_counts()
+    my_ms = float(sum(ms))
+    batches = nb * len(timed)
+    row = feat.row_bytes
+    row_txns = PL.feature_row_transactions(feat, spec)
+    cls = spec.cache_line_bytes
+    pcie_b = t["reads_host"] * 16 + t["edges_host"] * 4 + f["host"] * row
+    nvl_b = t["reads_peer"] * 16 + t["edges_peer"] * 4 + f["peer"] * row
+    hbm_b = acc["sampling"] + acc["dedup"] + acc["gather"] - pcie_b - nvl_b
+    peak, peak_kind = peak_hbm()
+    t_tier = {"hbm": hbm_b / (peak * 1e9), "nvlink": nvl_b / (NVLINK_GBS * 1e9), "pcie": pcie_b / (PCIE_NOMINAL_GBS * 1e9)}
+    my_roof_s = max(t_tier.values())  # this rank's epochs at the tier roofline
+    my_frac = my_roof_s / (my_ms / 1000.0)
+    measured_txn = t["host_txn"] + f["host"] * row_txns
+    # whole clique: device time is the max over ranks; bytes and transactions add up
+    total_ms = max_over_ranks(my_ms)
+    all_batches = sum_over_ranks(batches)
+    all_txn = sum_over_ranks(int(measured_txn))
+    min_frac = -max_over_ranks(-my_frac)
+    roof_sum = max_over_ranks(my_roof_s)  # the slowest rank's roofline time bounds the clique
+    pred_txn_per_batch = cr.predicted_pcie_txn_per_batch()
+    out = {
+        "metric": "sampled+gathered batches/s through the three tiers; PCIe GB/batch vs the reference plan",
+        "value": all_batches / (total_ms / 1000.0), "unit": "batches/s", "n_gpus": world,
+        "steps": len(timed), "warmup": args.c3_warmup, "ms_per_step": total_ms / len(timed),
+        "config": {**C3, "num_vertices": n, "num_edges": g.num_edges, "scale": args.c3_scale,
+                   "budget_bytes_clique": budget, "budget_frac_per_gpu": args.c3_budget_frac,
+                   "batches_per_step_per_gpu": nb, "window_batches": pipe.window, "lanes": pipe.lanes,
+                   "cuda_graph": True, "parallelism": f"dp{world}, cache partitioned over {world} GPU(s)",
+                   "host_tier": "one node-shared pinned table (/dev/shm + cudaHostRegister), UVA reads",
+                   "l2": "inputs (7 GB topology + 57 GB features at scale 1) far larger than L2"},
+        "plan": {"presample_epochs": cfg.presample_epochs, "alpha": cr.plan.alpha,
+                 "topo_prefix_len": cr.estimate.topo_prefix_len, "feat_prefix_len": cr.estimate.feat_prefix_len,
+                 "predicted_txn_total": cr.estimate.total_txns, "presample_batches": cr.presample_batches,
+                 "presample_txn_total": cr.sampling_txn_total},
+        "pcie": {"measured_gb_per_batch": all_txn * cls / all_batches / 1e9,
+                 "predicted_gb_per_batch": pred_txn_per_batch * cls / 1e9,
+                 "measured_over_predicted": (all_txn / all_batches) / pred_txn_per_batch if pred_txn_per_batch else None,
+                 "payload_gb_per_batch_rank0": pcie_b / batches / 1e9,
+                 "unit_note": "transactions x 64 B cache lines, the reference's PCIe unit (SPEC.md:403)"},
+        "tier_roofline": {"bytes_per_batch_rank0": {"hbm": hbm_b / batches, "nvlink": nvl_b / batches,
+                                                     "pcie": pcie_b / batches},
+                          "gbs": {"hbm": peak, "nvlink": NVLINK_GBS, "pcie": PCIE_NOMINAL_GBS}, "hbm_peak_kind": peak_kind,
+                          "t_us_per_batch_rank0": {k: v * 1e6 / batches for k, v in t_tier.items()},
+                          "bound_rank0": max(t_tier, key=t_tier.get),
+                          "measured_us_per_batch_rank0": my_ms * 1000 / batches,
+                          "frac_min_over_ranks": min_frac,
+                          "frac_clique": roof_sum / (total_ms / 1000.0)},
+        "tiers_per_batch_rank0": {**{k: v / batches for k, v in t.items()},
+                                  **{f"rows_{k}": v / batches for k, v in f.items()}},
+        "stages_ms_per_epoch_rank0": stages,
+        "setup_s": {"total": setup_s, "clique_cache": t_cache},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        done, el, kind, ref = cpu_batches(g, host.tensor.numpy(), pool, nb, args.cpu_seconds, keep=4, conf=C3,
+                                          seed=P.derive_seed(seed, 5))
+        out["cpu_baseline"] = {"value": done / el, "unit": "batches/s", "cores": 1, "kind": kind,
+                               "cpu_model": cpu_model(),
+                               "sample": f"first {done} batches of epoch 0 (C3, 1 core): gnncache.sample_batch + "
+                                         "distinct_vertices + X[ids] from the host table"}
+        out["verified"] = verify_epoch0(pipe, plans[0], ref)
+    del pipe, plans, timed, cr
+    barrier()  # no rank reads a peer's slabs or the host table any more
+    host.close()
+    torch.cuda.empty_cache()
+    return out
 
 
 def verify_epoch0(pipe, plan, ref):

@@ -87,7 +87,10 @@ def build_clique_cache(graph: CsrGraph, pool: np.ndarray, layout: CliqueLayout, 
     if layout.clique_count != 1 or layout.num_gpus != world:
         raise ValueError("one process per GPU of a single clique: layout must be block_layout(world, world)")
     clique_idx, local_idx = layout.gpu_position(rank)
-    backend = dist.get_backend(group)
+    distributed = dist.is_initialized()
+    if world > 1 and not distributed:
+        raise ValueError("world > 1 needs an initialised torch.distributed process group")
+    backend = dist.get_backend(group) if distributed else "none"
     # 1. presampling of this rank's tablet
     hot, my_batches = presample_rows(graph, pool, clique_idx, local_idx, cfg, spec)
     # 2. hotness merge (the one exchange step): rows on the collective backend's device
@@ -113,5 +116,6 @@ def build_clique_cache(graph: CsrGraph, pool: np.ndarray, layout: CliqueLayout, 
     features = FeatureStore.from_assignment(host_table, asg.feat_vertices, rank, peer_slabs=feat_slabs)
     # keep the own slabs alive with the stores; every rank must have mapped before use
     features._keep.append((t_offs, t_cols))
-    dist.barrier(group)
+    if distributed:
+        dist.barrier(group)
     return CliqueRank(rank, world, orders, plan, est, asg, txn_total, topology, features, batches)

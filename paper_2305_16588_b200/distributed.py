@@ -31,6 +31,10 @@ def merge_hotness(topo_row: torch.Tensor, feat_row: torch.Tensor, local_rank: in
     """All-reduce one rank's hotness rows into (topo_totals, topo_owner, feat_totals,
     feat_owner) on every rank. Rows are int64 on the backend's device."""
     out = []
+    if not dist.is_initialized():  # a single-GPU clique: the row is the column sum, owner 0
+        for row in (topo_row, feat_row):
+            out += [row.clone(), torch.zeros(row.shape, dtype=torch.int32, device=row.device)]
+        return tuple(out)
     for row in (topo_row, feat_row):
         if int(row.max().item() if row.numel() else 0) > MAX_HOTNESS:
             raise OverflowError("hotness counts exceed the packed owner all-reduce range")
@@ -98,6 +102,8 @@ def exchange_addresses(local: list, rank: int, world: int, group=None, export=No
     peers'. Returns addr[g][i]: device address of rank g's i-th tensor as seen from this
     rank (own tensors are returned as-is). export/import_ default to CUDA IPC; tests
     inject stand-ins to exercise the exchange logic on CPU."""
+    if world == 1:
+        return [list(local)]
     export = export or ipc_export
     import_ = import_ or ipc_import
     mine = [export(t) for t in local]
@@ -114,6 +120,8 @@ def exchange_addresses(local: list, rank: int, world: int, group=None, export=No
 
 def max_over_ranks(value: float, group=None) -> float:
     """Max of a host scalar over ranks (device-timed results, never wall clock)."""
+    if not dist.is_initialized():
+        return value
     backend = dist.get_backend(group)
     dev = "cuda" if backend == "nccl" else "cpu"
     t = torch.tensor([value], dtype=torch.float64, device=dev)
@@ -122,6 +130,8 @@ def max_over_ranks(value: float, group=None) -> float:
 
 
 def sum_over_ranks(value: int, group=None) -> int:
+    if not dist.is_initialized():
+        return value
     backend = dist.get_backend(group)
     dev = "cuda" if backend == "nccl" else "cpu"
     t = torch.tensor([value], dtype=torch.int64, device=dev)

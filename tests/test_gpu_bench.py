@@ -30,7 +30,21 @@ def _run(cmd, env=None):
     return json.loads(lines[0])
 
 
-SMALL = ["--steps", "3", "--warmup", "3", "--num-vertices", "200000", "--no-cpu-baseline", "--train-epochs", "0"]
+SMALL = ["--steps", "3", "--warmup", "3", "--num-vertices", "200000", "--no-cpu-baseline", "--train-epochs", "0",
+         "--c3-scale", "0.002", "--c3-steps", "2", "--c3-warmup", "1"]
+
+
+def _check_c3(d, world):
+    c3 = d["c3_three_tier"]
+    assert c3["n_gpus"] == world and c3["value"] > 0
+    assert c3["pcie"]["measured_gb_per_batch"] > 0 and c3["pcie"]["measured_over_predicted"] > 0
+    assert 0 < c3["tier_roofline"]["frac_min_over_ranks"] <= c3["tier_roofline"]["frac_clique"] * world + 1e-9
+    tiers = c3["tiers_per_batch_rank0"]
+    assert tiers["rows_local"] > 0 and tiers["rows_host"] > 0
+    if world > 1:  # the partitioned cache: peers' slabs are read through CUDA IPC
+        assert tiers["rows_peer"] > 0 and tiers["reads_peer"] > 0
+    else:
+        assert tiers["rows_peer"] == 0
 
 
 def test_bench_single_gpu_contract():
@@ -38,15 +52,28 @@ def test_bench_single_gpu_contract():
     assert KEYS <= set(d) and d["n_gpus"] == 1 and d["value"] > 0
     assert d["roofline"]["bound"] == "hbm" and 0 < d["roofline"]["frac"] < 1.5
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["scaling"] == "strong"
+    _check_c3(d, 1)
 
 
-def test_bench_two_ranks_weak_scaling():
+def test_bench_two_ranks_partitioned_clique():
     env = dict(os.environ, GC_DIST_BACKEND="gloo")
     d = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
               *SMALL, "--no-e2e"], env=env)
-    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
     assert d["config"]["dist_backend"] == "gloo"
+    _check_c3(d, 2)
+
+
+def test_bench_c3_self_check_against_reference():
+    """The C3 section's CPU leg runs the unmodified reference and the bench compares its
+    batches with the device's (distinct vertices + rows through all three tiers)."""
+    d = _run([sys.executable, "bench.py", "--steps", "3", "--warmup", "3", "--num-vertices", "200000",
+              "--train-epochs", "0", "--no-e2e", "--cpu-seconds", "3", "--c3-scale", "0.01", "--c3-steps", "2",
+              "--c3-warmup", "1"])
+    assert d["verified"]["bit_exact"] and d["c3_three_tier"]["verified"]["bit_exact"]
+    assert d["c3_three_tier"]["cpu_baseline"]["kind"] == "reference"
 
 
 def test_bench_reference_arm():
