@@ -214,7 +214,9 @@ class CpuPath:
             R = self.R
             self.g = R.CsrGraph(g.num_vertices, g.num_edges, g.row_offsets, g.col_indices)
             self.cfg = R.SamplingConfig(fanouts=tuple(self.conf["fanouts"]), batch_size=B)
-            self.stream = R.KeyedRng(seed).derive(epoch, 0, 0)
+            from gnncache.rng import KeyedRng
+
+            self.stream = KeyedRng(seed).derive(epoch, 0, 0)
             from gnncache.rng import ROLE_SAMPLE, ROLE_SHUFFLE
 
             self.role_sample = ROLE_SAMPLE
