@@ -718,36 +718,42 @@ def verify_epoch0(pipe, plan, ref):
 
 
 def train_run(args, g, cfg, pipe, pool, root, clique, local_idx, world):
-    """Full GraphSAGE epochs (hidden 256, 47 classes, SGD) on the device-prepared batches:
-    epoch time = sampling + gather + forward/backward/step of every batch (CUDA events)."""
+    """Full GraphSAGE epochs (3 layers, hidden 256, 47 classes, SGD lr 0.1) on the
+    device-prepared batches through TreeTrainer (hand-written forward/backward, one CUDA
+    graph per step; with N ranks the gradients are all-reduced every step — DDP):
+    epoch time = sampling + gather + forward/backward/step of every batch (CUDA events,
+    max over ranks)."""
     import torch
 
     from paper_2305_16588_b200.distributed import max_over_ranks
-    from paper_2305_16588_b200.train import GraphSAGE, synthetic_labels, train_epoch
+    from paper_2305_16588_b200.train import GraphSAGE, TreeTrainer, synthetic_labels, train_epoch_tree
 
     classes = 47
     labels = torch.from_numpy(synthetic_labels(np.arange(g.num_vertices), classes)).cuda()
     plans = [pipe.plan_epoch(pool, root.derive(1000 + e, clique, local_idx)) for e in range(args.train_epochs + 1)]
+    steps = int(max_over_ranks(float(plans[0].num_batches)))  # DDP: every rank runs the same steps
     out = {}
     for precision in ("fp32", "bf16"):
         torch.manual_seed(0)
         model = GraphSAGE(CONFIG["feature_dim"], 256, classes, len(cfg.fanouts)).cuda()
-        opt = torch.optim.SGD(model.parameters(), lr=0.1)
-        train_epoch(pipe, plans[0], model, opt, labels, max_batches=8, precision=precision)  # warm-up
+        tr = TreeTrainer(model, pipe.sampler, labels, lr=0.1, precision=precision)
+        train_epoch_tree(pipe, plans[0], tr, steps=8, max_batches=8)  # warm-up + graph capture
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         losses = []
         for e in range(args.train_epochs):
-            losses += train_epoch(pipe, plans[1 + e], model, opt, labels, precision=precision)
+            losses.append(train_epoch_tree(pipe, plans[1 + e], tr, steps=steps))
         e1.record()
         torch.cuda.synchronize()
         sec = e0.elapsed_time(e1) / 1000.0 / args.train_epochs
-        if world > 1:
-            sec = max_over_ranks(sec)
-        gemm = "fp32 (SIMT GEMMs)" if precision == "fp32" else "bf16 autocast GEMMs (fp32 weights, means, loss)"
+        sec = max_over_ranks(sec)
+        losses = torch.cat(losses).cpu().numpy()
+        gemm = "fp32 GEMMs (no TF32)" if precision == "fp32" else "bf16 GEMMs (fp32 accumulate, weights and loss)"
         res = {"seconds": sec, "batches_per_gpu": len(losses) // args.train_epochs, "epochs": args.train_epochs,
-               "model": f"GraphSAGE mean, 3 layers, hidden 256, 47 classes, {gemm}, SGD",
+               "steps_per_epoch": steps, "ddp_ranks": world,
+               "model": f"GraphSAGE mean, 3 layers, hidden 256, 47 classes, {gemm}, SGD lr 0.1",
+               "trainer": "TreeTrainer: gc_tree_* kernels + cuBLAS, one CUDA graph per step",
                "first_loss": float(losses[0]), "last_loss": float(losses[-1])}
         if precision == "fp32":
             out.update(res)

@@ -250,6 +250,45 @@ int gc_segment_mean_gather(const float* d_x, int dim, const int64_t* d_idx, cons
 int gc_scatter_add(const uint32_t* d_ids, const uint32_t* d_weights, int64_t count, uint64_t* d_counter,
                    void* stream);
 
+/* ---- Tree trainer (not in the reference; Legion's PyTorch backend).
+ * A sampled batch is a position tree: level 0 = seeds, level h+1 = hop h's neighbours
+ * (no dedup between hops, sampling.py:123-125), every position relabelled to a row of
+ * the batch's gathered feature matrix. Levels are stacked; level k padded to caps[k]. */
+#define GC_TREE_MAX_LEVELS 8
+typedef struct {
+    int32_t hops;                                    /* L; levels 0..L */
+    const int32_t* counts;                           /* [L+1, W] real positions per level */
+    int64_t counts_stride;                           /* W */
+    const int32_t* local[GC_TREE_MAX_LEVELS];        /* level k relabelled ids [W, local_stride[k]] */
+    int64_t local_stride[GC_TREE_MAX_LEVELS];
+    const int32_t* offsets[GC_TREE_MAX_LEVELS];      /* hop h child offsets [W, offsets_stride[h]] */
+    int64_t offsets_stride[GC_TREE_MAX_LEVELS];
+    const int32_t* seeds;                            /* global seed ids [W, seeds_stride] */
+    int64_t seeds_stride;
+    const int64_t* labels;                           /* class per vertex [n] (nullable) */
+    int64_t caps[GC_TREE_MAX_LEVELS];                /* padded slots per level */
+} gc_tree_src_t;
+
+/* Stage batch *d_batch (device scalar, so a captured graph replays for any batch):
+ * loc[P] feature row of each stacked position (0 when padded); for levels 0..L-1,
+ * cbeg/cdeg = stacked first child and child count; parent[P] (-1 for seeds and
+ * padding); labels[caps[0]] = labels[seed] or -100 for padding. */
+int gc_tree_stage(const gc_tree_src_t* src, const int32_t* d_batch, int32_t* d_loc, int32_t* d_cbeg, int32_t* d_cdeg,
+                  int32_t* d_parent, int64_t* d_labels, void* stream);
+/* Neighbour aggregation of one layer for positions [0, p_out). mode 0 (GraphSAGE):
+ * out[p] = [in[row(p)], mean of in[row(c)] over children c] (2*dim columns); mode 1
+ * (GCN): out[p] = (in[row(p)] + sum in[row(c)]) / (deg(p) + 1). row(q) =
+ * (*d_batch) * batch_rows + (rowmap ? rowmap[q] : q). dtypes: 0 fp32, 1 bf16; sums in
+ * fp32 in child order. dim and strides multiples of 4. */
+int gc_tree_aggregate(const void* d_in, int in_dtype, int64_t in_stride, int dim, const int32_t* d_rowmap,
+                      const int32_t* d_cbeg, const int32_t* d_cdeg, int64_t p_out, int mode, void* d_out, int out_dtype,
+                      int64_t out_stride, const int32_t* d_batch, int64_t batch_rows, void* stream);
+/* Its backward for input rows [0, p_in), fused with the ReLU mask of h (nullable):
+ * g[q] = [h[q] > 0] * (cs(q) dA[q, self] + cc(parent(q)) dA[parent(q), child]). */
+int gc_tree_aggregate_backward(const void* d_dA, int dtype, int64_t dA_stride, int dim, int mode,
+                               const int32_t* d_parent, const int32_t* d_cdeg, int64_t p_out, int64_t p_in,
+                               const void* d_h, int64_t h_stride, void* d_g, int64_t g_stride, void* stream);
+
 /* ------------------------------------------- K6/K7: cost model (planner.py:42-261) */
 
 /* Column sums and first argmax over K rows (planner.py:50-55): rows are int64 [K][n]. */

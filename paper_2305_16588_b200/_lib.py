@@ -84,6 +84,25 @@ class GcFeatureStore(ctypes.Structure):
     ]
 
 
+GC_TREE_MAX_LEVELS = 8
+
+
+class GcTreeSrc(ctypes.Structure):
+    _fields_ = [
+        ("hops", ctypes.c_int32),
+        ("counts", ctypes.c_void_p),
+        ("counts_stride", ctypes.c_int64),
+        ("local", ctypes.c_void_p * GC_TREE_MAX_LEVELS),
+        ("local_stride", ctypes.c_int64 * GC_TREE_MAX_LEVELS),
+        ("offsets", ctypes.c_void_p * GC_TREE_MAX_LEVELS),
+        ("offsets_stride", ctypes.c_int64 * GC_TREE_MAX_LEVELS),
+        ("seeds", ctypes.c_void_p),
+        ("seeds_stride", ctypes.c_int64),
+        ("labels", ctypes.c_void_p),
+        ("caps", ctypes.c_int64 * GC_TREE_MAX_LEVELS),
+    ]
+
+
 V = ctypes.c_void_p
 I32 = ctypes.c_int32
 U32 = ctypes.c_uint32
@@ -122,6 +141,11 @@ SIGNATURES = {
     "gc_gather": (ctypes.c_int, [ctypes.POINTER(GcFeatureStore), V, U64, V, U32, U32, V, U64, V, V]),
     "gc_scatter_add": (ctypes.c_int, [V, V, I64, V, V]),
     "gc_segment_mean_gather": (ctypes.c_int, [V, ctypes.c_int, V, V, I64, V, V]),
+    "gc_tree_stage": (ctypes.c_int, [ctypes.POINTER(GcTreeSrc), V, V, V, V, V, V, V]),
+    "gc_tree_aggregate": (ctypes.c_int, [V, ctypes.c_int, I64, ctypes.c_int, V, V, V, I64, ctypes.c_int, V,
+                                         ctypes.c_int, I64, V, I64, V]),
+    "gc_tree_aggregate_backward": (ctypes.c_int, [V, ctypes.c_int, I64, ctypes.c_int, ctypes.c_int, V, V, I64, I64,
+                                                  V, I64, V, I64, V]),
     "gc_colsum_argmax": (ctypes.c_int, [V, U32, I64, V, V, V]),
     "gc_descending_order_temp_bytes": (SZ, [I64]),
     "gc_descending_order": (ctypes.c_int, [V, I64, V, V, SZ, V]),

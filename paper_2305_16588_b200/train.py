@@ -192,3 +192,288 @@ def train_epoch(pipe, plan, model: GraphSAGE, opt, labels: torch.Tensor, max_bat
 
     pipe.run_epoch(plan, on_window=consume)
     return losses
+
+
+# ---------------------------------------------------------------------------------------
+# TreeTrainer: the same model and SGD step with a hand-written forward and backward.
+_MM_OUT_DTYPE = [None]  # does torch.mm(..., out_dtype=) work here (decided once, outside graph capture)
+
+
+def _mm_f32(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """a @ b accumulated and returned in fp32 (bf16 operands stay on the tensor cores)."""
+    if a.dtype == torch.float32:
+        return a @ b
+    if _MM_OUT_DTYPE[0] is None:
+        try:
+            torch.mm(a[:1], b[:, :1], out_dtype=torch.float32)
+            _MM_OUT_DTYPE[0] = True
+        except (RuntimeError, TypeError):
+            _MM_OUT_DTYPE[0] = False
+    return torch.mm(a, b, out_dtype=torch.float32) if _MM_OUT_DTYPE[0] else (a @ b).float()
+
+
+class TreeTrainer:
+    """Training steps of a GraphSAGE / GCN model on the pipeline's windows, B200-native.
+
+    Every position of the sampled tree has exactly one parent, so the whole backward is
+    gathers, no atomics: layer l's neighbour aggregation (gc_tree_aggregate) writes
+    A_l = [h_self, mean(h_children)] (GCN: the closed-neighbourhood mean), one cuBLAS
+    GEMM + bias + ReLU gives h_{l+1}; backward is dW = g^T A, dA = g W and
+    gc_tree_aggregate_backward, which routes dA back to each position from its own row
+    and its parent's (fused with the ReLU mask). The first layer reads its inputs straight
+    from the window's gathered feature rows through the relabelled ids. Batch b of the
+    window is staged (gc_tree_stage) into padded fixed-shape buffers — padded positions
+    have no children and no parent, padded seeds no label — so the whole step
+    (stage, forward, backward, SGD) is one CUDA graph, replayed for every batch with the
+    batch index read from device memory: no host work and no sync per batch.
+
+    Across ranks (DDP) the gradients live in one flat buffer: one all-reduce per step
+    (NCCL, or gloo for the CPU tests), averaged over the ranks that had a batch; a rank
+    whose tablet ran out of batches still joins each step with a zero gradient.
+    Semantics are GraphSAGE.forward + F.cross_entropy + torch.optim.SGD(lr) (no
+    momentum), which tests/test_gpu_train.py checks step by step."""
+
+    def __init__(self, model: GraphSAGE, sampler, labels: torch.Tensor, lr: float, precision: str = "fp32",
+                 use_graph: bool = True, group=None):
+        import torch.distributed as dist
+
+        from . import _lib
+
+        if precision not in PRECISIONS:
+            raise ValueError(f"precision must be one of {PRECISIONS}")
+        self.model, self.sp, self.lr = model, sampler, float(lr)
+        self.layers = list(model.layers)
+        L = len(self.layers)
+        if L != sampler.H:
+            raise ValueError("the model needs one layer per sampled hop")
+        if not sampler.relabel:
+            raise ValueError("the trainer needs relabelled windows (SampleGatherPipeline(relabel=True))")
+        self.mode = 0 if isinstance(self.layers[0], SAGELayer) else 1
+        self.act = torch.bfloat16 if precision == "bf16" else torch.float32
+        self.dt = 1 if precision == "bf16" else 0
+        self.L = L
+        caps = list(sampler.caps)
+        self.base = [0]
+        for c in caps:
+            self.base.append(self.base[-1] + c)
+        P = self.base[-1]
+        dev = "cuda"
+        i32 = torch.int32
+        self.b_dev = torch.zeros(1, dtype=i32, device=dev)
+        self.loc = torch.zeros(P, dtype=i32, device=dev)
+        self.cbeg = torch.zeros(max(self.base[L], 1), dtype=i32, device=dev)
+        self.cdeg = torch.zeros(max(self.base[L], 1), dtype=i32, device=dev)
+        self.parent = torch.zeros(P, dtype=i32, device=dev)
+        self.labels_b = torch.zeros(caps[0], dtype=torch.int64, device=dev)
+        src = _lib.GcTreeSrc()
+        src.hops = L
+        src.counts = sampler.counts.data_ptr()
+        src.counts_stride = sampler.counts.stride(0)
+        levels = [sampler.local_seeds] + list(sampler.local_nbrs)
+        for k, t in enumerate(levels):
+            src.local[k] = t.data_ptr()
+            src.local_stride[k] = t.stride(0)
+            src.caps[k] = caps[k]
+        for h, t in enumerate(sampler.offsets):
+            src.offsets[h] = t.data_ptr()
+            src.offsets_stride[h] = t.stride(0)
+        src.seeds = sampler.seeds.data_ptr()
+        src.seeds_stride = sampler.seeds.stride(0)
+        self.labels = labels.to(device=dev, dtype=torch.int64).contiguous()
+        src.labels = self.labels.data_ptr()
+        self.src = src
+        # activations: A_l [base_{L-l}, in_cols], h_{l+1} [base_{L-l}, hidden]
+        self.A, self.H = [], []
+        for l, layer in enumerate(self.layers):
+            rows = self.base[L - l]
+            cols = self._weights(layer)[0].shape[1]  # 2 d_in (SAGE: self | neighbour mean) or d_in (GCN)
+            self.A.append(torch.zeros((rows, cols), dtype=self.act, device=dev))
+            self.H.append(torch.zeros((rows, self._weights(layer)[0].shape[0]), dtype=self.act, device=dev))
+        # parameters and gradients: one flat buffer each (+1 slot: ranks contributing a batch)
+        self.params = [p for p in model.parameters()]
+        n = sum(p.numel() for p in self.params)
+        self.flat = torch.empty(n, dtype=torch.float32, device=dev)
+        self.gflat = torch.zeros(n + 1, dtype=torch.float32, device=dev)
+        o = 0
+        self.grad = {}
+        with torch.no_grad():
+            for p in self.params:
+                k = p.numel()
+                self.flat[o : o + k].copy_(p.detach().reshape(-1))
+                p.data = self.flat[o : o + k].view_as(p)
+                self.grad[id(p)] = self.gflat[o : o + k].view_as(p)
+                o += k
+        self.gflat[n] = 1.0
+        self.loss = torch.zeros((), dtype=torch.float32, device=dev)
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.backend = dist.get_backend(group) if self.world > 1 else None
+        self.use_graph = use_graph
+        self._graphs = None
+        self.steps = 0
+
+    @staticmethod
+    def _weights(layer):
+        if isinstance(layer, SAGELayer):
+            return torch.cat([layer.lin_self.weight, layer.lin_neigh.weight], 1), layer.lin_self.bias
+        return layer.lin.weight, layer.lin.bias
+
+    def _grad_w(self, layer, dW: torch.Tensor, db: torch.Tensor) -> None:
+        if isinstance(layer, SAGELayer):
+            d = layer.lin_self.weight.shape[1]
+            self.grad[id(layer.lin_self.weight)].copy_(dW[:, :d])
+            self.grad[id(layer.lin_neigh.weight)].copy_(dW[:, d:])
+            self.grad[id(layer.lin_self.bias)].copy_(db)
+        else:
+            self.grad[id(layer.lin.weight)].copy_(dW)
+            self.grad[id(layer.lin.bias)].copy_(db)
+
+    # ------------------------------------------------------------------ one step
+    def _fwd_bwd(self) -> None:
+        from . import _lib
+
+        lib, s = _lib.lib(), _lib.stream_handle()
+        sp, L, act = self.sp, self.L, self.act
+        _lib.check(lib.gc_tree_stage(self.src, self.b_dev.data_ptr(), self.loc.data_ptr(), self.cbeg.data_ptr(),
+                                     self.cdeg.data_ptr(), self.parent.data_ptr(), self.labels_b.data_ptr(), s),
+                   "tree_stage")
+        feats = self._features
+        dim = feats.shape[-1]
+        Ws = []
+        for l, layer in enumerate(self.layers):
+            W, b = self._weights(layer)
+            Wa, ba = W.detach().to(act), b.detach().to(act)
+            Ws.append(Wa)
+            A, rows = self.A[l], self.base[L - l]
+            if l == 0:  # children rows straight from the gathered features of batch b
+                _lib.check(lib.gc_tree_aggregate(feats.data_ptr(), 0, dim, dim, self.loc.data_ptr(),
+                                                 self.cbeg.data_ptr(), self.cdeg.data_ptr(), rows, self.mode,
+                                                 A.data_ptr(), self.dt, A.stride(0), self.b_dev.data_ptr(),
+                                                 feats.stride(0) // dim, s), "tree_aggregate")
+            else:
+                h = self.H[l - 1]
+                _lib.check(lib.gc_tree_aggregate(h.data_ptr(), self.dt, h.stride(0), h.shape[1], None,
+                                                 self.cbeg.data_ptr(), self.cdeg.data_ptr(), rows, self.mode,
+                                                 A.data_ptr(), self.dt, A.stride(0), None, 0, s), "tree_aggregate")
+            torch.addmm(ba, A, Wa.t(), out=self.H[l])
+            self.H[l].relu_()
+        B = self.base[1]
+        top = self.H[L - 1][:B]
+        cls = self.model.classifier
+        logits = _mm_f32(top, cls.weight.detach().to(act).t()) + cls.bias.detach()
+        y = self.labels_b
+        valid = (y >= 0).to(torch.float32)
+        nvalid = valid.sum().clamp_(min=1.0)
+        yc = y.clamp(min=0)
+        logp = torch.log_softmax(logits, dim=1)
+        torch.div(-(logp.gather(1, yc.view(-1, 1)).squeeze(1) * valid).sum(), nvalid, out=self.loss)
+        # backward
+        dlog = logp.exp_()
+        dlog.scatter_add_(1, yc.view(-1, 1), -torch.ones_like(valid).view(-1, 1))
+        dlog.mul_((valid / nvalid).view(-1, 1))
+        self.grad[id(cls.weight)].copy_(_mm_f32(dlog.t().to(act), top))
+        self.grad[id(cls.bias)].copy_(dlog.sum(0))
+        g = (dlog.to(act) @ cls.weight.detach().to(act)) * (top > 0)
+        for l in range(L - 1, -1, -1):
+            layer = self.layers[l]
+            self._grad_w(layer, _mm_f32(g.t(), self.A[l]), g.float().sum(0))
+            if l == 0:
+                break
+            dA = g @ Ws[l]
+            h = self.H[l - 1]
+            g_in = torch.empty_like(h)
+            _lib.check(lib.gc_tree_aggregate_backward(dA.data_ptr(), self.dt, dA.stride(0), h.shape[1], self.mode,
+                                                      self.parent.data_ptr(), self.cdeg.data_ptr(), dA.shape[0],
+                                                      h.shape[0], h.data_ptr(), h.stride(0), g_in.data_ptr(),
+                                                      g_in.stride(0), s), "tree_aggregate_backward")
+            g = g_in
+
+    def _update(self) -> None:
+        n = self.flat.numel()
+        if self.world > 1:
+            self.flat.sub_(self.gflat[:n] * (self.lr / self.gflat[n].clamp(min=1.0)))
+        else:
+            self.flat.add_(self.gflat[:n], alpha=-self.lr)
+
+    def _allreduce(self) -> None:
+        import torch.distributed as dist
+
+        if self.backend == "nccl":
+            dist.all_reduce(self.gflat, group=self.group)
+        else:
+            host = self.gflat.cpu()
+            dist.all_reduce(host, group=self.group)
+            self.gflat.copy_(host)
+
+    def _capture(self) -> None:
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # warm-up outside the capture (cuBLAS handles, lazy init)
+            for _ in range(2):
+                self._fwd_bwd()
+        torch.cuda.current_stream().wait_stream(side)
+        g1 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g1):
+            self._fwd_bwd()
+            if self.world == 1:
+                self._update()
+        g2 = None
+        if self.world > 1:
+            g2 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g2):
+                self._update()
+        self._graphs = (g1, g2)
+
+    def step(self, features: torch.Tensor, b: int | None) -> torch.Tensor:
+        """One SGD step on batch b of the sampler's current window (features: the
+        window's gathered rows [W, ucap, D]); b=None: this rank has no batch left this
+        step and joins the gradient all-reduce with zeros. Returns the loss (device)."""
+        self._features = features
+        if b is None:
+            self.gflat.zero_()
+            self._allreduce()
+            self._update()
+            self.gflat[-1] = 1.0
+            return self.loss
+        self.b_dev.fill_(int(b))
+        if not self.use_graph:
+            self._fwd_bwd()
+            if self.world > 1:
+                self._allreduce()
+            self._update()
+            if self.world > 1:
+                self.gflat[-1] = 1.0
+        else:
+            if self._graphs is None or self._graph_feats != features.data_ptr():
+                self._graph_feats = features.data_ptr()
+                self._capture()
+            g1, g2 = self._graphs
+            g1.replay()
+            if g2 is not None:
+                self._allreduce()
+                g2.replay()
+                self.gflat[-1] = 1.0
+        self.steps += 1
+        return self.loss
+
+
+def train_epoch_tree(pipe, plan, trainer: TreeTrainer, steps: int | None = None, max_batches: int | None = None):
+    """One epoch through TreeTrainer: windows sampled on the device, every batch one
+    graph replay; with DDP every rank runs `steps` steps (the max over ranks; ranks out
+    of batches join with zero gradients). Returns the per-batch losses as one device
+    tensor (no host sync inside the epoch)."""
+    losses = []
+
+    def consume(p, w0, nbw):
+        if p.sampler is not trainer.sp:
+            raise ValueError("the trainer was built on another window sampler (use lanes=1)")
+        for b in range(nbw):
+            if max_batches is not None and len(losses) >= max_batches:
+                return
+            losses.append(trainer.step(p.features, b).clone())
+
+    pipe.run_epoch(plan, on_window=consume)
+    for _ in range(len(losses), steps or 0):
+        trainer.step(pipe.features, None)
+    pipe.check_capacity(reset=True)
+    return torch.stack(losses) if losses else torch.zeros(0, device="cuda")
