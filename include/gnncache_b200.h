@@ -271,23 +271,28 @@ typedef struct {
 
 /* Stage batch *d_batch (device scalar, so a captured graph replays for any batch):
  * loc[P] feature row of each stacked position (0 when padded); for levels 0..L-1,
- * cbeg/cdeg = stacked first child and child count; parent[P] (-1 for seeds and
- * padding); labels[caps[0]] = labels[seed] or -100 for padding. */
+ * cbeg/cdeg = stacked first child and child count; level_counts[L+1] = real positions
+ * per level; labels[caps[0]] = labels[seed] or -100 for padding. */
 int gc_tree_stage(const gc_tree_src_t* src, const int32_t* d_batch, int32_t* d_loc, int32_t* d_cbeg, int32_t* d_cdeg,
-                  int32_t* d_parent, int64_t* d_labels, void* stream);
+                  int32_t* d_level_counts, int64_t* d_labels, void* stream);
 /* Neighbour aggregation of one layer for positions [0, p_out). mode 0 (GraphSAGE):
  * out[p] = [in[row(p)], mean of in[row(c)] over children c] (2*dim columns); mode 1
- * (GCN): out[p] = (in[row(p)] + sum in[row(c)]) / (deg(p) + 1). row(q) =
- * (*d_batch) * batch_rows + (rowmap ? rowmap[q] : q). dtypes: 0 fp32, 1 bf16; sums in
- * fp32 in child order. dim and strides multiples of 4. */
+ * (GCN): out[p] = (in[row(p)] + sum in[row(c)]) / (deg(p) + 1); mode + 2: ReLU applied
+ * to every input row as it is read (the input is a layer's pre-activations). row(q) =
+ * (*d_batch) * batch_rows + (rowmap ? rowmap[q] : q). dtypes: 0 fp32, 1 bf16 (fp32 ->
+ * bf16 allowed); sums in fp32 in child order. dim and strides: 16-byte multiples. */
 int gc_tree_aggregate(const void* d_in, int in_dtype, int64_t in_stride, int dim, const int32_t* d_rowmap,
                       const int32_t* d_cbeg, const int32_t* d_cdeg, int64_t p_out, int mode, void* d_out, int out_dtype,
                       int64_t out_stride, const int32_t* d_batch, int64_t batch_rows, void* stream);
-/* Its backward for input rows [0, p_in), fused with the ReLU mask of h (nullable):
- * g[q] = [h[q] > 0] * (cs(q) dA[q, self] + cc(parent(q)) dA[parent(q), child]). */
+/* Its backward for input rows [0, p_in), fused with the ReLU mask of the input
+ * pre-activations h (nullable): g[q] = [h[q] > 0] * (cs(q) dA[q, self] +
+ * cc(parent(q)) dA[parent(q), child]); SAGE cs = 1, cc = 1/deg; GCN 1/(deg+1).
+ * Rows [0, p_in) span levels 0..nlevels-1 of level_caps (host array); rows past
+ * d_level_counts[k] (padding) are written as zeros. */
 int gc_tree_aggregate_backward(const void* d_dA, int dtype, int64_t dA_stride, int dim, int mode,
-                               const int32_t* d_parent, const int32_t* d_cdeg, int64_t p_out, int64_t p_in,
-                               const void* d_h, int64_t h_stride, void* d_g, int64_t g_stride, void* stream);
+                               const int32_t* d_cbeg, const int32_t* d_cdeg, int64_t p_out, int64_t p_in,
+                               const void* d_h, int64_t h_stride, void* d_g, int64_t g_stride, int nlevels,
+                               const int64_t* level_caps, const int32_t* d_level_counts, void* stream);
 
 /* ------------------------------------------- K6/K7: cost model (planner.py:42-261) */
 

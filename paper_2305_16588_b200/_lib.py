@@ -145,7 +145,7 @@ SIGNATURES = {
     "gc_tree_aggregate": (ctypes.c_int, [V, ctypes.c_int, I64, ctypes.c_int, V, V, V, I64, ctypes.c_int, V,
                                          ctypes.c_int, I64, V, I64, V]),
     "gc_tree_aggregate_backward": (ctypes.c_int, [V, ctypes.c_int, I64, ctypes.c_int, ctypes.c_int, V, V, I64, I64,
-                                                  V, I64, V, I64, V]),
+                                                  V, I64, V, I64, ctypes.c_int, ctypes.POINTER(I64), V, V]),
     "gc_colsum_argmax": (ctypes.c_int, [V, U32, I64, V, V, V]),
     "gc_descending_order_temp_bytes": (SZ, [I64]),
     "gc_descending_order": (ctypes.c_int, [V, I64, V, V, SZ, V]),

@@ -79,9 +79,11 @@ namespace gc {
 
 __global__ void k_tree_stage(gc_tree_src_t s, const int32_t* __restrict__ d_batch, int64_t total,
                              int32_t* __restrict__ loc, int32_t* __restrict__ cbeg, int32_t* __restrict__ cdeg,
-                             int32_t* __restrict__ parent, int64_t* __restrict__ labels) {
+                             int32_t* __restrict__ level_counts, int64_t* __restrict__ labels) {
     const int b = *d_batch;
     const int L = s.hops;
+    if (blockIdx.x == 0 && threadIdx.x <= (unsigned)L)
+        level_counts[threadIdx.x] = s.counts[(int64_t)threadIdx.x * s.counts_stride + b];
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < total; p += (int64_t)gridDim.x * blockDim.x) {
         int k = 0;
         int64_t base = 0;
@@ -90,12 +92,7 @@ __global__ void k_tree_stage(gc_tree_src_t s, const int32_t* __restrict__ d_batc
         const int64_t cnt = s.counts[(int64_t)k * s.counts_stride + b];
         const bool real = i < cnt;
         loc[p] = real ? s.local[k][(int64_t)b * s.local_stride[k] + i] : 0;
-        if (k == 0) {
-            parent[p] = -1;
-            if (labels) labels[i] = real ? s.labels[(uint32_t)s.seeds[(int64_t)b * s.seeds_stride + i]] : -100;
-        } else if (!real) {
-            parent[p] = -1;
-        }
+        if (k == 0 && labels) labels[i] = real ? s.labels[(uint32_t)s.seeds[(int64_t)b * s.seeds_stride + i]] : -100;
         if (k < L) {
             const int64_t nbase = base + s.caps[k];
             const int32_t* off = s.offsets[k] + (int64_t)b * s.offsets_stride[k];
@@ -106,106 +103,243 @@ __global__ void k_tree_stage(gc_tree_src_t s, const int32_t* __restrict__ d_batc
             }
             cbeg[p] = (int32_t)(nbase + o0);
             cdeg[p] = d;
-            for (int32_t j = 0; j < d; ++j) parent[nbase + o0 + j] = (int32_t)p;
         }
     }
 }
 
+// 16-byte vectors of T: 4 fp32 or 8 bf16 elements, widened to fp32 in registers
 template <typename T>
-struct V4;
-template <>
-struct V4<float> {
-    __device__ static float4 load(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
-    __device__ static void store(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+struct Vec {
+    static constexpr int N = 16 / sizeof(T);
 };
-template <>
-struct V4<__nv_bfloat16> {
-    __device__ static float4 load(const __nv_bfloat16* p) {
-        const uint2 raw = __ldg(reinterpret_cast<const uint2*>(p));
-        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
-        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
-        return make_float4(a.x, a.y, b.x, b.y);
+__device__ __forceinline__ void vload(const float* p, float (&v)[4]) {
+    const float4 r = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = r.x; v[1] = r.y; v[2] = r.z; v[3] = r.w;
+}
+__device__ __forceinline__ void vload(const __nv_bfloat16* p, float (&v)[8]) {
+    const uint4 r = __ldg(reinterpret_cast<const uint4*>(p));
+    const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
+        v[2 * i] = f.x;
+        v[2 * i + 1] = f.y;
     }
-    __device__ static void store(__nv_bfloat16* p, float4 v) {
-        const __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y);
-        const __nv_bfloat162 b = __floats2bfloat162_rn(v.z, v.w);
-        uint2 raw;
-        raw.x = *reinterpret_cast<const uint32_t*>(&a);
-        raw.y = *reinterpret_cast<const uint32_t*>(&b);
-        *reinterpret_cast<uint2*>(p) = raw;
+}
+// raw 16-byte loads kept packed in registers until used (4 registers per vector)
+__device__ __forceinline__ uint4 rload(const void* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
+__device__ __forceinline__ void unpack(uint4 r, float (&v)[4]) {
+    v[0] = __uint_as_float(r.x); v[1] = __uint_as_float(r.y); v[2] = __uint_as_float(r.z); v[3] = __uint_as_float(r.w);
+}
+__device__ __forceinline__ void unpack(uint4 r, float (&v)[8]) {
+    const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
+        v[2 * i] = f.x;
+        v[2 * i + 1] = f.y;
     }
-};
+}
+// store N elements (any N multiple of 2) as fp32 or bf16
+template <int N>
+__device__ __forceinline__ void vstore(float* p, const float (&v)[N], float s) {
+#pragma unroll
+    for (int i = 0; i < N; i += 4)
+        *reinterpret_cast<float4*>(p + i) = make_float4(v[i] * s, v[i + 1] * s, v[i + 2] * s, v[i + 3] * s);
+}
+template <int N>
+__device__ __forceinline__ void vstore(__nv_bfloat16* p, const float (&v)[N], float s) {
+    uint32_t w[N / 2];
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) {
+        const __nv_bfloat162 b = __floats2bfloat162_rn(v[2 * i] * s, v[2 * i + 1] * s);
+        w[i] = *reinterpret_cast<const uint32_t*>(&b);
+    }
+    if constexpr (N == 8) {
+        *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+    } else {
+        *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
+    }
+}
 
-__device__ __forceinline__ float4 f4add(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
-__device__ __forceinline__ float4 f4mul(float4 a, float s) { return make_float4(a.x * s, a.y * s, a.z * s, a.w * s); }
-
-// forward aggregation, warp per output position, lanes over 4-element column groups:
-//   SAGE: out[p] = [ in[row(p)], mean_{c in children(p)} in[row(c)] ]      (2*dim columns)
-//   GCN:  out[p] = ( in[row(p)] + sum_c in[row(c)] ) / (deg(p) + 1)        (dim columns)
-// row(q) = batch_row0 + (rowmap ? rowmap[q] : q); children summed in order, in fp32.
-template <typename TI, typename TO, int MODE>
-__global__ void __launch_bounds__(256) k_tree_aggregate(const TI* __restrict__ in, int64_t in_stride, int dim,
+// forward aggregation, warp per output position, lanes over 16-byte column groups:
+//   SAGE: out[p] = [ f(in[row(p)]), mean_{c in children(p)} f(in[row(c)]) ]   (2*dim columns)
+//   GCN:  out[p] = ( f(in[row(p)]) + sum_c f(in[row(c)]) ) / (deg(p) + 1)      (dim columns)
+// f = ReLU when the input rows are a layer's pre-activations (RELU), else identity.
+// row(q) = batch_row0 + (rowmap ? rowmap[q] : q). Children are consecutive positions;
+// 4 child rows are loaded before any is summed (summed in child order, in fp32).
+template <typename TI, typename TO, int MODE, bool RELU>
+__global__ void __launch_bounds__(256, 4) k_tree_aggregate(const TI* __restrict__ in, int64_t in_stride, int dim,
                                                         const int32_t* __restrict__ rowmap,
                                                         const int32_t* __restrict__ cbeg,
                                                         const int32_t* __restrict__ cdeg, int64_t p_out,
                                                         TO* __restrict__ out, int64_t out_stride,
                                                         const int32_t* __restrict__ d_batch, int64_t batch_rows) {
+    constexpr int N = Vec<TI>::N;
     const int lane = threadIdx.x & 31;
     const int64_t row0 = d_batch ? (int64_t)(*d_batch) * batch_rows : 0;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
     for (int64_t p = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); p < p_out; p += warps) {
         const int32_t c0 = cbeg[p], d = cdeg[p];
-        const TI* self = in + (row0 + (rowmap ? rowmap[p] : p)) * in_stride;
-        for (int c = lane * 4; c < dim; c += 128) {
-            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int32_t j = 0; j < d; ++j) {
-                const int64_t q = c0 + j;
-                acc = f4add(acc, V4<TI>::load(in + (row0 + (rowmap ? rowmap[q] : q)) * in_stride + c));
+        const TI* self = in + (row0 + (rowmap ? __ldg(rowmap + p) : p)) * in_stride;
+        for (int c = lane * N; c < dim; c += 32 * N) {
+            float acc[N], v[N];
+#pragma unroll
+            for (int i = 0; i < N; ++i) acc[i] = 0.f;
+            const uint4 sr = rload(self + c);
+            int32_t j = 0;
+            for (; j + 4 <= d; j += 4) {
+                uint4 w[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int64_t q = c0 + j + u;
+                    w[u] = rload(in + (row0 + (rowmap ? __ldg(rowmap + q) : q)) * in_stride + c);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    unpack(w[u], v);
+#pragma unroll
+                    for (int i = 0; i < N; ++i) acc[i] += RELU ? fmaxf(v[i], 0.f) : v[i];
+                }
             }
-            const float4 sv = V4<TI>::load(self + c);
+            for (; j < d; ++j) {
+                const int64_t q = c0 + j;
+                unpack(rload(in + (row0 + (rowmap ? __ldg(rowmap + q) : q)) * in_stride + c), v);
+#pragma unroll
+                for (int i = 0; i < N; ++i) acc[i] += RELU ? fmaxf(v[i], 0.f) : v[i];
+            }
+            unpack(sr, v);
+            if (RELU) {
+#pragma unroll
+                for (int i = 0; i < N; ++i) v[i] = fmaxf(v[i], 0.f);
+            }
             TO* o = out + p * out_stride;
             if (MODE == 0) {
-                V4<TO>::store(o + c, sv);
-                V4<TO>::store(o + dim + c, f4mul(acc, d ? 1.0f / (float)d : 0.0f));
+                vstore<N>(o + c, v, 1.0f);
+                vstore<N>(o + dim + c, acc, d ? 1.0f / (float)d : 0.0f);
             } else {
-                V4<TO>::store(o + c, f4mul(f4add(sv, acc), 1.0f / (float)(d + 1)));
+#pragma unroll
+                for (int i = 0; i < N; ++i) acc[i] += v[i];
+                vstore<N>(o + c, acc, 1.0f / (float)(d + 1));
             }
         }
     }
 }
 
-// backward of the aggregation, fused with the ReLU mask of the input activations:
-//   g[q] = [h[q] > 0] * ( cs(q) * dA[q, self cols]  (q < p_out)
-//                       + cc(parent) * dA[parent(q), child cols]  (q has a parent) )
-// SAGE: self cols [0, dim), child cols [dim, 2 dim), cs = 1, cc = 1/deg(parent)
-// GCN:  both [0, dim), cs = 1/(deg(q)+1), cc = 1/(deg(parent)+1)
+// backward of the aggregation, fused with the ReLU mask of the input pre-activations z.
+// Row q of g (q < p_in) receives cs(q) * dA[q, self cols] when q < p_out and
+// cc(p) * dA[p, child cols] when q is a child of p:
+//   SAGE: self cols [0, dim), child cols [dim, 2 dim), cs = 1, cc = 1/deg(p)
+//   GCN:  both [0, dim), cs = 1/(deg(q)+1), cc = 1/(deg(p)+1)
+// and g[q] = [z[q] > 0] * that. Work is parent-centric — a warp takes a parent p, loads
+// dA[p, child cols] once and walks its consecutive children, 4 rows in flight — plus
+// warps for the level-0 rows (no parent) and for 32-row chunks of every level, which
+// zero the padded rows (no parent, no gradient) past the batch's count.
+struct TreeBwd {
+    const void* dA;
+    int64_t dA_stride;
+    int dim;
+    const int32_t* cbeg;
+    const int32_t* cdeg;
+    int64_t p_out, p_in;
+    const void* h;
+    int64_t h_stride;
+    void* g;
+    int64_t g_stride;
+    int nlev;  // levels spanned by rows [0, p_in)
+    int64_t base[GC_TREE_MAX_LEVELS + 1];
+    int64_t chunk0[GC_TREE_MAX_LEVELS + 1];  // first zeroing task of level k (k >= 1)
+    const int32_t* level_counts;
+};
+
 template <typename T, int MODE>
-__global__ void __launch_bounds__(256) k_tree_aggregate_bwd(const T* __restrict__ dA, int64_t dA_stride, int dim,
-                                                            const int32_t* __restrict__ parent,
-                                                            const int32_t* __restrict__ cdeg, int64_t p_out,
-                                                            int64_t p_in, const T* __restrict__ h, int64_t h_stride,
-                                                            T* __restrict__ g, int64_t g_stride) {
+__device__ __forceinline__ void bwd_row(const TreeBwd& a, int64_t q, float cs, const uint4& pr, float cc, int c,
+                                        uint4 self_raw, uint4 z_raw) {
+    constexpr int N = Vec<T>::N;
+    float v[N], fa[N], fz[N];
+    if (cc != 0.f) {
+        unpack(pr, fa);
+#pragma unroll
+        for (int i = 0; i < N; ++i) v[i] = fa[i] * cc;
+    } else {
+#pragma unroll
+        for (int i = 0; i < N; ++i) v[i] = 0.f;
+    }
+    if (cs != 0.f) {
+        unpack(self_raw, fa);
+#pragma unroll
+        for (int i = 0; i < N; ++i) v[i] += fa[i] * cs;
+    }
+    if (a.h) {
+        unpack(z_raw, fz);
+#pragma unroll
+        for (int i = 0; i < N; ++i) v[i] = fz[i] > 0.f ? v[i] : 0.f;
+    }
+    vstore<N>(static_cast<T*>(a.g) + q * a.g_stride + c, v, 1.0f);
+}
+
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256, 4) k_tree_aggregate_bwd(TreeBwd a, int64_t tasks) {
+    constexpr int N = Vec<T>::N;
     const int lane = threadIdx.x & 31;
+    const T* dA = static_cast<const T*>(a.dA);
+    const T* h = static_cast<const T*>(a.h);
+    const int child_col = MODE == 0 ? a.dim : 0;
+    const int64_t B0 = a.base[1] < a.p_in ? a.base[1] : a.p_in;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
-    for (int64_t q = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); q < p_in; q += warps) {
-        const int32_t par = parent[q];
-        float cs = 0.f, cc = 0.f;
-        if (q < p_out) cs = MODE == 0 ? 1.0f : 1.0f / (float)(cdeg[q] + 1);
-        if (par >= 0) cc = MODE == 0 ? 1.0f / (float)cdeg[par] : 1.0f / (float)(cdeg[par] + 1);
-        const int child_col = MODE == 0 ? dim : 0;
-        for (int c = lane * 4; c < dim; c += 128) {
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (cs != 0.f) v = f4mul(V4<T>::load(dA + q * dA_stride + c), cs);
-            if (cc != 0.f) v = f4add(v, f4mul(V4<T>::load(dA + (int64_t)par * dA_stride + child_col + c), cc));
-            if (h) {
-                const float4 a = V4<T>::load(h + q * h_stride + c);
-                v.x = a.x > 0.f ? v.x : 0.f;
-                v.y = a.y > 0.f ? v.y : 0.f;
-                v.z = a.z > 0.f ? v.z : 0.f;
-                v.w = a.w > 0.f ? v.w : 0.f;
-            }
-            V4<T>::store(g + q * g_stride + c, v);
+    const uint4 zero = make_uint4(0, 0, 0, 0);
+    for (int64_t t = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); t < tasks; t += warps) {
+        if (t < B0) {  // level-0 row: self part only
+            const int64_t q = t;
+            const float cs = MODE == 0 ? 1.0f : 1.0f / (float)(a.cdeg[q] + 1);
+            for (int c = lane * N; c < a.dim; c += 32 * N)
+                bwd_row<T, MODE>(a, q, q < a.p_out ? cs : 0.f, zero, 0.f, c,
+                                 q < a.p_out ? rload(dA + q * a.dA_stride + c) : zero,
+                                 h ? rload(h + q * a.h_stride + c) : zero);
+            continue;
         }
+        if (t < B0 + a.p_out) {  // parent p: its consecutive children
+            const int64_t p = t - B0;
+            const int32_t c0 = a.cbeg[p], d = a.cdeg[p];
+            if (d == 0) continue;
+            const float cc = MODE == 0 ? 1.0f / (float)d : 1.0f / (float)(d + 1);
+            for (int c = lane * N; c < a.dim; c += 32 * N) {
+                const uint4 pr = rload(dA + p * a.dA_stride + child_col + c);
+                constexpr int RU = sizeof(T) == 2 ? 2 : 4;  // rows in flight (bf16: 64 registers)
+                int32_t j = 0;
+                for (; j < d; j += RU) {
+                    uint4 sr[RU], zr[RU];
+                    float cs[RU];
+#pragma unroll
+                    for (int u = 0; u < RU; ++u) {
+                        const int64_t q = c0 + j + u;
+                        sr[u] = zr[u] = zero;
+                        cs[u] = 0.f;
+                        if (j + u < d) {
+                            if (q < a.p_out) {
+                                cs[u] = MODE == 0 ? 1.0f : 1.0f / (float)(a.cdeg[q] + 1);
+                                sr[u] = rload(dA + q * a.dA_stride + c);
+                            }
+                            if (h) zr[u] = rload(h + q * a.h_stride + c);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < RU; ++u)
+                        if (j + u < d) bwd_row<T, MODE>(a, c0 + j + u, cs[u], pr, cc, c, sr[u], zr[u]);
+                }
+            }
+            continue;
+        }
+        // zeroing task: 32 rows of level k past the batch's count (padding: no parent)
+        const int64_t z = t - B0 - a.p_out;
+        int k = 1;
+        while (k + 1 < a.nlev && z >= a.chunk0[k + 1]) ++k;
+        const int64_t r0 = a.base[k] + (z - a.chunk0[k]) * 32;
+        const int64_t first_pad = a.base[k] + a.level_counts[k];
+        const int64_t r1 = min(r0 + 32, min(a.base[k + 1], a.p_in));
+        for (int64_t q = max(r0, first_pad); q < r1; ++q)
+            for (int c = lane * N; c < a.dim; c += 32 * N)
+                *reinterpret_cast<uint4*>(static_cast<T*>(a.g) + q * a.g_stride + c) = zero;
     }
 }
 
@@ -221,8 +355,8 @@ static inline unsigned warp_grid(int64_t rows) {
 extern "C" {
 
 int gc_tree_stage(const gc_tree_src_t* src, const int32_t* d_batch, int32_t* d_loc, int32_t* d_cbeg, int32_t* d_cdeg,
-                  int32_t* d_parent, int64_t* d_labels, void* stream) {
-    GC_REQUIRE(src && d_batch && d_loc && d_parent, GC_ERR_VALUE, "gc_tree_stage: null pointer");
+                  int32_t* d_level_counts, int64_t* d_labels, void* stream) {
+    GC_REQUIRE(src && d_batch && d_loc && d_level_counts, GC_ERR_VALUE, "gc_tree_stage: null pointer");
     GC_REQUIRE(src->hops >= 0 && src->hops < GC_TREE_MAX_LEVELS, GC_ERR_VALUE, "gc_tree_stage: bad hop count");
     GC_REQUIRE(src->hops == 0 || (d_cbeg && d_cdeg), GC_ERR_VALUE, "gc_tree_stage: null child arrays");
     int64_t total = 0;
@@ -230,8 +364,8 @@ int gc_tree_stage(const gc_tree_src_t* src, const int32_t* d_batch, int32_t* d_l
     if (total == 0) return GC_OK;
     int64_t g = (total + 255) / 256;
     if (g > (int64_t)sm_count() * 32) g = (int64_t)sm_count() * 32;
-    k_tree_stage<<<(unsigned)g, 256, 0, as_stream(stream)>>>(*src, d_batch, total, d_loc, d_cbeg, d_cdeg, d_parent,
-                                                            d_labels);
+    k_tree_stage<<<(unsigned)g, 256, 0, as_stream(stream)>>>(*src, d_batch, total, d_loc, d_cbeg, d_cdeg,
+                                                            d_level_counts, d_labels);
     GC_CHECK_LAUNCH("gc_tree_stage");
     return GC_OK;
 }
@@ -239,45 +373,85 @@ int gc_tree_stage(const gc_tree_src_t* src, const int32_t* d_batch, int32_t* d_l
 int gc_tree_aggregate(const void* d_in, int in_dtype, int64_t in_stride, int dim, const int32_t* d_rowmap,
                       const int32_t* d_cbeg, const int32_t* d_cdeg, int64_t p_out, int mode, void* d_out, int out_dtype,
                       int64_t out_stride, const int32_t* d_batch, int64_t batch_rows, void* stream) {
-    GC_REQUIRE(dim >= 4 && dim % 4 == 0, GC_ERR_VALUE, "gc_tree_aggregate: dim must be a multiple of 4");
-    GC_REQUIRE(in_stride % 4 == 0 && out_stride % 4 == 0, GC_ERR_VALUE, "gc_tree_aggregate: strides must be multiples of 4");
-    GC_REQUIRE(mode == 0 || mode == 1, GC_ERR_VALUE, "gc_tree_aggregate: mode is 0 (SAGE) or 1 (GCN)");
+    GC_REQUIRE(mode >= 0 && mode <= 3, GC_ERR_VALUE,
+               "gc_tree_aggregate: mode is 0 (SAGE) or 1 (GCN), +2 for ReLU on the input rows");
     GC_REQUIRE((in_dtype == 0 || in_dtype == 1) && (out_dtype == 0 || out_dtype == 1), GC_ERR_VALUE,
                "gc_tree_aggregate: dtype is 0 (fp32) or 1 (bf16)");
+    const int vec = in_dtype == 0 ? 4 : 8;
+    GC_REQUIRE(dim >= vec && dim % vec == 0 && in_stride % vec == 0 && out_stride % vec == 0, GC_ERR_VALUE,
+               "gc_tree_aggregate: dim and strides must be multiples of 16 bytes of the input type");
+    GC_REQUIRE(in_dtype == out_dtype || in_dtype == 0, GC_ERR_VALUE, "gc_tree_aggregate: bf16 -> fp32 unsupported");
     if (p_out <= 0) return GC_OK;
     const unsigned g = warp_grid(p_out);
     cudaStream_t s = as_stream(stream);
-#define GC_AGG(TI, TO, M)                                                                                           \
-    k_tree_aggregate<TI, TO, M><<<g, 256, 0, s>>>(static_cast<const TI*>(d_in), in_stride, dim, d_rowmap, d_cbeg, \
-                                                  d_cdeg, p_out, static_cast<TO*>(d_out), out_stride, d_batch,     \
-                                                  batch_rows)
+    const int m = mode & 1;
+    const bool relu = (mode & 2) != 0;
+#define GC_AGG(TI, TO, M, R)                                                                                        \
+    k_tree_aggregate<TI, TO, M, R><<<g, 256, 0, s>>>(static_cast<const TI*>(d_in), in_stride, dim, d_rowmap,       \
+                                                     d_cbeg, d_cdeg, p_out, static_cast<TO*>(d_out), out_stride,    \
+                                                     d_batch, batch_rows)
+#define GC_AGG2(TI, TO)                                  \
+    if (m == 0) {                                        \
+        if (relu) GC_AGG(TI, TO, 0, true); else GC_AGG(TI, TO, 0, false); \
+    } else {                                             \
+        if (relu) GC_AGG(TI, TO, 1, true); else GC_AGG(TI, TO, 1, false); \
+    }
     using bf = __nv_bfloat16;
-    if (in_dtype == 0 && out_dtype == 0) { if (mode == 0) GC_AGG(float, float, 0); else GC_AGG(float, float, 1); }
-    else if (in_dtype == 0) { if (mode == 0) GC_AGG(float, bf, 0); else GC_AGG(float, bf, 1); }
-    else if (out_dtype == 1) { if (mode == 0) GC_AGG(bf, bf, 0); else GC_AGG(bf, bf, 1); }
-    else { if (mode == 0) GC_AGG(bf, float, 0); else GC_AGG(bf, float, 1); }
+    if (in_dtype == 0 && out_dtype == 0) { GC_AGG2(float, float) }
+    else if (in_dtype == 0) { GC_AGG2(float, bf) }
+    else { GC_AGG2(bf, bf) }
+#undef GC_AGG2
 #undef GC_AGG
     GC_CHECK_LAUNCH("gc_tree_aggregate");
     return GC_OK;
 }
 
 int gc_tree_aggregate_backward(const void* d_dA, int dtype, int64_t dA_stride, int dim, int mode,
-                               const int32_t* d_parent, const int32_t* d_cdeg, int64_t p_out, int64_t p_in,
-                               const void* d_h, int64_t h_stride, void* d_g, int64_t g_stride, void* stream) {
-    GC_REQUIRE(dim >= 4 && dim % 4 == 0, GC_ERR_VALUE, "gc_tree_aggregate_backward: dim must be a multiple of 4");
+                               const int32_t* d_cbeg, const int32_t* d_cdeg, int64_t p_out, int64_t p_in,
+                               const void* d_h, int64_t h_stride, void* d_g, int64_t g_stride, int nlevels,
+                               const int64_t* level_caps, const int32_t* d_level_counts, void* stream) {
     GC_REQUIRE(mode == 0 || mode == 1, GC_ERR_VALUE, "gc_tree_aggregate_backward: mode is 0 (SAGE) or 1 (GCN)");
     GC_REQUIRE(dtype == 0 || dtype == 1, GC_ERR_VALUE, "gc_tree_aggregate_backward: dtype is 0 (fp32) or 1 (bf16)");
+    const int vec = dtype == 0 ? 4 : 8;
+    GC_REQUIRE(dim >= vec && dim % vec == 0 && dA_stride % vec == 0 && g_stride % vec == 0 && h_stride % vec == 0,
+               GC_ERR_VALUE, "gc_tree_aggregate_backward: dim and strides must be multiples of 16 bytes");
+    GC_REQUIRE(nlevels >= 1 && nlevels <= GC_TREE_MAX_LEVELS && level_caps && d_level_counts, GC_ERR_VALUE,
+               "gc_tree_aggregate_backward: bad level description");
     GC_REQUIRE(p_out <= p_in, GC_ERR_VALUE, "gc_tree_aggregate_backward: p_out > p_in");
     if (p_in <= 0) return GC_OK;
-    const unsigned g = warp_grid(p_in);
+    TreeBwd a{};
+    a.dA = d_dA;
+    a.dA_stride = dA_stride;
+    a.dim = dim;
+    a.cbeg = d_cbeg;
+    a.cdeg = d_cdeg;
+    a.p_out = p_out;
+    a.p_in = p_in;
+    a.h = d_h;
+    a.h_stride = h_stride;
+    a.g = d_g;
+    a.g_stride = g_stride;
+    a.nlev = nlevels;
+    a.level_counts = d_level_counts;
+    a.base[0] = 0;
+    for (int k = 0; k < nlevels; ++k) a.base[k + 1] = a.base[k] + level_caps[k];
+    GC_REQUIRE(a.base[nlevels] == p_in, GC_ERR_VALUE, "gc_tree_aggregate_backward: level caps must sum to p_in");
+    int64_t chunks = 0;
+    for (int k = 1; k < nlevels; ++k) {
+        a.chunk0[k] = chunks;
+        chunks += (level_caps[k] + 31) / 32;
+    }
+    a.chunk0[nlevels] = chunks;
+    const int64_t tasks = (p_in < level_caps[0] ? p_in : level_caps[0]) + p_out + chunks;
+    const unsigned g = warp_grid(tasks);
     cudaStream_t s = as_stream(stream);
-#define GC_BWD(T, M)                                                                                                \
-    k_tree_aggregate_bwd<T, M><<<g, 256, 0, s>>>(static_cast<const T*>(d_dA), dA_stride, dim, d_parent, d_cdeg, \
-                                                 p_out, p_in, static_cast<const T*>(d_h), h_stride,              \
-                                                 static_cast<T*>(d_g), g_stride)
-    if (dtype == 0) { if (mode == 0) GC_BWD(float, 0); else GC_BWD(float, 1); }
-    else { if (mode == 0) GC_BWD(__nv_bfloat16, 0); else GC_BWD(__nv_bfloat16, 1); }
-#undef GC_BWD
+    if (dtype == 0) {
+        if (mode == 0) k_tree_aggregate_bwd<float, 0><<<g, 256, 0, s>>>(a, tasks);
+        else k_tree_aggregate_bwd<float, 1><<<g, 256, 0, s>>>(a, tasks);
+    } else {
+        if (mode == 0) k_tree_aggregate_bwd<__nv_bfloat16, 0><<<g, 256, 0, s>>>(a, tasks);
+        else k_tree_aggregate_bwd<__nv_bfloat16, 1><<<g, 256, 0, s>>>(a, tasks);
+    }
     GC_CHECK_LAUNCH("gc_tree_aggregate_backward");
     return GC_OK;
 }

@@ -217,19 +217,23 @@ class TreeTrainer:
 
     Every position of the sampled tree has exactly one parent, so the whole backward is
     gathers, no atomics: layer l's neighbour aggregation (gc_tree_aggregate) writes
-    A_l = [h_self, mean(h_children)] (GCN: the closed-neighbourhood mean), one cuBLAS
-    GEMM + bias + ReLU gives h_{l+1}; backward is dW = g^T A, dA = g W and
-    gc_tree_aggregate_backward, which routes dA back to each position from its own row
-    and its parent's (fused with the ReLU mask). The first layer reads its inputs straight
-    from the window's gathered feature rows through the relabelled ids. Batch b of the
-    window is staged (gc_tree_stage) into padded fixed-shape buffers — padded positions
-    have no children and no parent, padded seeds no label — so the whole step
-    (stage, forward, backward, SGD) is one CUDA graph, replayed for every batch with the
-    batch index read from device memory: no host work and no sync per batch.
+    A_l = [h_self, mean(h_children), 1] (GCN: [closed-neighbourhood mean, 1]) and one
+    cuBLAS GEMM with the bias folded into the weights (W_ext = [W | b]) gives the
+    pre-activations z_{l+1}; ReLU is applied when the next layer reads them, and the
+    backward mask is z > 0. Backward: dW_ext = g^T A_l (the bias gradient is the ones
+    column's), dA = g W and gc_tree_aggregate_backward, which routes dA back to each
+    position from its own row and its parent's (fused with the mask). The first layer
+    reads its inputs straight from the window's gathered feature rows through the
+    relabelled ids. Batch b is staged (gc_tree_stage) into padded fixed-shape buffers —
+    padded positions have no children and no parent, padded seeds no label — so the whole
+    step (stage, forward, backward, SGD) is one CUDA graph, replayed for every batch with
+    the batch index read from device memory: no host work and no sync per batch.
 
-    Across ranks (DDP) the gradients live in one flat buffer: one all-reduce per step
-    (NCCL, or gloo for the CPU tests), averaged over the ranks that had a batch; a rank
-    whose tablet ran out of batches still joins each step with a zero gradient.
+    The model's parameters become views into one flat fp32 buffer laid out as the GEMMs
+    want it (a layer's self/neighbour weights and bias are column blocks of W_ext); the
+    gradients live in a matching flat buffer, so across ranks (DDP) one all-reduce per
+    step (NCCL, or gloo for the CPU tests) averages them over the ranks that had a batch
+    — a rank whose tablet ran out of batches joins each step with a zero gradient.
     Semantics are GraphSAGE.forward + F.cross_entropy + torch.optim.SGD(lr) (no
     momentum), which tests/test_gpu_train.py checks step by step."""
 
@@ -263,7 +267,8 @@ class TreeTrainer:
         self.loc = torch.zeros(P, dtype=i32, device=dev)
         self.cbeg = torch.zeros(max(self.base[L], 1), dtype=i32, device=dev)
         self.cdeg = torch.zeros(max(self.base[L], 1), dtype=i32, device=dev)
-        self.parent = torch.zeros(P, dtype=i32, device=dev)
+        self.level_counts = torch.zeros(L + 1, dtype=i32, device=dev)
+        self.caps_c = (_lib.I64 * (L + 1))(*caps)
         self.labels_b = torch.zeros(caps[0], dtype=torch.int64, device=dev)
         src = _lib.GcTreeSrc()
         src.hops = L
@@ -282,85 +287,98 @@ class TreeTrainer:
         self.labels = labels.to(device=dev, dtype=torch.int64).contiguous()
         src.labels = self.labels.data_ptr()
         self.src = src
-        # activations: A_l [base_{L-l}, in_cols], h_{l+1} [base_{L-l}, hidden]
-        self.A, self.H = [], []
-        for l, layer in enumerate(self.layers):
-            rows = self.base[L - l]
-            cols = self._weights(layer)[0].shape[1]  # 2 d_in (SAGE: self | neighbour mean) or d_in (GCN)
-            self.A.append(torch.zeros((rows, cols), dtype=self.act, device=dev))
-            self.H.append(torch.zeros((rows, self._weights(layer)[0].shape[0]), dtype=self.act, device=dev))
-        # parameters and gradients: one flat buffer each (+1 slot: ranks contributing a batch)
-        self.params = [p for p in model.parameters()]
-        n = sum(p.numel() for p in self.params)
-        self.flat = torch.empty(n, dtype=torch.float32, device=dev)
-        self.gflat = torch.zeros(n + 1, dtype=torch.float32, device=dev)
+        # per layer: input width d, aggregate width cols (2d SAGE / d GCN), + ones column
+        # (the bias), padded to 8 so every row is 16-byte aligned in bf16
+        self.shape = []
+        for layer in self.layers:
+            if isinstance(layer, SAGELayer):
+                hid, d = layer.lin_self.weight.shape
+                cols = 2 * d
+            else:
+                hid, d = layer.lin.weight.shape
+                cols = d
+            self.shape.append((d, cols, (cols + 1 + 7) // 8 * 8, hid))
+        # flat parameters: W_ext of every layer [hid, ext], then the classifier W, b
+        cls = model.classifier
+        sizes = [hid * ext for (_, _, ext, hid) in self.shape] + [cls.weight.numel(), cls.bias.numel()]
+        n = sum(sizes)
+        self.flat = torch.zeros(n, dtype=torch.float32, device=dev)
+        self.gflat = torch.zeros(n + 1, dtype=torch.float32, device=dev)  # + ranks contributing this step
+        self.W, self.dW = [], []
         o = 0
-        self.grad = {}
         with torch.no_grad():
-            for p in self.params:
-                k = p.numel()
-                self.flat[o : o + k].copy_(p.detach().reshape(-1))
-                p.data = self.flat[o : o + k].view_as(p)
-                self.grad[id(p)] = self.gflat[o : o + k].view_as(p)
-                o += k
+            for layer, (d, cols, ext, hid) in zip(self.layers, self.shape):
+                W = self.flat[o : o + hid * ext].view(hid, ext)
+                self.dW.append(self.gflat[o : o + hid * ext].view(hid, ext))
+                o += hid * ext
+                if isinstance(layer, SAGELayer):
+                    parts = [(layer.lin_self.weight, W[:, :d]), (layer.lin_neigh.weight, W[:, d : 2 * d]),
+                             (layer.lin_self.bias, W[:, cols])]
+                else:
+                    parts = [(layer.lin.weight, W[:, :d]), (layer.lin.bias, W[:, cols])]
+                for param, view in parts:
+                    view.copy_(param.detach())
+                    param.data = view
+                self.W.append(W)
+            k = cls.weight.numel()
+            self.Wc = self.flat[o : o + k].view_as(cls.weight)
+            self.dWc = self.gflat[o : o + k].view_as(cls.weight)
+            self.Wc.copy_(cls.weight.detach())
+            cls.weight.data = self.Wc
+            o += k
+            k = cls.bias.numel()
+            self.bc = self.flat[o : o + k]
+            self.dbc = self.gflat[o : o + k]
+            self.bc.copy_(cls.bias.detach())
+            cls.bias.data = self.bc
         self.gflat[n] = 1.0
+        # activations: A_l [base_{L-l}, ext] with the ones column; z_{l+1} [base_{L-l}, hid]
+        self.A, self.Z = [], []
+        for l, (d, cols, ext, hid) in enumerate(self.shape):
+            rows = self.base[L - l]
+            A = torch.zeros((rows, ext), dtype=self.act, device=dev)
+            A[:, cols] = 1.0
+            self.A.append(A)
+            self.Z.append(torch.zeros((rows, hid), dtype=self.act, device=dev))
         self.loss = torch.zeros((), dtype=torch.float32, device=dev)
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.backend = dist.get_backend(group) if self.world > 1 else None
         self.use_graph = use_graph
         self._graphs = None
+        self._graph_feats = None
         self.steps = 0
-
-    @staticmethod
-    def _weights(layer):
-        if isinstance(layer, SAGELayer):
-            return torch.cat([layer.lin_self.weight, layer.lin_neigh.weight], 1), layer.lin_self.bias
-        return layer.lin.weight, layer.lin.bias
-
-    def _grad_w(self, layer, dW: torch.Tensor, db: torch.Tensor) -> None:
-        if isinstance(layer, SAGELayer):
-            d = layer.lin_self.weight.shape[1]
-            self.grad[id(layer.lin_self.weight)].copy_(dW[:, :d])
-            self.grad[id(layer.lin_neigh.weight)].copy_(dW[:, d:])
-            self.grad[id(layer.lin_self.bias)].copy_(db)
-        else:
-            self.grad[id(layer.lin.weight)].copy_(dW)
-            self.grad[id(layer.lin.bias)].copy_(db)
 
     # ------------------------------------------------------------------ one step
     def _fwd_bwd(self) -> None:
         from . import _lib
 
         lib, s = _lib.lib(), _lib.stream_handle()
-        sp, L, act = self.sp, self.L, self.act
+        L, act = self.L, self.act
         _lib.check(lib.gc_tree_stage(self.src, self.b_dev.data_ptr(), self.loc.data_ptr(), self.cbeg.data_ptr(),
-                                     self.cdeg.data_ptr(), self.parent.data_ptr(), self.labels_b.data_ptr(), s),
+                                     self.cdeg.data_ptr(), self.level_counts.data_ptr(), self.labels_b.data_ptr(), s),
                    "tree_stage")
         feats = self._features
         dim = feats.shape[-1]
-        Ws = []
-        for l, layer in enumerate(self.layers):
-            W, b = self._weights(layer)
-            Wa, ba = W.detach().to(act), b.detach().to(act)
-            Ws.append(Wa)
+        Wa = [W.to(act) for W in self.W]
+        for l in range(L):
+            d, cols, ext, hid = self.shape[l]
             A, rows = self.A[l], self.base[L - l]
             if l == 0:  # children rows straight from the gathered features of batch b
                 _lib.check(lib.gc_tree_aggregate(feats.data_ptr(), 0, dim, dim, self.loc.data_ptr(),
                                                  self.cbeg.data_ptr(), self.cdeg.data_ptr(), rows, self.mode,
                                                  A.data_ptr(), self.dt, A.stride(0), self.b_dev.data_ptr(),
                                                  feats.stride(0) // dim, s), "tree_aggregate")
-            else:
-                h = self.H[l - 1]
-                _lib.check(lib.gc_tree_aggregate(h.data_ptr(), self.dt, h.stride(0), h.shape[1], None,
-                                                 self.cbeg.data_ptr(), self.cdeg.data_ptr(), rows, self.mode,
+            else:  # ReLU of the previous layer's pre-activations, applied as they are read
+                z = self.Z[l - 1]
+                _lib.check(lib.gc_tree_aggregate(z.data_ptr(), self.dt, z.stride(0), z.shape[1], None,
+                                                 self.cbeg.data_ptr(), self.cdeg.data_ptr(), rows, self.mode + 2,
                                                  A.data_ptr(), self.dt, A.stride(0), None, 0, s), "tree_aggregate")
-            torch.addmm(ba, A, Wa.t(), out=self.H[l])
-            self.H[l].relu_()
+            torch.mm(A, Wa[l].t(), out=self.Z[l])
         B = self.base[1]
-        top = self.H[L - 1][:B]
-        cls = self.model.classifier
-        logits = _mm_f32(top, cls.weight.detach().to(act).t()) + cls.bias.detach()
+        ztop = self.Z[L - 1][:B]
+        top = torch.relu(ztop)
+        logits = _mm_f32(top, self.Wc.to(act).t()) + self.bc
         y = self.labels_b
         valid = (y >= 0).to(torch.float32)
         nvalid = valid.sum().clamp_(min=1.0)
@@ -371,21 +389,22 @@ class TreeTrainer:
         dlog = logp.exp_()
         dlog.scatter_add_(1, yc.view(-1, 1), -torch.ones_like(valid).view(-1, 1))
         dlog.mul_((valid / nvalid).view(-1, 1))
-        self.grad[id(cls.weight)].copy_(_mm_f32(dlog.t().to(act), top))
-        self.grad[id(cls.bias)].copy_(dlog.sum(0))
-        g = (dlog.to(act) @ cls.weight.detach().to(act)) * (top > 0)
+        self.dWc.copy_(_mm_f32(dlog.t().to(act), top))
+        torch.sum(dlog, 0, out=self.dbc)
+        g = (dlog.to(act) @ self.Wc.to(act)) * (ztop > 0)
         for l in range(L - 1, -1, -1):
-            layer = self.layers[l]
-            self._grad_w(layer, _mm_f32(g.t(), self.A[l]), g.float().sum(0))
+            d, cols, ext, hid = self.shape[l]
+            self.dW[l].copy_(_mm_f32(g.t(), self.A[l]))  # the ones column gives the bias gradient
             if l == 0:
                 break
-            dA = g @ Ws[l]
-            h = self.H[l - 1]
-            g_in = torch.empty_like(h)
-            _lib.check(lib.gc_tree_aggregate_backward(dA.data_ptr(), self.dt, dA.stride(0), h.shape[1], self.mode,
-                                                      self.parent.data_ptr(), self.cdeg.data_ptr(), dA.shape[0],
-                                                      h.shape[0], h.data_ptr(), h.stride(0), g_in.data_ptr(),
-                                                      g_in.stride(0), s), "tree_aggregate_backward")
+            dA = g @ Wa[l][:, :cols]
+            z = self.Z[l - 1]
+            g_in = torch.empty_like(z)
+            _lib.check(lib.gc_tree_aggregate_backward(dA.data_ptr(), self.dt, dA.stride(0), z.shape[1], self.mode,
+                                                      self.cbeg.data_ptr(), self.cdeg.data_ptr(), dA.shape[0],
+                                                      z.shape[0], z.data_ptr(), z.stride(0), g_in.data_ptr(),
+                                                      g_in.stride(0), L - l + 1, self.caps_c,
+                                                      self.level_counts.data_ptr(), s), "tree_aggregate_backward")
             g = g_in
 
     def _update(self) -> None:
