@@ -41,7 +41,19 @@ C3 = {
     "batch_size": 1024,
     "training_fraction": 0.1,
     "master_seed": 7,
+    "budget_frac_per_gpu": 0.1,
+    "window": 256,  # batches per launch window
+    "feat_rows_cap": 60_000,  # distinct rows per batch the window buffers hold (checked before timing)
 }
+# BASELINE configs[3] and [4]: the same flow at their shapes (python bench.py --tier-workload c4|c5)
+C4 = {**C3, "workload": "C4 UK-2007-shaped synthetic (GCN 2-layer input): 105M vertices, 3.7B edges, 128-d; "
+                        "topology partially host-resident (UVA), cache partitioned over the clique",
+      "num_vertices": 105_000_000, "avg_degree": 35, "window": 128, "feat_rows_cap": 160_000}
+C5 = {**C3, "workload": "C5 Friendster-shaped synthetic: 65M vertices, 3.6B edges, 256-d features, tight HBM budget "
+                        "(5% of topology+feature bytes per GPU)",
+      "num_vertices": 65_000_000, "avg_degree": 55, "feature_dim": 256, "budget_frac_per_gpu": 0.05, "window": 64,
+      "feat_rows_cap": 160_000}
+TIER_WORKLOADS = {"c3": C3, "c4": C4, "c5": C5}
 PCIE_NOMINAL_GBS = 64.0  # PCIe Gen5 x16, north_star's tier roofline
 NVLINK_GBS = 900.0  # NVLink 5 per direction
 CONFIG = {
@@ -67,6 +79,8 @@ def parse():
     ap.add_argument("--window", type=int, default=0,
                     help="batches per launch window (0 = whole epoch / lanes*2 windows when lanes > 1)")
     ap.add_argument("--lanes", type=int, default=1, help="concurrent window lanes (inter-batch pipeline streams)")
+    ap.add_argument("--mem-priority", type=int, default=0,
+                    help="1: each window's dedup/relabel/gather on a high-priority stream (overlaps the next hop)")
     ap.add_argument("--graph", type=int, default=1, help="1: each timed epoch is one CUDA-graph launch")
     ap.add_argument("--visited", default="auto", choices=["auto", "dense", "sparse"],
                     help="visited-set layout for dedup (auto: sparse above 4M vertices)")
@@ -76,12 +90,15 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--train-epochs", type=int, default=1, help="GraphSAGE epochs timed after the data-path bench")
     ap.add_argument("--c3-scale", type=float, default=1.0,
-                    help="C3 three-tier section (papers100M shape x scale; 0 skips it)")
+                    help="three-tier section (the --tier-workload shape x scale; 0 skips it)")
+    ap.add_argument("--tier-workload", default="c3", choices=sorted(TIER_WORKLOADS),
+                    help="configuration of the three-tier section (BASELINE configs[2..4])")
     ap.add_argument("--c3-steps", type=int, default=3)
     ap.add_argument("--c3-warmup", type=int, default=3)
     ap.add_argument("--c3-presample-epochs", type=int, default=4)
-    ap.add_argument("--c3-budget-frac", type=float, default=0.1,
-                    help="per-GPU cache budget / (topology + feature bytes); the clique's is world x this")
+    ap.add_argument("--c3-budget-frac", type=float, default=0.0,
+                    help="per-GPU cache budget / (topology + feature bytes), 0 = the workload's; the clique's is "
+                         "world x this")
     return ap.parse_args()
 
 
@@ -379,7 +396,7 @@ def run_b200(args):
     # window's gather buffer small, and the run checks it never overflowed
     sparse = None if args.visited == "auto" else args.visited == "sparse"
     pipe = SampleGatherPipeline(g, cfg, store, len(pool), window=window, feat_rows_cap=65536, lanes=args.lanes,
-                                sparse_visited=sparse)
+                                sparse_visited=sparse, mem_priority=bool(args.mem_priority))
     root = KeyedRng(cfg.seed)
     clique, local_idx = layout.gpu_position(rank)
     plans = [pipe.plan_epoch(pool, root.derive(e, clique, local_idx)) for e in range(args.warmup + args.steps)]
@@ -518,7 +535,7 @@ def run_b200(args):
     if args.c3_scale > 0:
         del pipe, seq, store, table
         torch.cuda.empty_cache()
-        line["c3_three_tier"] = c3_run(args, rank, local, world)
+        line[f"{args.tier_workload}_three_tier"] = c3_run(args, rank, local, world)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -526,7 +543,7 @@ def run_b200(args):
 
 
 def c3_run(args, rank, local, world):
-    """C3 (BASELINE configs[2]) through Legion's full flow, one process per GPU of one
+    """C3 (BASELINE configs[2]; C4/C5 with --tier-workload) through Legion's full flow, one process per GPU of one
     NVSwitch clique: per-rank presampling -> hotness merge -> CSLP plan -> each rank fills
     its own slabs -> CUDA IPC peer slabs (clique.build_clique_cache), the host tier one
     node-shared pinned table; then timed epochs through the three tiers. Reports
@@ -546,6 +563,8 @@ def c3_run(args, rank, local, world):
     from paper_2305_16588_b200.pipeline import SampleGatherPipeline, StageTimer
 
     t_setup = time.perf_counter()
+    C3 = TIER_WORKLOADS[args.tier_workload]
+    budget_frac = args.c3_budget_frac or C3["budget_frac_per_gpu"]
     multi = world > 1
     barrier = dist.barrier if multi else (lambda: None)
     n = int(round(C3["num_vertices"] * args.c3_scale))
@@ -558,7 +577,7 @@ def c3_run(args, rank, local, world):
     pool = pools[rank]
     feat = P.FeatureSpec(dim)
     total_bytes = g.num_edges * 4 + 8 * n + n * feat.row_bytes
-    budget = int(args.c3_budget_frac * total_bytes) * world
+    budget = int(budget_frac * total_bytes) * world
     spec = P.HardwareSpec(layout, clique_budget_bytes=budget)
     cfg = P.SamplingConfig(fanouts=tuple(C3["fanouts"]), batch_size=B, presample_epochs=args.c3_presample_epochs,
                            seed=P.derive_seed(seed, 4))
@@ -571,20 +590,22 @@ def c3_run(args, rank, local, world):
         torch.cuda.synchronize()
 
     run_id = os.environ.get("TORCHELASTIC_RUN_ID", "") + os.environ.get("MASTER_PORT", str(os.getpid()))
-    host = shared_host_table(f"gc_c3_{run_id}", (n, dim), torch.float32, local, fill=fill, barrier=barrier)
+    host = shared_host_table(f"gc_{args.tier_workload}_{run_id}", (n, dim), torch.float32, local, fill=fill,
+                             barrier=barrier)
     t0 = time.perf_counter()
     cr = build_clique_cache(g, pool, layout, cfg, feat, spec, host.tensor, rank=rank, world=world)
     torch.cuda.synchronize()
     t_cache = time.perf_counter() - t0
     nb = math.ceil(len(pool) / B)
-    pipe = SampleGatherPipeline(g, cfg, cr.features, len(pool), window=min(256, nb), feat_rows_cap=60_000,
+    win, fcap = min(C3["window"], nb), C3["feat_rows_cap"]
+    pipe = SampleGatherPipeline(g, cfg, cr.features, len(pool), window=win, feat_rows_cap=fcap,
                                 topology=cr.topology, lanes=2)
     root = P.KeyedRng(P.derive_seed(seed, 5))
     plans = [pipe.plan_epoch(pool, root.derive(e, 0, rank)) for e in range(args.c3_warmup + args.c3_steps)]
     timed = plans[args.c3_warmup :]
     # untimed passes over the timed epochs, one lane: algorithmic bytes, the capacity
     # check (before timing), per-stage device times
-    seq = SampleGatherPipeline(g, cfg, cr.features, len(pool), window=min(256, nb), feat_rows_cap=60_000,
+    seq = SampleGatherPipeline(g, cfg, cr.features, len(pool), window=win, feat_rows_cap=fcap,
                                topology=cr.topology, lanes=1)
     acc = {"sampling": 0, "dedup": 0, "gather": 0}
 
@@ -648,11 +669,11 @@ def c3_run(args, rank, local, world):
         "value": all_batches / (total_ms / 1000.0), "unit": "batches/s", "n_gpus": world,
         "steps": len(timed), "warmup": args.c3_warmup, "ms_per_step": total_ms / len(timed),
         "config": {**C3, "num_vertices": n, "num_edges": g.num_edges, "scale": args.c3_scale,
-                   "budget_bytes_clique": budget, "budget_frac_per_gpu": args.c3_budget_frac,
+                   "budget_bytes_clique": budget, "budget_frac_per_gpu": budget_frac,
                    "batches_per_step_per_gpu": nb, "window_batches": pipe.window, "lanes": pipe.lanes,
                    "cuda_graph": True, "parallelism": f"dp{world}, cache partitioned over {world} GPU(s)",
                    "host_tier": "one node-shared pinned table (/dev/shm + cudaHostRegister), UVA reads",
-                   "l2": "inputs (7 GB topology + 57 GB features at scale 1) far larger than L2"},
+                   "l2": "inputs (tens of GB of topology and features at scale 1) far larger than L2"},
         "plan": {"presample_epochs": cfg.presample_epochs, "alpha": cr.plan.alpha,
                  "topo_prefix_len": cr.estimate.topo_prefix_len, "feat_prefix_len": cr.estimate.feat_prefix_len,
                  "predicted_txn_total": cr.estimate.total_txns, "presample_batches": cr.presample_batches,
@@ -680,7 +701,8 @@ def c3_run(args, rank, local, world):
                                           seed=P.derive_seed(seed, 5))
         out["cpu_baseline"] = {"value": done / el, "unit": "batches/s", "cores": 1, "kind": kind,
                                "cpu_model": cpu_model(),
-                               "sample": f"first {done} batches of epoch 0 (C3, 1 core): gnncache.sample_batch + "
+                               "sample": f"first {done} batches of epoch 0 ({args.tier_workload.upper()}, 1 core): "
+                                         "gnncache.sample_batch + "
                                          "distinct_vertices + X[ids] from the host table"}
         out["verified"] = verify_epoch0(pipe, plans[0], ref)
     del pipe, plans, timed, cr

@@ -83,7 +83,7 @@ class SampleGatherPipeline:
     def __init__(self, graph: CsrGraph, cfg: SamplingConfig, store: FeatureStore | None, max_pool: int,
                  window: int | None = None, relabel: bool = True, feat_rows_cap: int | None = None,
                  placement: str = "hbm", topology=None, sparse_visited: bool | None = None, lanes: int = 1,
-                 defer_host: bool | None = None, overlap_relabel: bool = True):
+                 defer_host: bool | None = None, overlap_relabel: bool = True, mem_priority: bool = False):
         self.graph = graph
         self.cfg = cfg
         self.store = store
@@ -114,7 +114,12 @@ class SampleGatherPipeline:
         self.features = self.lane_features[0]
         # relabel overlaps the gather on a side stream per lane (None: back to back), so
         # one lane's relabel never queues behind another lane's compaction
-        self._relabel_sides = [torch.cuda.Stream() for _ in range(lanes)] if overlap_relabel else None
+        # mem_priority: a window's memory-bound stages (dedup, relabel, gather) run on a
+        # high-priority stream of its lane, so with lanes > 1 their CTAs take SM slots
+        # ahead of the next window's ALU-bound hop expansion as those slots free up
+        self.mem_streams = [torch.cuda.Stream(priority=-1) for _ in range(lanes)] if mem_priority else None
+        prio = -1 if mem_priority else 0
+        self._relabel_sides = [torch.cuda.Stream(priority=prio) for _ in range(lanes)] if overlap_relabel else None
         self._lane = 0
         self.feat_cap = self.sampler.ucap
         self.timer: StageTimer | None = None
@@ -228,6 +233,18 @@ class SampleGatherPipeline:
             sp.keys[:, :nb].copy_(plan.keys[w0:w1].t())
         sp.expand(hot, timer=self.timer)
         self.launches += max(H, 1)
+        if self.mem_streams is not None and self.timer is None:
+            lane_stream = torch.cuda.current_stream()
+            mem = self.mem_streams[self._lane]
+            mem.wait_stream(lane_stream)
+            with torch.cuda.stream(mem):
+                self._memory_stages(sp, nb, hot, w0, on_window)
+            lane_stream.wait_stream(mem)
+            return
+        self._memory_stages(sp, nb, hot, w0, on_window)
+
+    def _memory_stages(self, sp, nb, hot, w0, on_window) -> None:
+        H = len(self.cfg.fanouts)
         end = self._stage("unique_relabel")
         # relabel and gather both only need the compaction: with the side stream the two
         # HBM-bound passes share the GPU instead of running back to back
