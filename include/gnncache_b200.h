@@ -342,6 +342,9 @@ int gc_tier_account(const uint64_t* d_row_offsets, int64_t n, const uint64_t* d_
 /* Register host memory as mapped, read-only pinned memory (UVA host tier). */
 int gc_host_register(void* host_ptr, size_t bytes, void** d_alias);
 int gc_host_unregister(void* host_ptr);
+/* Copy `bytes` (a multiple of 4) from device memory into mapped pinned host memory with
+ * SM stores (no DMA engine: small reads that must not queue behind bulk D2H copies). */
+int gc_copy_d2h_mapped(const void* d_src, void* h_dst, uint64_t bytes, void* stream);
 
 /* Host tier through the CUDA VMM API (cuMemCreate, CU_MEM_LOCATION_TYPE_HOST_NUMA):
  * pinned host memory mapped for the CPU and every GPU at one address with the

@@ -160,4 +160,34 @@ int gc_host_free_numa(void* ptr, size_t mapped_bytes) {
     return drv(d.free_va(va, mapped_bytes), "cuMemAddressFree");
 }
 
+// Small device -> host reads that must not queue behind bulk DMA: the SMs store the
+// words straight into mapped pinned memory over PCIe (a window's per-batch sizes read
+// while the previous window's results are still draining through the copy engine).
+}  // extern "C"
+
+namespace gc {
+__global__ void k_copy_to_mapped(const uint32_t* __restrict__ src, uint32_t* dst, uint64_t words) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < words; i += (uint64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+    __threadfence_system();
+}
+}  // namespace gc
+
+extern "C" {
+
+int gc_copy_d2h_mapped(const void* d_src, void* h_dst, uint64_t bytes, void* stream) {
+    GC_REQUIRE(bytes % 4 == 0, GC_ERR_VALUE, "gc_copy_d2h_mapped: bytes must be a multiple of 4");
+    if (bytes == 0) return GC_OK;
+    GC_REQUIRE(d_src && h_dst, GC_ERR_VALUE, "gc_copy_d2h_mapped: null pointer");
+    void* d_dst = nullptr;
+    GC_TRY(cudaHostGetDevicePointer(&d_dst, h_dst, 0), "cudaHostGetDevicePointer");
+    const uint64_t words = bytes / 4;
+    unsigned grid = (unsigned)((words + 255) / 256);
+    if (grid > 64) grid = 64;
+    gc::k_copy_to_mapped<<<grid, 256, 0, as_stream(stream)>>>(static_cast<const uint32_t*>(d_src),
+                                                               static_cast<uint32_t*>(d_dst), words);
+    GC_CHECK_LAUNCH("gc_copy_d2h_mapped");
+    return GC_OK;
+}
+
 }  // extern "C"

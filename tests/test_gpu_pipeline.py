@@ -338,10 +338,13 @@ def test_epoch_graph_replay_tiered_matches_eager(lanes):
                 assert torch.equal(xa[bi, :u].cpu(), host_table[sa.unique[bi, :u].cpu().long() & 0xFFFFFFFF])
 
 
-@pytest.mark.parametrize("relabel,lanes", [(True, 1), (False, 1), (True, 2)])
-def test_window_to_host_packs_every_batch(relabel, lanes):
+@pytest.mark.parametrize("relabel,lanes,compact", [(True, 1, False), (False, 1, False), (True, 2, False),
+                                                    (True, 1, True), (False, 1, True)])
+def test_window_to_host_packs_every_batch(relabel, lanes, compact):
     """window_to_host: one packed pinned copy per array equals the per-batch slices of
-    the padded device buffers, batch boundaries included; staging is reused."""
+    the padded device buffers, batch boundaries included; staging is reused. compact:
+    relabelled ids travel as 16-bit values (global ids never do); wait=False returns an
+    event the host waits on before reading."""
     import paper_2305_16588_b200 as P
     from paper_2305_16588_b200.cache import FeatureStore
     from paper_2305_16588_b200.graph import synthetic_features_device
@@ -356,7 +359,10 @@ def test_window_to_host_packs_every_batch(relabel, lanes):
     staging, seen = {}, []
 
     def check(p, w0, nbw):
-        out = p.window_to_host(nbw, staging)
+        out = p.window_to_host(nbw, staging, compact_ids=compact, wait=not compact)
+        if compact:
+            out["ready"].synchronize()
+        assert out["local_bits"] == (16 if compact and relabel else 32)
         sp = p.sampler
         for b in range(nbw):
             u0, u1 = out["unique_ptr"][b : b + 2]
@@ -371,7 +377,11 @@ def test_window_to_host_packs_every_batch(relabel, lanes):
                 assert o1 - o0 == f + 1 and l1 - l0 == t
                 assert torch.equal(out["offsets"][h][o0:o1], sp.offsets[h][b, : f + 1].cpu())
                 ids = sp.local_nbrs[h] if relabel else sp.nbrs[h]
-                assert torch.equal(out["local"][h][l0:l1], ids[b, :t].cpu())
+                got = out["local"][h][l0:l1]
+                if out["local_bits"] == 16:
+                    assert got.dtype == torch.int16
+                    got = got.to(torch.int32) & 0xFFFF
+                assert torch.equal(got, ids[b, :t].cpu())
         seen.append(nbw)
 
     pipe.run_epoch(pipe.plan_epoch(pool, P.KeyedRng(3).derive(0, 0, 0)), on_window=check)
