@@ -253,12 +253,12 @@ class CpuPath:
         if self.R is not None:
             bs = self.R.sample_batch(self.g, seeds, self.cfg, self.stream.derive(self.role_sample, b))
             uniq = bs.distinct_vertices()
-            return uniq, self.table[uniq]
+            return uniq, self.table[uniq], [(h.offsets, h.neighbors) for h in bs.hops]
         O, g = self.O, self.g
         hops = O.sample_batch(g.row_offsets, g.col_indices, g.num_vertices, seeds, self.conf["fanouts"],
                               O.derive(self.gkey, 2, b))
         uniq = O.distinct_vertices(seeds, hops)
-        return uniq, O.gather(self.table, uniq)
+        return uniq, O.gather(self.table, uniq), [(off, nbr) for _, off, nbr in hops]
 
 
 def _seed():
@@ -714,8 +714,9 @@ def c3_run(args, rank, local, world):
 
 def verify_epoch0(pipe, plan, ref):
     """The bench checks its own output: epoch 0 once more through the benched pipeline,
-    and each batch the CPU leg ran is compared with the reference's result (sorted
-    distinct vertices and their gathered feature rows, bit for bit)."""
+    and each batch the CPU leg ran is compared with the reference's result — every
+    hop's offsets and sampled neighbours, the sorted distinct vertices and their
+    gathered feature rows, bit for bit."""
     import torch
 
     got = {}
@@ -727,16 +728,29 @@ def verify_epoch0(pipe, plan, ref):
             b = w0 + bi
             if b < len(ref):
                 u = int(sp.ucount[bi])
+                hops = []
+                for h in range(sp.H):
+                    f, t = int(sp.counts[h, bi]), int(sp.counts[h + 1, bi])
+                    hops.append((sp.offsets[h][bi, : f + 1].cpu().numpy().astype(np.int64),
+                                 sp.nbrs[h][bi, :t].cpu().numpy().view(np.uint32).astype(np.int64)))
                 got[b] = (sp.unique[bi, :u].cpu().numpy().view(np.uint32).astype(np.int64),
-                          p.features[bi, :u].cpu().numpy())
+                          p.features[bi, :u].cpu().numpy(), hops)
+
+    def same(b, want):
+        if b not in got:
+            return False
+        uniq, rows, hops = got[b]
+        ok = np.array_equal(uniq, want[0]) and np.array_equal(rows, want[1]) and len(hops) == len(want[2])
+        for (o, n), (wo, wn) in zip(hops, want[2]):
+            ok = ok and np.array_equal(o, np.asarray(wo, np.int64)) and np.array_equal(n, np.asarray(wn, np.int64))
+        return ok
 
     pipe.run_epoch(plan, on_window=grab)
-    bad = [b for b, (uniq, rows) in enumerate(ref)
-           if b not in got or not (np.array_equal(got[b][0], uniq) and np.array_equal(got[b][1], rows))]
+    bad = [b for b, want in enumerate(ref) if not same(b, want)]
     if bad:
         raise RuntimeError(f"bench self-check failed: batches {bad} of epoch 0 differ from the reference")
     return {"batches": len(ref), "epoch": 0, "bit_exact": True,
-            "against": "the CPU leg's own results (distinct vertices + gathered rows)"}
+            "against": "the CPU leg's own results: per-hop offsets and neighbours, distinct vertices, gathered rows"}
 
 
 def train_run(args, g, cfg, pipe, pool, root, clique, local_idx, world):

@@ -81,3 +81,19 @@ def test_bench_reference_arm():
               "--num-vertices", "200000"])
     assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_bench_c3_full_shape_self_check():
+    """C3 at its full ogbn-papers100M shape (111M vertices, 1.55B edges, 57 GB host tier):
+    the bench's three-tier section samples and gathers through TopologyStore and
+    FeatureStore built from the reference plan and compares 4 batches of epoch 0 — every
+    hop's offsets and neighbours, the distinct vertices and their rows — with the
+    unmodified reference, bit for bit."""
+    d = _run([sys.executable, "bench.py", "--steps", "3", "--warmup", "3", "--num-vertices", "200000",
+              "--train-epochs", "0", "--no-e2e", "--cpu-seconds", "2", "--c3-scale", "1.0", "--c3-steps", "1",
+              "--c3-warmup", "1"])
+    c3 = d["c3_three_tier"]
+    assert c3["config"]["num_vertices"] == 111_000_000 and c3["config"]["num_edges"] == 1_554_000_000
+    assert c3["verified"]["bit_exact"] and c3["verified"]["batches"] == 4
+    assert c3["cpu_baseline"]["kind"] == "reference"
+    assert c3["tiers_per_batch_rank0"]["rows_host"] > 0 and c3["tiers_per_batch_rank0"]["reads_host"] > 0
