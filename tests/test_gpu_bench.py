@@ -8,6 +8,7 @@ import subprocess
 import sys
 from pathlib import Path
 
+import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
@@ -60,9 +61,11 @@ def test_bench_two_ranks_partitioned_clique():
     env = dict(os.environ, GC_DIST_BACKEND="gloo")
     d = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
-              *SMALL, "--no-e2e"], env=env)
+              *SMALL, "--no-e2e", "--train-epochs", "1"], env=env)
     assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
     assert d["config"]["dist_backend"] == "gloo"
+    ge = d["graphsage_epoch"]  # DDP: the gradient all-reduce every step across the two ranks
+    assert ge["ddp_ranks"] == 2 and ge["seconds"] > 0 and np.isfinite(ge["bf16"]["last_loss"])
     _check_c3(d, 2)
 
 

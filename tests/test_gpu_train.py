@@ -135,3 +135,77 @@ def test_tree_trainer_equals_autograd_step_by_step(layer, use_graph):
     assert rel.max() < 1e-5, (got, want)
     for a, b in zip(mine.parameters(), ref.parameters()):
         assert torch.allclose(a, b, rtol=1e-4, atol=1e-5)
+
+
+def _ddp_rank(rank, world, port, q):
+    import os
+    import sys
+    from pathlib import Path
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    root = Path(__file__).resolve().parents[1]
+    sys.path[:0] = [str(root), str(root / "oracle")]
+    try:
+        import torch
+        import torch.distributed as dist
+
+        import paper_2305_16588_b200 as P
+        from paper_2305_16588_b200.cache import FeatureStore
+        from paper_2305_16588_b200.graph import synthetic_features_device
+        from paper_2305_16588_b200.pipeline import SampleGatherPipeline
+        from paper_2305_16588_b200.train import GraphSAGE, TreeTrainer, synthetic_labels, train_epoch_tree
+
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.backends.cuda.matmul.allow_tf32 = False
+        n, dim = 20_000, 32
+        g = P.generate_synthetic(n, 12, 1.2, seed=4)
+        pools = [np.arange(rank, n, 23, dtype=np.int64)[: 700 - 300 * rank]]  # rank 1 has fewer batches
+        cfg = P.SamplingConfig(fanouts=(6, 3), batch_size=128)
+        labels = torch.from_numpy(synthetic_labels(np.arange(n), 5)).cuda()
+        torch.manual_seed(0)  # identical initial weights on every rank
+        model = GraphSAGE(dim, 32, 5, 2).cuda()
+        store = FeatureStore.resident(synthetic_features_device(0, n, dim))
+        pipe = SampleGatherPipeline(g, cfg, store, len(pools[0]), window=3)
+        tr = TreeTrainer(model, pipe.sampler, labels, lr=0.2)
+        steps = 6  # max over ranks: rank 0 has 6 batches, rank 1 has 4 (+2 zero-gradient joins)
+        losses = train_epoch_tree(pipe, pipe.plan_epoch(pools[0], P.KeyedRng(9).derive(0, 0, rank)), tr, steps=steps)
+        q.put((rank, tr.flat.cpu().numpy(), losses.cpu().numpy(), tr.steps))
+        dist.barrier()
+    except Exception as exc:
+        import traceback
+
+        q.put(f"rank {rank}: {exc}\n{traceback.format_exc()}")
+    finally:
+        import torch.distributed as dist
+
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def test_tree_trainer_ddp_two_ranks():
+    """DDP across two processes (gloo, sharing the test GPU): uneven tablets (6 and 4
+    batches), the short rank joins the last steps with zero gradients; every rank ends
+    with bit-identical parameters that differ from the initial ones."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ddp_rank, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    errs = [r for r in res if isinstance(r, str)]
+    assert not errs, errs
+    res.sort(key=lambda r: r[0])
+    (_, f0, l0, s0), (_, f1, l1, s1) = res
+    assert np.array_equal(f0, f1)
+    assert len(l0) == 6 and len(l1) == 4 and s0 == 6 and s1 == 4
+    assert np.isfinite(l0).all() and np.isfinite(l1).all()
