@@ -501,8 +501,9 @@ def run_b200(args):
                      "launches": dom_launches, "avg_launch_ms": dom_ms / max(dom_launches, 1),
                      "bytes_per_launch": stage_bytes[dom] / max(dom_launches, 1),
                      # the kernel is issue/ALU-bound, not HBM-bound: its pipe counters
-                     # from the committed ncu capture (profiles/r01_ncu_full.md)
-                     "ncu_pipes": pipes},
+                     # from the committed ncu capture and its issue roofline below
+                     "ncu_pipes": pipes,
+                     "issue": issue_roofline(pipes, dom_ms / max(dom_launches, 1), clocks)},
         "step_roofline": {"bytes_per_batch": step_bytes / (nb * args.steps),
                           "t_roof_us_per_batch": step_bytes / (nb * args.steps) / (peak * 1e9) * 1e6,
                           "measured_us_per_batch": total_ms * 1000 / (nb * args.steps),
@@ -710,6 +711,22 @@ def c3_run(args, rank, local, world):
     host.close()
     torch.cuda.empty_cache()
     return out
+
+
+def issue_roofline(pipes, launch_ms, clocks):
+    """Issue roofline of an ALU-bound kernel: its warp-instructions (ncu capture of the
+    same launch) at one warp-instruction per cycle per SM sub-partition (4 per SM) at
+    the max SM clock, against the kernel's live-measured launch time."""
+    import torch
+
+    if not pipes or not pipes.get("warp_inst"):
+        return None
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    mhz = clocks.max_mhz or 1965.0
+    peak = sms * 4 * mhz * 1e6  # warp-instructions per second
+    floor_ms = pipes["warp_inst"] / peak * 1e3
+    return {"warp_inst_per_launch": pipes["warp_inst"], "peak_warp_inst_per_s": peak, "floor_ms": floor_ms,
+            "measured_ms": launch_ms, "frac": floor_ms / launch_ms}
 
 
 def verify_epoch0(pipe, plan, ref):

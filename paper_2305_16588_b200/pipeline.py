@@ -23,9 +23,9 @@ from .graph import CsrGraph
 from .rng import ROLE_SHUFFLE, KeyedRng
 from .sampling import DeviceHotness, SamplingConfig, WindowSampler, batch_hop_keys, check_seed_pool
 
-# kernels each stage launches (for the bench's gpu_launches count): CUB's onesweep
-# radix sort of the keys' high 32 bits is 1 histogram + 1 scan + 4 digit passes, plus keys, ties, emit
-LAUNCHES_PERMUTATION = 3 + 6
+# kernels each stage launches (for the bench's gpu_launches count): the permutation is a
+# histogram, a 3-kernel scan of the bucket counts, a scatter and the in-bucket rank/emit
+LAUNCHES_PERMUTATION = 6
 
 
 def _as_i64(key: int) -> int:
