@@ -16,7 +16,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parents[1]
 STAGE = {  # kernel -> pipeline stage (bench.py stages_ms)
     "k_hop_expand": "hop_expand", "k_unique": "unique_relabel", "k_relabel": "unique_relabel",
-    "k_gather": "gather", "k_perm_keys": "shuffle", "k_perm_emit": "shuffle", "DeviceRadixSort": "shuffle",
+    "k_gather": "gather", "k_perm_": "shuffle", "k_scan_": "shuffle",
 }
 METRICS = [
     ("gpu__time_duration.sum", "time"), ("dram__bytes_read.sum", "dram_read"), ("dram__bytes_write.sum", "dram_write"),
@@ -51,8 +51,8 @@ def launches(path: Path):
     hdr = rows[0]
     ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
     seq = [(r[ki].split("(")[0].replace("void ", ""), float(r[vi].replace(",", ""))) for r in rows[1:] if len(r) > vi]
-    # one epoch = from a k_perm_keys to the next; use the last complete one
-    starts = [i for i, (n, _) in enumerate(seq) if "k_perm_keys" in n]
+    # one epoch = from a k_perm_hist (the shuffle's first kernel) to the next; use the last complete one
+    starts = [i for i, (n, _) in enumerate(seq) if "k_perm_hist" in n]
     a, b = starts[-2], starts[-1]
     epoch = seq[a:b]
     tot = sum(t for _, t in epoch)
