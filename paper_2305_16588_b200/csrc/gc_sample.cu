@@ -89,7 +89,7 @@ struct HopParams {
     uint32_t cls;
     uint32_t u32b;
     uint64_t* tile_state;
-    uint32_t* tile_counter;  // tile ids are claimed from it in dispatch order (zeroed per launch)
+    uint32_t* tile_counter;  // [num_batches]: batch b's tile ids are claimed from [b] in dispatch order (zeroed per launch)
     int exact_only;  // test hook: always take the 64-bit extraction path
     uint32_t k32;    // == 32, opaque to the compiler (see PairHashHigh::hi_counter)
 };
@@ -328,6 +328,19 @@ __device__ __forceinline__ bool select_thread(uint64_t hc, uint32_t deg, uint32_
     for (; c + 1 < cend; c += 2)
         insert_pair<S>(t, (hh.hi_counter(c, k32) & kKeep) | c, (hh.hi_counter(c + 1, k32) & kKeep) | (c + 1));
     if (c < cend) insert_slot<S>(t, (hh.hi_counter(c, k32) & kKeep) | c);
+    const uint64_t base = o0 - kGoldenLow;
+    if (!CHECKED && fanout == S - 1) {
+        // the widest fanout of the network (C2 hop 3: 5 of S = 6): every slot is
+        // checked and staged without per-slot predicates, from one base address
+        bool tie = false;
+#pragma unroll
+        for (int s = 0; s + 1 < S; ++s) tie |= (t[s] >> IB) == (t[s + 1] >> IB);
+        if (tie) return false;
+        Item* const out = s_items + excl;
+#pragma unroll
+        for (int s = 0; s + 1 < S; ++s) out[s] = (Item)(base + (t[s] & ((1u << IB) - 1u)));
+        return true;
+    }
     bool tie = false;
 #pragma unroll
     for (int s = 0; s + 1 < S; ++s) tie |= (s < (int)fanout) & ((t[s] >> IB) == (t[s + 1] >> IB));
@@ -335,7 +348,7 @@ __device__ __forceinline__ bool select_thread(uint64_t hc, uint32_t deg, uint32_
 #pragma unroll
     for (int s = 0; s < S; ++s)
         if (s < (int)fanout) {
-            const uint64_t e = o0 + ((t[s] & ((1u << IB) - 1u)) - kGoldenLow);
+            const uint64_t e = base + (t[s] & ((1u << IB) - 1u));
             if (CHECKED)
                 stage(s_items, excl + s, r0, r1, e);
             else
@@ -369,6 +382,52 @@ __device__ __forceinline__ void select_warp(uint64_t hc, uint32_t d, uint32_t fa
     }
 }
 
+// Emission of one group of K staged items per thread (item q at items[q * kHopThreads]):
+// column loads, then visited-word loads, then streaming stores and the (rare) atomics,
+// so the dependent-load chains of the K items overlap. FULL: all K are in range, so
+// there are no per-item predicates and every address is one base plus an immediate.
+template <int K, bool FULL, bool TIERED, typename Item>
+__device__ __forceinline__ void emit_group(const Item* items, uint32_t left, uint32_t* dst, const HopParams& p,
+                                           uint32_t* bm, uint32_t* sm) {
+    const uint32_t* __restrict__ ci = p.ci;
+    uint32_t u[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+        u[q] = 0;
+        if (FULL || q * kHopThreads < left) {
+            const uint64_t it = items[q * kHopThreads];  // u32 items widen for the plain CSR
+            if (TIERED) {
+                const uint32_t code = (uint32_t)(it >> kTierShift);
+                const uint32_t* cols = code ? p.scols[code - 1] : ci;
+                u[q] = __ldg(cols + (it & kEdgeMask));
+            } else {
+                u[q] = __ldg(ci + it);
+            }
+        }
+    }
+    if (bm == nullptr) {
+#pragma unroll
+        for (int q = 0; q < K; ++q)
+            if (FULL || q * kHopThreads < left) __stcs(dst + q * kHopThreads, u[q]);
+        return;
+    }
+    uint32_t w[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) w[q] = (FULL || q * kHopThreads < left) ? bm[u[q] >> 5] : ~0u;
+#pragma unroll
+    for (int q = 0; q < K; ++q)
+        if (FULL || q * kHopThreads < left) __stcs(dst + q * kHopThreads, u[q]);
+    if (sm == nullptr) {
+#pragma unroll
+        for (int q = 0; q < K; ++q)
+            if (!((w[q] >> (u[q] & 31)) & 1u)) atomicOr(bm + (u[q] >> 5), 1u << (u[q] & 31));
+    } else {
+#pragma unroll
+        for (int q = 0; q < K; ++q)
+            if (!((w[q] >> (u[q] & 31)) & 1u)) mark_visited_unchecked(bm, sm, u[q]);
+    }
+}
+
 // TIERED: the topology has a location table or lives in host memory, so rows resolve
 // through the tier rule and staged edges carry a slab code; otherwise the plain CSR.
 template <int S, bool TIERED>
@@ -386,14 +445,14 @@ __global__ void __launch_bounds__(kHopThreads, hop_min_blocks<S>()) k_hop_expand
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
-    // tile id claimed from a counter, not blockIdx.x: a tile only starts after every
-    // lower tile id has been handed to a running CTA, so each predecessor its look-back
-    // waits on is resident or done whatever order the hardware dispatches CTAs in
-    if (tid == 0) s_vid = atomicAdd(p.tile_counter, 1u);
+    // grid = (tiles per batch, batches). The tile id within batch b is claimed from the
+    // batch's counter, not blockIdx.x: a tile only starts after every lower tile of its
+    // batch has been handed to a running CTA, so each predecessor its look-back waits on
+    // is resident or done whatever order the hardware dispatches CTAs in
+    const uint32_t b = blockIdx.y;
+    if (tid == 0) s_vid = atomicAdd(p.tile_counter + b, 1u);
     __syncthreads();
-    const uint32_t vid = s_vid;
-    const uint32_t b = vid / p.tiles_per_batch;
-    const uint32_t t = vid % p.tiles_per_batch;
+    const uint32_t t = s_vid;
     const uint32_t F = p.fcount[b];
     const uint64_t p0 = (uint64_t)t * p.tile_pos;
     if (p0 >= F && t != 0) return;  // past the end of this batch's frontier: no successor needs it
@@ -547,37 +606,10 @@ __global__ void __launch_bounds__(kHopThreads, hop_min_blocks<S>()) k_hop_expand
         uint32_t* dst = out + (uint32_t)s_prefix + r0;
         constexpr int kEmit = emit_items<S>();
         for (uint32_t k0 = tid; k0 < cnt; k0 += kEmit * kHopThreads) {
-            uint32_t u[kEmit];
-#pragma unroll
-            for (int q = 0; q < kEmit; ++q) {
-                const uint32_t k = k0 + q * kHopThreads;
-                u[q] = 0;
-                if (k < cnt) {
-                    const uint64_t it = s_items[k];  // u32 items widen for the plain CSR
-                    if (TIERED) {
-                        const uint32_t code = (uint32_t)(it >> kTierShift);
-                        const uint32_t* cols = code ? p.scols[code - 1] : p.ci;
-                        u[q] = __ldg(cols + (it & kEdgeMask));
-                    } else {
-                        u[q] = __ldg(p.ci + it);
-                    }
-                }
-            }
-            if (bm) {
-                uint32_t w[kEmit];
-#pragma unroll
-                for (int q = 0; q < kEmit; ++q) w[q] = k0 + q * kHopThreads < cnt ? bm[u[q] >> 5] : ~0u;
-#pragma unroll
-                for (int q = 0; q < kEmit; ++q)
-                    if (k0 + q * kHopThreads < cnt) __stcs(dst + k0 + q * kHopThreads, u[q]);
-#pragma unroll
-                for (int q = 0; q < kEmit; ++q)
-                    if (!((w[q] >> (u[q] & 31)) & 1u)) mark_visited_unchecked(bm, sm, u[q]);
-            } else {
-#pragma unroll
-                for (int q = 0; q < kEmit; ++q)
-                    if (k0 + q * kHopThreads < cnt) __stcs(dst + k0 + q * kHopThreads, u[q]);
-            }
+            if (k0 + (kEmit - 1) * kHopThreads < cnt)
+                emit_group<kEmit, true, TIERED>(s_items + k0, cnt - k0, dst + k0, p, bm, sm);
+            else
+                emit_group<kEmit, false, TIERED>(s_items + k0, cnt - k0, dst + k0, p, bm, sm);
         }
         // s_items is reused by the next round only; the last round exits without a barrier
         if (r + 1 < rounds) __syncthreads();
@@ -605,7 +637,7 @@ static int network_slots(uint32_t fanout) {
 }
 
 template <int S>
-static void launch_hop(const HopParams& p, unsigned grid, bool tiered, cudaStream_t s) {
+static void launch_hop(const HopParams& p, dim3 grid, bool tiered, cudaStream_t s) {
     if (tiered)
         k_hop_expand<S, true><<<grid, kHopThreads, 0, s>>>(p);
     else
@@ -635,7 +667,8 @@ int gc_set_option(int option, int value) {
 }
 
 size_t gc_hop_expand_temp_bytes(uint32_t num_batches, uint32_t max_frontier) {
-    return align_up((size_t)num_batches * tiles_for(max_frontier, 32) * sizeof(uint64_t), 256) + 256;
+    return align_up((size_t)num_batches * tiles_for(max_frontier, 32) * sizeof(uint64_t), 256) +
+           align_up((size_t)num_batches * sizeof(uint32_t), 256);
 }
 
 int gc_hop_expand(const gc_topology_t* topo, const uint32_t* d_frontier, uint64_t frontier_stride,
@@ -702,22 +735,23 @@ int gc_hop_expand(const gc_topology_t* topo, const uint32_t* d_frontier, uint64_
     const size_t state_bytes = align_up((size_t)num_batches * tiles * sizeof(uint64_t), 256);
     p.tile_state = static_cast<uint64_t*>(d_temp);
     p.tile_counter = reinterpret_cast<uint32_t*>(static_cast<char*>(d_temp) + state_bytes);
-    GC_TRY(cudaMemsetAsync(d_temp, 0, state_bytes + 256, s), "gc_hop_expand memset");
-    const uint64_t grid = (uint64_t)num_batches * tiles;
-    GC_REQUIRE(grid < (1ull << 31), GC_ERR_VALUE, "gc_hop_expand: window too large");
+    GC_TRY(cudaMemsetAsync(d_temp, 0, state_bytes + align_up((size_t)num_batches * sizeof(uint32_t), 256), s),
+           "gc_hop_expand memset");
+    GC_REQUIRE(num_batches <= 65535 && tiles < (1u << 31), GC_ERR_VALUE, "gc_hop_expand: window too large");
+    const dim3 grid(tiles, num_batches);
     // the plain-CSR kernel stages 32-bit edge indices; a CSR with 2^32 or more edges
     // takes the tiered kernel (64-bit items), which also reads a location-free CSR
     const bool tiered = topo->location != nullptr || topo->full_on_host || graph->num_edges >= (1ull << 32);
     switch (network_slots(fanout)) {
-        case 4: launch_hop<4>(p, (unsigned)grid, tiered, s); break;
-        case 6: launch_hop<6>(p, (unsigned)grid, tiered, s); break;
-        case 8: launch_hop<8>(p, (unsigned)grid, tiered, s); break;
-        case 11: launch_hop<11>(p, (unsigned)grid, tiered, s); break;
-        case 16: launch_hop<16>(p, (unsigned)grid, tiered, s); break;
-        case 21: launch_hop<21>(p, (unsigned)grid, tiered, s); break;
-        case 26: launch_hop<26>(p, (unsigned)grid, tiered, s); break;
-        case 32: launch_hop<32>(p, (unsigned)grid, tiered, s); break;
-        default: launch_hop<0>(p, (unsigned)grid, tiered, s); break;
+        case 4: launch_hop<4>(p, grid, tiered, s); break;
+        case 6: launch_hop<6>(p, grid, tiered, s); break;
+        case 8: launch_hop<8>(p, grid, tiered, s); break;
+        case 11: launch_hop<11>(p, grid, tiered, s); break;
+        case 16: launch_hop<16>(p, grid, tiered, s); break;
+        case 21: launch_hop<21>(p, grid, tiered, s); break;
+        case 26: launch_hop<26>(p, grid, tiered, s); break;
+        case 32: launch_hop<32>(p, grid, tiered, s); break;
+        default: launch_hop<0>(p, grid, tiered, s); break;
     }
     GC_CHECK_LAUNCH("gc_hop_expand");
     return GC_OK;
