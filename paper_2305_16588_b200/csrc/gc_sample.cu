@@ -48,6 +48,9 @@ __host__ __device__ constexpr int emit_items() {
 #define GC_HOP_MIN_BLOCKS 6
 #endif
 constexpr int kHopMinBlocks = GC_HOP_MIN_BLOCKS;
+#ifndef GC_HOP_PPT
+#define GC_HOP_PPT 2  // frontier positions per thread of the small-network kernels
+#endif
 template <int S>
 constexpr int hop_min_blocks() {
     return (S > 0 && S <= 8 ? kHopMinBlocks : (S > 0 && S <= 16 ? 5 : 4)) * 256 / kHopThreads;
@@ -430,7 +433,11 @@ __device__ __forceinline__ void emit_group(const Item* items, uint32_t left, uin
 
 // TIERED: the topology has a location table or lives in host memory, so rows resolve
 // through the tier rule and staged edges carry a slab code; otherwise the plain CSR.
-template <int S, bool TIERED>
+// PPT frontier positions per thread (blocked: thread i owns positions PPT*i ..
+// PPT*i + PPT-1 of the tile). PPT = 2 for the small networks: phase 1's chain of
+// dependent loads (tile claim -> frontier -> row offsets) and the per-tile work (scan,
+// look-back, uniform setup) are then paid once per 512 positions instead of 256.
+template <int S, bool TIERED, int PPT>
 __global__ void __launch_bounds__(kHopThreads, hop_min_blocks<S>()) k_hop_expand(HopParams p) {
     using Scan = cub::BlockScan<uint32_t, kHopThreads>;
     using Reduce = cub::BlockReduce<uint64_t, kHopThreads>;
@@ -455,56 +462,78 @@ __global__ void __launch_bounds__(kHopThreads, hop_min_blocks<S>()) k_hop_expand
         s_vid = atomicAdd(p.tile_counter + b, 1u);
         s_arrive = 0;
     }
+    // batch-uniform loads overlap the claim's round trip
+    const uint32_t F = p.fcount[b];
+    const uint64_t hkey = p.hop_keys[b];
     __syncthreads();
     const uint32_t t = s_vid;
-    const uint32_t F = p.fcount[b];
     const uint64_t p0 = (uint64_t)t * p.tile_pos;
     if (p0 >= F && t != 0) return;  // past the end of this batch's frontier: no successor needs it
     const uint32_t npos = p0 < F ? (uint32_t)((F - p0) < (uint64_t)p.tile_pos ? (F - p0) : (uint64_t)p.tile_pos) : 0u;
 
-    // ---- phase 1: thread-per-position degree, take and position hash
-    const bool valid = tid < (int)npos;
-    uint32_t v = 0, deg = 0, take = 0;
-    uint64_t o0 = 0, hc = 0;
-    // 0 local, 1 peer slab, 2 host; the full CSR is local unless it lives in host memory
-    int tier = TIERED ? 2 : 0;
-    if (valid) {
-        v = p.frontier[b * p.fstride + p0 + tid];
-        if (!TIERED && v < p.n) {
-            o0 = p.ro[v];
-            deg = (uint32_t)(p.ro[v + 1] - o0);
-        } else if (v < p.n) {
-            const uint32_t L = p.loc ? __ldg(p.loc + v) : GC_TIER_HOST;
-            if (L == GC_TIER_HOST) {
-                o0 = p.ro[v];
-                deg = (uint32_t)(p.ro[v + 1] - o0);
-            } else {
-                const uint32_t g = L >> 28, slot = L & 0x0FFFFFFFu;
-                const uint64_t* so = p.soff[g];
-                o0 = so[slot];
-                deg = (uint32_t)(so[slot + 1] - o0);
-                o0 |= (uint64_t)(g + 1) << kTierShift;  // tag: read the columns from slab g
-                tier = g == p.self_rank ? 0 : 1;
+    // ---- phase 1: per position degree, take and position hash
+    bool valid[PPT];
+    uint32_t v[PPT], deg[PPT], take[PPT];
+    uint64_t o0[PPT], hc[PPT];
+    int tier[PPT];  // 0 local, 1 peer slab, 2 host; the full CSR is local unless it lives in host memory
+    const uint32_t* fr = p.frontier + b * p.fstride + p0 + (uint32_t)tid * PPT;
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+        valid[q] = (uint32_t)tid * PPT + q < npos;
+        v[q] = valid[q] ? fr[q] : 0u;
+        deg[q] = 0;
+        take[q] = 0;
+        o0[q] = 0;
+        hc[q] = 0;
+        tier[q] = TIERED ? 2 : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+        if (valid[q]) {
+            if (!TIERED && v[q] < p.n) {
+                o0[q] = p.ro[v[q]];
+                deg[q] = (uint32_t)(p.ro[v[q] + 1] - o0[q]);
+            } else if (v[q] < p.n) {
+                const uint32_t L = p.loc ? __ldg(p.loc + v[q]) : GC_TIER_HOST;
+                if (L == GC_TIER_HOST) {
+                    o0[q] = p.ro[v[q]];
+                    deg[q] = (uint32_t)(p.ro[v[q] + 1] - o0[q]);
+                } else {
+                    const uint32_t g = L >> 28, slot = L & 0x0FFFFFFFu;
+                    const uint64_t* so = p.soff[g];
+                    o0[q] = so[slot];
+                    deg[q] = (uint32_t)(so[slot + 1] - o0[q]);
+                    o0[q] |= (uint64_t)(g + 1) << kTierShift;  // tag: read the columns from slab g
+                    tier[q] = g == p.self_rank ? 0 : 1;
+                }
             }
         }
-        take = min(deg, p.fanout);
-        if (p.mark_frontier && p.bitmap && v < p.n)
-            mark_visited(p.bitmap + b * p.bwords, p.summary ? p.summary + b * p.swords : nullptr, v);
-        // hash_counters(position), position = index in this batch's frontier (rng.py:64-66)
-        if (deg > p.fanout) hc = hash_counter(p.hop_keys[b], p0 + tid);
+    }
+#pragma unroll
+    for (int q = 0; q < PPT; ++q) {
+        if (valid[q]) {
+            take[q] = min(deg[q], p.fanout);
+            if (p.mark_frontier && p.bitmap && v[q] < p.n)
+                mark_visited(p.bitmap + b * p.bwords, p.summary ? p.summary + b * p.swords : nullptr, v[q]);
+            // hash_counters(position), position = index in this batch's frontier (rng.py:64-66)
+            if (deg[q] > p.fanout) hc[q] = hash_counter(hkey, p0 + (uint32_t)tid * PPT + q);
+        }
     }
     if (p.topo_reads || p.edge_trav) {
-        // ids outside [0, n) are rejected on the host; never let one index a counter
-        const bool counted = valid && v < p.n;
-        unsigned act = __ballot_sync(kFull, counted);
-        if (counted) {
-            // vertex 0 of a Zipf graph fills ~1/5 of a frontier: one atomic per
-            // distinct vertex per warp (take depends on v only)
-            unsigned peers = __match_any_sync(act, v);
-            if (lane == __ffs(peers) - 1) {
-                unsigned long long c = __popc(peers);
-                if (p.topo_reads) atomicAdd((unsigned long long*)(p.topo_reads + v), c);
-                if (p.edge_trav && take) atomicAdd((unsigned long long*)(p.edge_trav + v), c * take);
+#pragma unroll
+        for (int q = 0; q < PPT; ++q) {
+            // ids outside [0, n) are rejected on the host; never let one index a counter
+            const bool counted = valid[q] && v[q] < p.n;
+            unsigned act = __ballot_sync(kFull, counted);
+            if (counted) {
+                // vertex 0 of a Zipf graph fills ~1/5 of a frontier: one atomic per
+                // distinct vertex per warp (take depends on v only)
+                unsigned peers = __match_any_sync(act, v[q]);
+                if (lane == __ffs(peers) - 1) {
+                    unsigned long long c = __popc(peers);
+                    if (p.topo_reads) atomicAdd((unsigned long long*)(p.topo_reads + v[q]), c);
+                    if (p.edge_trav && take[q]) atomicAdd((unsigned long long*)(p.edge_trav + v[q]), c * take[q]);
+                }
             }
         }
     }
@@ -512,29 +541,38 @@ __global__ void __launch_bounds__(kHopThreads, hop_min_blocks<S>()) k_hop_expand
         // topology reads by tier: positions and sampled edges (PCIe bytes for the host tier)
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const unsigned m = __ballot_sync(kFull, valid && tier == c);
-            uint32_t e = (valid && tier == c) ? take : 0u;
+            uint32_t n = 0, e = 0;
+#pragma unroll
+            for (int q = 0; q < PPT; ++q) {
+                n += __popc(__ballot_sync(kFull, valid[q] && tier[q] == c));
+                e += (valid[q] && tier[q] == c) ? take[q] : 0u;
+            }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(kFull, e, o);
-            if (lane == 0 && m) {
-                atomicAdd((unsigned long long*)(p.tier_reads + c), (unsigned long long)__popc(m));
+            if (lane == 0 && n) {
+                atomicAdd((unsigned long long*)(p.tier_reads + c), (unsigned long long)n);
                 atomicAdd((unsigned long long*)(p.tier_reads + 3 + c), (unsigned long long)e);
             }
         }
         // PCIe transactions of host-tier reads, t(v) = 1 + ceil(deg * 4 / CLS)
-        uint32_t tx = (valid && tier == 2) ? 1u + (uint32_t)(((uint64_t)deg * p.u32b + p.cls - 1) / p.cls) : 0u;
+        uint32_t tx = 0;
+#pragma unroll
+        for (int q = 0; q < PPT; ++q)
+            tx += (valid[q] && tier[q] == 2) ? 1u + (uint32_t)(((uint64_t)deg[q] * p.u32b + p.cls - 1) / p.cls) : 0u;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) tx += __shfl_xor_sync(kFull, tx, o);
         if (lane == 0 && tx) atomicAdd((unsigned long long*)(p.tier_reads + 6), (unsigned long long)tx);
     }
     if (p.txn_total) {
         // t(v) = 1 + ceil(nc(v) * uint32_bytes / CLS), sampling.py:177-187
-        uint64_t tv = valid ? 1ull + ((uint64_t)deg * p.u32b + p.cls - 1) / p.cls : 0ull;
+        uint64_t tv = 0;
+#pragma unroll
+        for (int q = 0; q < PPT; ++q) tv += valid[q] ? 1ull + ((uint64_t)deg[q] * p.u32b + p.cls - 1) / p.cls : 0ull;
         uint64_t sum = Reduce(tmp.reduce).Sum(tv);
         if (tid == 0 && sum) atomicAdd((unsigned long long*)p.txn_total, (unsigned long long)sum);
         __syncthreads();
     }
-    uint32_t excl, total;
+    uint32_t excl[PPT], total;
     Scan(tmp.scan).ExclusiveSum(take, excl, total);
     const uint64_t sidx = (uint64_t)b * p.tiles_per_batch + t;
     const uint64_t sfirst = (uint64_t)b * p.tiles_per_batch;
@@ -544,42 +582,49 @@ __global__ void __launch_bounds__(kHopThreads, hop_min_blocks<S>()) k_hop_expand
     uint32_t* bm = p.bitmap ? p.bitmap + b * p.bwords : nullptr;
     uint32_t* sm = p.summary ? p.summary + b * p.swords : nullptr;
     const uint32_t rounds = (total + kItemCap - 1) / kItemCap;
-    const bool thread_copy = deg <= p.fanout && deg <= 64;
-    const bool thread_choice = S > 0 && !p.exact_only && deg > p.fanout && deg <= 64 && p.fanout < (uint32_t)S;
 
     for (uint32_t r = 0; r < max(rounds, 1u); ++r) {
         const uint32_t r0 = r * kItemCap;
         const uint32_t r1 = min(total, r0 + kItemCap);
         // ---- phase 2a: stage the source edge index of every output item in [r0, r1)
-        bool need_warp = false;
-        if (valid && take && excl + take > r0 && excl < r1) {
-            if (thread_copy) {
-                if (rounds <= 1)
-                    for (uint32_t k = 0; k < deg; ++k) s_items[excl + k] = (Item)(o0 + k);
-                else
-                    for (uint32_t k = 0; k < deg; ++k) stage(s_items, excl + k, r0, r1, o0 + k);
-            } else if (thread_choice) {
-                need_warp = rounds <= 1
-                                ? !select_thread<(S > 0 ? S : 4), false>(hc, deg, p.fanout, o0, excl, r0, r1, s_items,
-                                                                        p.k32)
-                                : !select_thread<(S > 0 ? S : 4), true>(hc, deg, p.fanout, o0, excl, r0, r1, s_items,
-                                                                       p.k32);
-            } else {
-                need_warp = true;
+        bool need_warp[PPT];
+#pragma unroll
+        for (int q = 0; q < PPT; ++q) {
+            need_warp[q] = false;
+            const bool thread_copy = deg[q] <= p.fanout && deg[q] <= 64;
+            const bool thread_choice =
+                S > 0 && !p.exact_only && deg[q] > p.fanout && deg[q] <= 64 && p.fanout < (uint32_t)S;
+            if (valid[q] && take[q] && excl[q] + take[q] > r0 && excl[q] < r1) {
+                if (thread_copy) {
+                    if (rounds <= 1)
+                        for (uint32_t k = 0; k < deg[q]; ++k) s_items[excl[q] + k] = (Item)(o0[q] + k);
+                    else
+                        for (uint32_t k = 0; k < deg[q]; ++k) stage(s_items, excl[q] + k, r0, r1, o0[q] + k);
+                } else if (thread_choice) {
+                    need_warp[q] = rounds <= 1 ? !select_thread<(S > 0 ? S : 4), false>(
+                                                     hc[q], deg[q], p.fanout, o0[q], excl[q], r0, r1, s_items, p.k32)
+                                               : !select_thread<(S > 0 ? S : 4), true>(
+                                                     hc[q], deg[q], p.fanout, o0[q], excl[q], r0, r1, s_items, p.k32);
+                } else {
+                    need_warp[q] = true;
+                }
             }
         }
-        unsigned todo = __ballot_sync(kFull, need_warp);
-        while (todo) {
-            const int src = __ffs(todo) - 1;
-            todo &= todo - 1u;
-            const uint32_t d = __shfl_sync(kFull, deg, src);
-            const uint64_t base = __shfl_sync(kFull, o0, src);
-            const uint32_t e0 = __shfl_sync(kFull, excl, src);
-            const uint64_t h = __shfl_sync(kFull, hc, src);
-            if (d <= p.fanout) {
-                for (uint32_t k = lane; k < d; k += 32) stage(s_items, e0 + k, r0, r1, base + k);
-            } else {
-                select_warp(h, d, p.fanout, base, e0, r0, r1, s_items, p.exact_only);
+#pragma unroll
+        for (int q = 0; q < PPT; ++q) {
+            unsigned todo = __ballot_sync(kFull, need_warp[q]);
+            while (todo) {
+                const int src = __ffs(todo) - 1;
+                todo &= todo - 1u;
+                const uint32_t d = __shfl_sync(kFull, deg[q], src);
+                const uint64_t base = __shfl_sync(kFull, o0[q], src);
+                const uint32_t e0 = __shfl_sync(kFull, excl[q], src);
+                const uint64_t h = __shfl_sync(kFull, hc[q], src);
+                if (d <= p.fanout) {
+                    for (uint32_t k = lane; k < d; k += 32) stage(s_items, e0 + k, r0, r1, base + k);
+                } else {
+                    select_warp(h, d, p.fanout, base, e0, r0, r1, s_items, p.exact_only);
+                }
             }
         }
         if (r == 0) {
@@ -596,10 +641,14 @@ __global__ void __launch_bounds__(kHopThreads, hop_min_blocks<S>()) k_hop_expand
             __syncthreads();
             const uint32_t prefix = (uint32_t)s_prefix;
             uint32_t* offs = p.out_off + b * p.ostride;
-            if (valid) __stcs(offs + p0 + tid, prefix + excl);
-            if (valid && p0 + tid + 1 == F) {
-                offs[F] = prefix + excl + take;
-                p.out_count[b] = prefix + excl + take;
+#pragma unroll
+            for (int q = 0; q < PPT; ++q) {
+                const uint64_t pos = p0 + (uint32_t)tid * PPT + q;
+                if (valid[q]) __stcs(offs + pos, prefix + excl[q]);
+                if (valid[q] && pos + 1 == F) {
+                    offs[F] = prefix + excl[q] + take[q];
+                    p.out_count[b] = prefix + excl[q] + take[q];
+                }
             }
             if (F == 0 && tid == 0) {
                 offs[0] = 0;
@@ -608,9 +657,7 @@ __global__ void __launch_bounds__(kHopThreads, hop_min_blocks<S>()) k_hop_expand
         } else {
             __syncthreads();
         }
-        // ---- phase 2b: coalesced emission of the staged items. Each thread keeps
-        // kEmit items in flight — column loads, then visited-word loads, then stores and
-        // the (rare) atomics — so the dependent-load chains of its items overlap.
+        // ---- phase 2b: coalesced emission of the staged items
         const uint32_t cnt = r1 > r0 ? r1 - r0 : 0;
         uint32_t* dst = out + (uint32_t)s_prefix + r0;
         constexpr int kEmit = emit_items<S>();
@@ -625,10 +672,15 @@ __global__ void __launch_bounds__(kHopThreads, hop_min_blocks<S>()) k_hop_expand
     }
 }
 
+// positions per thread: 2 for the small networks (fanout <= 7: a 512-position tile
+// stages at most 3584 items in one round), else 1
+static int positions_per_thread(uint32_t fanout) { return fanout < 8 ? GC_HOP_PPT : 1; }
+
 // positions per tile: one staging round whenever fanout <= 128
 static uint32_t tile_positions(uint32_t fanout) {
+    const uint32_t cap = (uint32_t)kTilePos * positions_per_thread(fanout);
     uint32_t tp = kItemCap / (fanout ? fanout : 1);
-    tp = tp >= (uint32_t)kTilePos ? (uint32_t)kTilePos : (tp / 32) * 32;
+    tp = tp >= cap ? cap : (tp / 32) * 32;
     return tp < 32 ? 32 : tp;
 }
 
@@ -647,10 +699,11 @@ static int network_slots(uint32_t fanout) {
 
 template <int S>
 static void launch_hop(const HopParams& p, dim3 grid, bool tiered, cudaStream_t s) {
+    constexpr int PPT = S > 0 && S <= 8 ? GC_HOP_PPT : 1;
     if (tiered)
-        k_hop_expand<S, true><<<grid, kHopThreads, 0, s>>>(p);
+        k_hop_expand<S, true, PPT><<<grid, kHopThreads, 0, s>>>(p);
     else
-        k_hop_expand<S, false><<<grid, kHopThreads, 0, s>>>(p);
+        k_hop_expand<S, false, PPT><<<grid, kHopThreads, 0, s>>>(p);
 }
 
 }  // namespace gc
