@@ -1,13 +1,15 @@
 // K6/K7 cost-model kernels (planner.py:42-67, :87-121, :215-267):
 //   colsum_argmax       clique-wide hotness totals and the first-argmax owner GPU
-//   descending_order    CSLP ranking: totals descending, ties by ascending id
-//   topo/hot prefix     inclusive byte and hotness scans along a ranking
+//   descending_order    CSLP ranking: totals descending, ties by ascending id — a
+//                       hand-written stable LSD radix sort (8-bit digits of ~total,
+//                       only as many passes as the largest total needs)
+//   topo/hot prefix     inclusive byte and hotness scans along a ranking — a single-pass
+//                       scan with decoupled look-back (gc_common.cuh)
 //   searchsorted_right  batched boundary lookup for the alpha grid's float64 budgets
 //   distribute_prefix   stable split of a ranked prefix into per-owner queues
 // The final 101-point _estimate_at evaluation stays on the host, where Python's
 // correctly rounded int/int division reproduces the reference bit for bit.
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
+#include <cub/block/block_scan.cuh>
 
 #include "gc_common.cuh"
 
@@ -163,31 +165,214 @@ __global__ void __launch_bounds__(1024, 1) k_split_scan(const int64_t* __restric
     }
 }
 
+// ---- single-pass inclusive scan of non-negative int64 (decoupled look-back)
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+static int64_t scan_tiles(int64_t n) { return (n + kScanTile - 1) / kScanTile; }
+static size_t scan_state_bytes(int64_t n) { return align_up((size_t)(scan_tiles(n) > 0 ? scan_tiles(n) : 1) * 8, 256) + 256; }
+
+// in[] -> out[] (may alias). Tiles are claimed from `counter` (zeroed with `state`), so a
+// tile's look-back only waits on tiles already held by running CTAs. `skip` (optional,
+// device): the scan does nothing when *skip != 0 (inactive radix passes).
+__global__ void __launch_bounds__(kScanThreads) k_scan_incl(const int64_t* in, int64_t n, int64_t* out,
+                                                             uint64_t* __restrict__ state, uint32_t* __restrict__ counter,
+                                                             const uint32_t* __restrict__ skip) {
+    using BScan = cub::BlockScan<int64_t, kScanThreads>;
+    __shared__ typename BScan::TempStorage tmp;
+    __shared__ int64_t s_data[kScanTile];
+    __shared__ uint32_t s_tile;
+    __shared__ int64_t s_prefix;
+    if (skip && *skip) return;
+    const int tid = threadIdx.x;
+    if (tid == 0) s_tile = atomicAdd(counter, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const int64_t base = (int64_t)tile * kScanTile;
+#pragma unroll
+    for (int r = 0; r < kScanItems; ++r) {  // coalesced, striped
+        const int64_t i = base + r * kScanThreads + tid;
+        s_data[r * kScanThreads + tid] = i < n ? in[i] : 0;
+    }
+    __syncthreads();
+    int64_t sum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) sum += s_data[tid * kScanItems + k];  // blocked
+    int64_t excl, total;
+    BScan(tmp).ExclusiveSum(sum, excl, total);
+    // the aggregate first, so successors sum past this tile instead of waiting for its prefix
+    if (tid == 0 && tile != 0) publish(state + tile, kFlagAgg | (uint64_t)total);
+    if (tid < 32) {
+        const uint64_t pre = lookback_warp(state, 0, tile, (uint64_t)total);
+        if ((tid & 31) == 0) s_prefix = (int64_t)pre;
+    }
+    __syncthreads();
+    int64_t run = s_prefix + excl;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        run += s_data[tid * kScanItems + k];
+        s_data[tid * kScanItems + k] = run;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kScanItems; ++r) {
+        const int64_t i = base + r * kScanThreads + tid;
+        if (i < n) out[i] = s_data[r * kScanThreads + tid];
+    }
+}
+
+static int scan_incl(const int64_t* in, int64_t n, int64_t* out, void* state_buf, cudaStream_t s,
+                     const uint32_t* skip, const char* what) {
+    const int64_t tiles = scan_tiles(n);
+    GC_REQUIRE(tiles < (1ll << 31), GC_ERR_VALUE, "scan: too many items");
+    const size_t sb = scan_state_bytes(n);
+    GC_TRY(cudaMemsetAsync(state_buf, 0, sb, s), what);
+    auto* state = static_cast<uint64_t*>(state_buf);
+    auto* counter = reinterpret_cast<uint32_t*>(static_cast<char*>(state_buf) + sb - 256);
+    k_scan_incl<<<(unsigned)(tiles > 0 ? tiles : 1), kScanThreads, 0, s>>>(in, n, out, state, counter, skip);
+    GC_CHECK_LAUNCH(what);
+    return GC_OK;
+}
+
+// ---- stable LSD radix sort of (~key, id): descending keys, equal keys by ascending id
+constexpr int kRadixThreads = 256;
+constexpr int kRadixRounds = 16;
+constexpr int kRadixTile = kRadixThreads * kRadixRounds;
+constexpr int kRadixBins = 256;
+constexpr int kRadixPasses = 8;  // 64-bit keys; passes above the largest key's top bit do nothing
+
+static int64_t radix_tiles(int64_t n) { return (n + kRadixTile - 1) / kRadixTile; }
+
+__device__ __forceinline__ uint32_t desc_digit(uint64_t key, int pass) { return 255u - (uint32_t)((key >> (8 * pass)) & 0xFFu); }
+
+// bits[0] = significant bits of the largest key; bits[1 + p] = 1 if pass p is skipped
+__global__ void k_radix_bits(const uint64_t* __restrict__ maxkey, uint32_t* __restrict__ bits) {
+    if (threadIdx.x == 0) {
+        const uint64_t m = *maxkey;
+        const uint32_t b = m ? 64u - (uint32_t)__clzll((long long)m) : 0u;
+        bits[0] = b;
+        for (int p = 0; p < kRadixPasses; ++p) bits[1 + p] = (uint32_t)(8 * p) >= b;
+    }
+}
+
+__global__ void k_max_u64(const uint64_t* __restrict__ keys, int64_t n, unsigned long long* __restrict__ out) {
+    unsigned long long m = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, (unsigned long long)keys[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(kFull, m, o));
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+// per-tile digit counts, digit-major: hist[d * tiles + tile]
+__global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const uint64_t* __restrict__ keys, int64_t n, int pass,
+                                                               const uint32_t* __restrict__ bits,
+                                                               int64_t* __restrict__ hist) {
+    __shared__ uint32_t s_cnt[kRadixBins];
+    if (bits[1 + pass]) return;
+    const int tid = threadIdx.x, lane = tid & 31;
+    s_cnt[tid] = 0;
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * kRadixTile;
+    for (int r = 0; r < kRadixRounds; ++r) {
+        const int64_t i = base + r * kRadixThreads + tid;
+        const bool valid = i < n;
+        const uint32_t d = valid ? desc_digit(keys[i], pass) : 0u;
+        // one shared atomic per distinct digit per warp (zero hotness fills most bins' peers)
+        const unsigned act = __ballot_sync(kFull, valid);
+        if (valid) {
+            const unsigned peers = __match_any_sync(act, d);
+            if (lane == __ffs(peers) - 1) atomicAdd(&s_cnt[d], (uint32_t)__popc(peers));
+        }
+    }
+    __syncthreads();
+    hist[(int64_t)tid * gridDim.x + blockIdx.x] = s_cnt[tid];
+}
+
+// stable scatter: items keep their index order within a digit (round, then warp, then lane)
+__global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(const uint64_t* __restrict__ kin,
+                                                                  const uint32_t* __restrict__ vin, int64_t n, int pass,
+                                                                  const uint32_t* __restrict__ bits,
+                                                                  const int64_t* __restrict__ hist,
+                                                                  const int64_t* __restrict__ incl,
+                                                                  uint64_t* __restrict__ kout,
+                                                                  uint32_t* __restrict__ vout) {
+    constexpr int kWarps = kRadixThreads / 32;
+    __shared__ int64_t s_run[kRadixBins];
+    __shared__ uint32_t s_wcnt[kWarps][kRadixBins];
+    if (bits[1 + pass]) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    {
+        const int64_t h = (int64_t)tid * gridDim.x + blockIdx.x;
+        s_run[tid] = incl[h] - hist[h];  // exclusive offset of (digit tid, this tile)
+    }
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) s_wcnt[w][tid] = 0;
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * kRadixTile;
+    for (int r = 0; r < kRadixRounds; ++r) {
+        const int64_t i = base + r * kRadixThreads + tid;
+        const bool valid = i < n;
+        uint64_t key = 0;
+        uint32_t val = 0, d = 0, rank = 0;
+        const unsigned act = __ballot_sync(kFull, valid);
+        if (valid) {
+            key = kin[i];
+            val = vin[i];
+            d = desc_digit(key, pass);
+            const unsigned peers = __match_any_sync(act, d);
+            rank = __popc(peers & ((1u << lane) - 1u));
+            if (lane == __ffs(peers) - 1) s_wcnt[warp][d] = (uint32_t)__popc(peers);
+        }
+        __syncthreads();
+        if (valid) {
+            int64_t pos = s_run[d] + rank;
+            for (int w = 0; w < warp; ++w) pos += s_wcnt[w][d];
+            kout[pos] = key;
+            vout[pos] = val;
+        }
+        __syncthreads();
+        {
+            uint32_t add = 0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                add += s_wcnt[w][tid];
+                s_wcnt[w][tid] = 0;
+            }
+            s_run[tid] += add;
+        }
+        __syncthreads();
+    }
+}
+
+// the sorted ids are in v0 after an even number of executed passes, else in v1
+__global__ void k_widen_sorted(const uint32_t* __restrict__ v0, const uint32_t* __restrict__ v1,
+                               const uint32_t* __restrict__ bits, int64_t n, int64_t* __restrict__ out) {
+    const uint32_t passes = (bits[0] + 7) / 8;
+    const uint32_t* in = (passes & 1u) ? v1 : v0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (int64_t)in[i];
+}
+
 struct SortLayout {
-    size_t k0, k1, v0, v1, cub, total, cub_bytes;
+    size_t k0, k1, v0, v1, hist, incl, state, misc, total;
 };
 
 static SortLayout sort_layout(int64_t n) {
     SortLayout L{};
-    size_t cub_bytes = 0;
-    cub::DoubleBuffer<uint64_t> kb(nullptr, nullptr);
-    cub::DoubleBuffer<uint32_t> vb(nullptr, nullptr);
-    cub::DeviceRadixSort::SortPairsDescending(nullptr, cub_bytes, kb, vb, (int)(n > 0 ? n : 1));
+    const int64_t nh = (int64_t)kRadixBins * (radix_tiles(n) > 0 ? radix_tiles(n) : 1);
     size_t off = 0;
     L.k0 = off; off = align_up(off + 8 * (size_t)n, 256);
     L.k1 = off; off = align_up(off + 8 * (size_t)n, 256);
     L.v0 = off; off = align_up(off + 4 * (size_t)n, 256);
     L.v1 = off; off = align_up(off + 4 * (size_t)n, 256);
-    L.cub = off; off = align_up(off + cub_bytes, 256);
+    L.hist = off; off = align_up(off + 8 * (size_t)nh, 256);
+    L.incl = off; off = align_up(off + 8 * (size_t)nh, 256);
+    L.state = off; off = align_up(off + scan_state_bytes(nh), 256);
+    L.misc = off; off = align_up(off + 256, 256);  // max key (u64) + pass flags (u32[1 + passes])
     L.total = off;
-    L.cub_bytes = cub_bytes;
     return L;
-}
-
-static size_t scan_cub_bytes(int64_t n) {
-    size_t b = 0;
-    cub::DeviceScan::InclusiveSum(nullptr, b, (int64_t*)nullptr, (int64_t*)nullptr, (int)(n > 0 ? n : 1));
-    return b;
 }
 
 }  // namespace gc
@@ -223,27 +408,44 @@ int gc_descending_order(const int64_t* d_totals, int64_t n, int64_t* d_order, vo
     GC_CHECK_LAUNCH("gc_descending_order keys");
     // stable descending radix sort: equal totals keep ascending id, which is the
     // lexsort((arange(n), -totals)) order of planner.py:45
-    cub::DoubleBuffer<uint64_t> kb(k0, k1);
-    cub::DoubleBuffer<uint32_t> vb(v0, v1);
-    size_t cub_bytes = L.cub_bytes;
-    GC_TRY(cub::DeviceRadixSort::SortPairsDescending(t + L.cub, cub_bytes, kb, vb, (int)n, 0, 64, s),
-           "gc_descending_order sort");
-    k_widen<<<grid1d(n, 256), 256, 0, s>>>(vb.Current(), d_order, n);
+    auto* maxkey = reinterpret_cast<unsigned long long*>(t + L.misc);
+    auto* bits = reinterpret_cast<uint32_t*>(t + L.misc + 8);
+    GC_TRY(cudaMemsetAsync(maxkey, 0, 8, s), "gc_descending_order memset");
+    k_max_u64<<<grid1d(n, 256), 256, 0, s>>>(k0, n, maxkey);
+    k_radix_bits<<<1, 32, 0, s>>>(reinterpret_cast<const uint64_t*>(maxkey), bits);
+    GC_CHECK_LAUNCH("gc_descending_order max");
+    const int64_t tiles = radix_tiles(n);
+    GC_REQUIRE(tiles < (1ll << 31), GC_ERR_VALUE, "gc_descending_order: too many items");
+    const int64_t nh = (int64_t)kRadixBins * tiles;
+    auto* hist = reinterpret_cast<int64_t*>(t + L.hist);
+    auto* incl = reinterpret_cast<int64_t*>(t + L.incl);
+    uint64_t* kb[2] = {k0, k1};
+    uint32_t* vb[2] = {v0, v1};
+    // pass p reads buffer p & 1 when every earlier pass ran; a skipped pass implies all
+    // later ones skip too (their digits are zero), so the parity stays consistent
+    for (int p = 0; p < kRadixPasses; ++p) {
+        k_radix_hist<<<(unsigned)tiles, kRadixThreads, 0, s>>>(kb[p & 1], n, p, bits, hist);
+        GC_CHECK_LAUNCH("gc_descending_order hist");
+        const int rc = scan_incl(hist, nh, incl, t + L.state, s, bits + 1 + p, "gc_descending_order scan");
+        if (rc != GC_OK) return rc;
+        k_radix_scatter<<<(unsigned)tiles, kRadixThreads, 0, s>>>(kb[p & 1], vb[p & 1], n, p, bits, hist, incl,
+                                                                  kb[(p + 1) & 1], vb[(p + 1) & 1]);
+        GC_CHECK_LAUNCH("gc_descending_order scatter");
+    }
+    k_widen_sorted<<<grid1d(n, 256), 256, 0, s>>>(v0, v1, bits, n, d_order);
     GC_CHECK_LAUNCH("gc_descending_order widen");
     return GC_OK;
 }
 
 size_t gc_order_scan_temp_bytes(int64_t n) {
     if (n < 0) return 0;
-    return align_up(8 * (size_t)n, 256) + align_up(scan_cub_bytes(n), 256);
+    return align_up(8 * (size_t)n, 256) + scan_state_bytes(n);
 }
 
 static int order_scan(const int64_t* vals, int64_t n, int64_t* d_out, void* d_temp, size_t temp_bytes, cudaStream_t s,
                       const char* what) {
-    size_t cub_bytes = scan_cub_bytes(n);
-    char* t = static_cast<char*>(d_temp);
-    GC_TRY(cub::DeviceScan::InclusiveSum(t + align_up(8 * (size_t)n, 256), cub_bytes, vals, d_out, (int)n, s), what);
-    return GC_OK;
+    (void)temp_bytes;
+    return scan_incl(vals, n, d_out, static_cast<char*>(d_temp) + align_up(8 * (size_t)n, 256), s, nullptr, what);
 }
 
 int gc_topo_prefix_bytes(const uint64_t* d_row_offsets, const int64_t* d_order, int64_t n, uint32_t u32_bytes,
