@@ -72,9 +72,12 @@ def test_boundaries_match_linear_scan(golden):
         PL.boundary_topology(orders, -1.0, graph, spec)
 
 
-@pytest.mark.parametrize("n,k,hi", [(2_000_003, 8, 5), (300_000, 3, 1000), (100_000, 1, 2**40)])
+@pytest.mark.parametrize("n,k,hi", [(2_000_003, 8, 5), (300_000, 3, 1000), (100_000, 1, 2**40), (50_000, 2, 1),
+                                    (70_001, 2, 2**61)])
 def test_ranking_with_heavy_ties_matches_lexsort(n, k, hi):
-    """Stable descending sort: ties (many, with small hi) must stay in ascending-id order."""
+    """Stable descending sort: ties (many, with small hi) must stay in ascending-id order.
+    The radix sort runs only the digit passes below the largest total's top bit: all
+    totals zero (hi=1) runs none, totals near 2^62 (hi=2^61, k=2) run all eight."""
     from paper_2305_16588_b200 import planner as PL
 
     rng = np.random.default_rng(n)
