@@ -345,6 +345,13 @@ int gc_host_unregister(void* host_ptr);
 /* Copy `bytes` (a multiple of 4) from device memory into mapped pinned host memory with
  * SM stores (no DMA engine: small reads that must not queue behind bulk D2H copies). */
 int gc_copy_d2h_mapped(const void* d_src, void* h_dst, uint64_t bytes, void* stream);
+/* Pack a padded window array for delivery (SampleGatherPipeline.window_to_host): batch
+ * b's rows [0, d_ptr[b+1] - d_ptr[b]) of `row_bytes` bytes at d_src + b*src_stride_bytes
+ * go to d_dst from row d_ptr[b] on; max_rows bounds every batch's row count (grid size).
+ * narrow16: the rows are u32 values stored as their low 16 bits (relabelled ids of a
+ * window whose batches have <= 65536 distinct vertices). One launch per array. */
+int gc_pack_segments(const void* d_src, uint64_t src_stride_bytes, uint64_t row_bytes, const int64_t* d_ptr,
+                     uint32_t num_batches, uint64_t max_rows, int narrow16, void* d_dst, void* stream);
 
 /* Host tier through the CUDA VMM API (cuMemCreate, CU_MEM_LOCATION_TYPE_HOST_NUMA):
  * pinned host memory mapped for the CPU and every GPU at one address with the

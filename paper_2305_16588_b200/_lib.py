@@ -163,6 +163,7 @@ SIGNATURES = {
                            [ctypes.POINTER(GcFeatureStore), V, U64, V, U32, U32, V, U64, V, V, U64, V, V]),
     "gc_host_unregister": (ctypes.c_int, [V]),
     "gc_copy_d2h_mapped": (ctypes.c_int, [V, V, U64, V]),
+    "gc_pack_segments": (ctypes.c_int, [V, U64, U64, V, U32, U64, ctypes.c_int, V, V]),
     "gc_host_alloc_numa": (ctypes.c_int, [SZ, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(SZ)]),
     "gc_host_free_numa": (ctypes.c_int, [V, SZ]),
     "gc_synth_zipf_targets": (ctypes.c_int, [U64, U64, U64, U64, V, U64, U64, U64, U64, V, V]),

@@ -171,9 +171,50 @@ __global__ void k_copy_to_mapped(const uint32_t* __restrict__ src, uint32_t* dst
         dst[i] = src[i];
     __threadfence_system();
 }
+
+// Segment pack of a padded window array (grid.y = batch): batch b's first
+// (ptr[b+1] - ptr[b]) rows, each `words` u32, move to the packed array at row ptr[b];
+// NARROW stores each u32 as its low 16 bits.
+template <bool NARROW>
+__global__ void k_pack_segments(const uint32_t* __restrict__ src, uint64_t stride_words, uint64_t words,
+                                const int64_t* __restrict__ ptr, void* __restrict__ dst) {
+    const uint32_t b = blockIdx.y;
+    const int64_t r0 = ptr[b];
+    const uint64_t n = (uint64_t)(ptr[b + 1] - r0) * words;
+    const uint32_t* s = src + b * stride_words;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t x = s[i];
+        if (NARROW)
+            static_cast<uint16_t*>(dst)[(uint64_t)r0 * words + i] = (uint16_t)x;
+        else
+            static_cast<uint32_t*>(dst)[(uint64_t)r0 * words + i] = x;
+    }
+}
 }  // namespace gc
 
 extern "C" {
+
+int gc_pack_segments(const void* d_src, uint64_t src_stride_bytes, uint64_t row_bytes, const int64_t* d_ptr,
+                     uint32_t num_batches, uint64_t max_rows, int narrow16, void* d_dst, void* stream) {
+    GC_REQUIRE(row_bytes % 4 == 0 && src_stride_bytes % 4 == 0, GC_ERR_VALUE,
+               "gc_pack_segments: row and stride bytes must be multiples of 4");
+    GC_REQUIRE(num_batches <= 65535, GC_ERR_VALUE, "gc_pack_segments: at most 65535 batches");
+    if (num_batches == 0 || row_bytes == 0 || max_rows == 0) return GC_OK;
+    GC_REQUIRE(d_src && d_ptr && d_dst, GC_ERR_VALUE, "gc_pack_segments: null pointer");
+    const uint64_t words = row_bytes / 4;
+    uint64_t gx = (max_rows * words + 255) / 256;
+    const uint64_t cap = (uint64_t)sm_count() * 8 / num_batches + 1;  // ~8 CTAs per SM over the window
+    if (gx > cap) gx = cap;
+    const dim3 grid((unsigned)gx, num_batches);
+    if (narrow16)
+        gc::k_pack_segments<true><<<grid, 256, 0, as_stream(stream)>>>(static_cast<const uint32_t*>(d_src),
+                                                                     src_stride_bytes / 4, words, d_ptr, d_dst);
+    else
+        gc::k_pack_segments<false><<<grid, 256, 0, as_stream(stream)>>>(static_cast<const uint32_t*>(d_src),
+                                                                      src_stride_bytes / 4, words, d_ptr, d_dst);
+    GC_CHECK_LAUNCH("gc_pack_segments");
+    return GC_OK;
+}
 
 int gc_copy_d2h_mapped(const void* d_src, void* h_dst, uint64_t bytes, void* stream) {
     GC_REQUIRE(bytes % 4 == 0, GC_ERR_VALUE, "gc_copy_d2h_mapped: bytes must be a multiple of 4");

@@ -30,7 +30,10 @@ namespace gc {
 #endif
 constexpr int kHopThreads = GC_HOP_THREADS;  // CTA = one tile of kTilePos frontier positions
 constexpr int kTilePos = kHopThreads;
-constexpr int kItemCap = 16 * kHopThreads;  // staged output items per round (u64 edge indices)
+// staged output items per round: 24 KB of u32 edge indices (plain CSR) or 40 KB of
+// u64 (tiered), so a 512-position tile of fanout 10 stages in one round
+constexpr int kItemCap = 16 * kHopThreads;
+__host__ __device__ constexpr int item_cap(bool tiered) { return tiered ? 20 * kHopThreads : 24 * kHopThreads; }
 // emission items in flight per thread: a full tile of 256 positions with take =
 // fanout stages exactly `fanout` items per thread, so for the small networks S - 1
 // (the largest fanout of the network) covers it in one pass (C2 hop 3: 1.68 -> 1.60
@@ -446,7 +449,8 @@ __global__ void __launch_bounds__(kHopThreads, hop_min_blocks<S>()) k_hop_expand
         typename Reduce::TempStorage reduce;
     } tmp;
     using Item = typename std::conditional<TIERED, uint64_t, uint32_t>::type;
-    __shared__ Item s_items[kItemCap];
+    constexpr uint32_t kCap = item_cap(TIERED);
+    __shared__ Item s_items[kCap];
     __shared__ uint64_t s_prefix;
     __shared__ uint32_t s_vid;
     __shared__ uint32_t s_arrive;  // warps done with phase 2a (the first runs the look-back)
@@ -581,11 +585,11 @@ __global__ void __launch_bounds__(kHopThreads, hop_min_blocks<S>()) k_hop_expand
     uint32_t* out = p.out_nbrs + b * p.nstride;
     uint32_t* bm = p.bitmap ? p.bitmap + b * p.bwords : nullptr;
     uint32_t* sm = p.summary ? p.summary + b * p.swords : nullptr;
-    const uint32_t rounds = (total + kItemCap - 1) / kItemCap;
+    const uint32_t rounds = (total + kCap - 1) / kCap;
 
     for (uint32_t r = 0; r < max(rounds, 1u); ++r) {
-        const uint32_t r0 = r * kItemCap;
-        const uint32_t r1 = min(total, r0 + kItemCap);
+        const uint32_t r0 = r * kCap;
+        const uint32_t r1 = min(total, r0 + kCap);
         // ---- phase 2a: stage the source edge index of every output item in [r0, r1)
         bool need_warp[PPT];
 #pragma unroll
@@ -672,14 +676,17 @@ __global__ void __launch_bounds__(kHopThreads, hop_min_blocks<S>()) k_hop_expand
     }
 }
 
-// positions per thread: 2 for the small networks (fanout <= 7: a 512-position tile
-// stages at most 3584 items in one round), else 1
-static int positions_per_thread(uint32_t fanout) { return fanout < 8 ? GC_HOP_PPT : 1; }
+// positions per thread: 2 for the networks up to S = 11 (fanout <= 10: a 512-position
+// tile stages at most 5120 items in one round), else 1 — as launch_hop instantiates
+static int positions_per_thread(uint32_t fanout, bool tiered) {
+    (void)tiered;
+    return fanout < 11 ? GC_HOP_PPT : 1;
+}
 
 // positions per tile: one staging round whenever fanout <= 128
-static uint32_t tile_positions(uint32_t fanout) {
-    const uint32_t cap = (uint32_t)kTilePos * positions_per_thread(fanout);
-    uint32_t tp = kItemCap / (fanout ? fanout : 1);
+static uint32_t tile_positions(uint32_t fanout, bool tiered) {
+    const uint32_t cap = (uint32_t)kTilePos * positions_per_thread(fanout, tiered);
+    uint32_t tp = (uint32_t)item_cap(tiered) / (fanout ? fanout : 1);
     tp = tp >= cap ? cap : (tp / 32) * 32;
     return tp < 32 ? 32 : tp;
 }
@@ -699,11 +706,12 @@ static int network_slots(uint32_t fanout) {
 
 template <int S>
 static void launch_hop(const HopParams& p, dim3 grid, bool tiered, cudaStream_t s) {
-    constexpr int PPT = S > 0 && S <= 8 ? GC_HOP_PPT : 1;
+    constexpr int PPT_CSR = S > 0 && S <= 11 ? GC_HOP_PPT : 1;
+    constexpr int PPT_TIERED = PPT_CSR;
     if (tiered)
-        k_hop_expand<S, true, PPT><<<grid, kHopThreads, 0, s>>>(p);
+        k_hop_expand<S, true, PPT_TIERED><<<grid, kHopThreads, 0, s>>>(p);
     else
-        k_hop_expand<S, false, PPT><<<grid, kHopThreads, 0, s>>>(p);
+        k_hop_expand<S, false, PPT_CSR><<<grid, kHopThreads, 0, s>>>(p);
 }
 
 }  // namespace gc
@@ -750,7 +758,10 @@ int gc_hop_expand(const gc_topology_t* topo, const uint32_t* d_frontier, uint64_
     const size_t need = gc_hop_expand_temp_bytes(num_batches, max_frontier);
     GC_REQUIRE(d_temp && temp_bytes >= need, GC_ERR_VALUE, "gc_hop_expand: temp buffer too small");
     cudaStream_t s = as_stream(stream);
-    const uint32_t tile_pos = tile_positions(fanout);
+    // the plain-CSR kernel stages 32-bit edge indices; a CSR with 2^32 or more edges
+    // takes the tiered kernel (64-bit items), which also reads a location-free CSR
+    const bool tiered = topo->location != nullptr || topo->full_on_host || graph->num_edges >= (1ull << 32);
+    const uint32_t tile_pos = tile_positions(fanout, tiered);
     const unsigned tiles = tiles_for(max_frontier, tile_pos);
     HopParams p{};
     p.tile_pos = tile_pos;
@@ -801,9 +812,6 @@ int gc_hop_expand(const gc_topology_t* topo, const uint32_t* d_frontier, uint64_
            "gc_hop_expand memset");
     GC_REQUIRE(num_batches <= 65535 && tiles < (1u << 31), GC_ERR_VALUE, "gc_hop_expand: window too large");
     const dim3 grid(tiles, num_batches);
-    // the plain-CSR kernel stages 32-bit edge indices; a CSR with 2^32 or more edges
-    // takes the tiered kernel (64-bit items), which also reads a location-free CSR
-    const bool tiered = topo->location != nullptr || topo->full_on_host || graph->num_edges >= (1ull << 32);
     switch (network_slots(fanout)) {
         case 4: launch_hop<4>(p, grid, tiered, s); break;
         case 6: launch_hop<6>(p, grid, tiered, s); break;

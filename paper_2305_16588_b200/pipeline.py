@@ -328,20 +328,37 @@ class SampleGatherPipeline:
         def ptr(sizes):
             return np.concatenate(([0], np.cumsum(sizes))).astype(np.int64)
 
+        lib = _lib.lib()
+
+        def dev_buffer(key, shape, dtype):
+            # persistent per staging set (the caller alternates sets and waits for a set's
+            # copies before reusing it): no allocator traffic inside an epoch
+            t = st.get(key)
+            if t is None or t.shape[0] < shape[0] or t.shape[1:] != shape[1:] or t.dtype != dtype:
+                rows = max(shape[0] + shape[0] // 4, 1)
+                t = torch.empty((rows,) + tuple(shape[1:]), dtype=dtype, device="cuda")
+                st[key] = t
+            return t
+
         def pack(name, buf, sizes, narrow=False):
-            # sync-free segment pack: flat row of packed element k = b * cap + (k - ptr[b])
+            # one gc_pack_segments launch: batch b's first sizes[b] rows of the padded
+            # [nb, cap, ...] buffer land at row ptr[b] of a packed device array
             total = int(sizes.sum())
-            cap = buf.shape[1]
+            dtype = torch.int16 if narrow else buf.dtype
+            tail = tuple(buf.shape[2:])
+            packed = dev_buffer(f"_dev_{name}", (total,) + tail, dtype)[:total]
             if total:
-                sz = torch.from_numpy(sizes).to(buf.device, non_blocking=True)
-                shift = torch.from_numpy(np.arange(nb, dtype=np.int64) * cap - ptr(sizes)[:-1]).to(
-                    buf.device, non_blocking=True)
-                rows = torch.arange(total, device=buf.device) + torch.repeat_interleave(shift, sz, output_size=total)
-                packed = buf[:nb].reshape((nb * cap,) + tuple(buf.shape[2:])).index_select(0, rows)
-            else:
-                packed = buf.new_empty((0,) + tuple(buf.shape[2:]))
-            if narrow:
-                packed = packed.to(torch.int16)  # values < 2^16: the low 16 bits, uint16 pattern
+                p = ptr(sizes)
+                hp = st.get(f"_ptr_{name}")
+                if hp is None or hp.numel() < p.size:
+                    hp = st[f"_ptr_{name}"] = torch.empty(max(p.size, 1024), dtype=torch.int64, pin_memory=True)
+                hp[: p.size].copy_(torch.from_numpy(p))
+                dp = dev_buffer(f"_dptr_{name}", (hp.numel(),), torch.int64)
+                dp[: p.size].copy_(hp[: p.size], non_blocking=True)
+                row_bytes = buf.element_size() * int(np.prod(tail, dtype=np.int64))
+                _lib.check(lib.gc_pack_segments(buf.data_ptr(), buf.stride(0) * buf.element_size(), row_bytes,
+                                                dp.data_ptr(), nb, int(sizes.max()), int(narrow), packed.data_ptr(),
+                                                _lib.stream_handle(main)), "pack_segments")
             host = st.get(name)
             if host is None or host.shape[0] < total or host.shape[1:] != packed.shape[1:] or host.dtype != packed.dtype:
                 # 25% slack: pinned allocations are slow, so a slightly larger window later reuses it
@@ -354,7 +371,6 @@ class SampleGatherPipeline:
             copy.wait_event(ev)
             with torch.cuda.stream(copy):
                 host[:total].copy_(packed, non_blocking=True)
-            packed.record_stream(copy)  # the allocator keeps it until the copy is done
             return host[:total]
 
         out = {"unique_ptr": ptr(ucount), "offsets_ptr": [], "local_ptr": [], "offsets": [], "local": [],
