@@ -21,7 +21,7 @@ from . import _lib
 from .cache import FeatureStore
 from .graph import CsrGraph
 from .rng import ROLE_SHUFFLE, KeyedRng
-from .sampling import DeviceHotness, SamplingConfig, WindowSampler, batch_hop_keys, check_seed_pool
+from .sampling import MAX_WINDOW, DeviceHotness, SamplingConfig, WindowSampler, batch_hop_keys, check_seed_pool
 
 # kernels each stage launches (for the bench's gpu_launches count): the permutation is a
 # histogram, a 3-kernel scan of the bucket counts, a scatter and the in-bucket rank/emit
@@ -89,7 +89,7 @@ class SampleGatherPipeline:
         self.store = store
         B = cfg.batch_size
         nb = max(1, math.ceil(max_pool / B))
-        self.window = min(nb, window or nb)
+        self.window = min(nb, window or nb, MAX_WINDOW)
         if lanes < 1:
             raise ValueError("lanes must be >= 1")
         self.lane_samplers = []

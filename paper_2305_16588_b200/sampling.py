@@ -171,6 +171,8 @@ class WindowSampler:
         self.H = len(self.fanouts)
         self.B = int(batch_size)
         self.W = int(window)
+        if not 1 <= self.W <= MAX_WINDOW:
+            raise ValueError(f"window must be in [1, {MAX_WINDOW}] batches")
         self.relabel = relabel
         caps = [self.B]
         for f in self.fanouts:
@@ -470,9 +472,13 @@ class GpuTrace:
     num_batches: int = 0
 
 
+MAX_WINDOW = 65535  # batches per window: the hop/pack kernels put the batch in grid.y
+
+
 def _window_for(sampler_caps: list[int], words: int, num_batches: int, budget_bytes: int = 2 << 30) -> int:
     per_batch = 4 * (2 * sum(sampler_caps) + len(sampler_caps) + 2 * words) + 4 * min(sum(sampler_caps), 1 << 30)
-    return max(1, min(num_batches, budget_bytes // max(per_batch, 1)))
+    # <= 65535: the batch index is a launch's grid.y
+    return max(1, min(num_batches, budget_bytes // max(per_batch, 1), MAX_WINDOW))
 
 
 class EpochRunner:
