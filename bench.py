@@ -872,7 +872,7 @@ def e2e_run(args, g, cfg, store, pool, root, clique, local_idx, world, results_t
             if ev is not None:
                 torch.cuda.current_stream().wait_event(ev)  # the timed region ends after the last copy
 
-    steps = max(1, min(args.steps, 5))
+    steps = max(1, min(args.steps, 10))
     for e in range(min(args.warmup, 2)):
         step(e)
     settle()
