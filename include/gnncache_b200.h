@@ -50,8 +50,8 @@ int gc_abi_version(void);
  * 32-bit REDUX extraction and always use the 64-bit path (a test hook: both paths
  * must give identical output). */
 #define GC_OPT_EXACT_SELECTION 1
-/* GC_OPT_DEFER_CTAS: CTAs (128 threads each) of gc_gather_deferred's host-row kernel
- * (default 148, one per SM); a tuning knob for the PCIe-bound part. */
+/* GC_OPT_DEFER_CTAS: CTAs (one warp each, TMA bulk copies) of gc_gather_deferred's
+ * host-row kernel (default 296, two per SM); a tuning knob for the PCIe-bound part. */
 #define GC_OPT_DEFER_CTAS 2
 /* GC_OPT_GATHER_CTAS_PER_SM: grid of the warp-per-row gather in CTAs per SM over the
  * whole window (default 16: the GPU is full). Fewer leave SM room for another lane's

@@ -221,10 +221,8 @@ __global__ void __launch_bounds__(256, VPL == 1 ? GC_GATHER_MIN_BLOCKS : 4) k_ga
     }
 }
 
-// host-row kernel footprint: 2 warps and ~32 registers per thread per CTA, so its CTAs
-// still fit in the few thousand registers the sampling kernels leave free on an SM
-constexpr int kDeferThreads = 64;
-constexpr int kDeferRows = 4;
+// host-row kernel grid (GC_OPT_DEFER_CTAS): 2 CTAs per SM of one warp and ~33 KB of
+// shared memory each, so they fit beside the sampling kernels
 static int g_defer_ctas = 296;
 void set_defer_ctas(int ctas) { g_defer_ctas = ctas; }
 // warp-per-row gather grid: CTAs per SM over the whole window (16 fills the GPU; fewer
@@ -232,39 +230,75 @@ void set_defer_ctas(int ctas) { g_defer_ctas = ctas; }
 static int g_gather_ctas_per_sm = 16;
 void set_gather_ctas_per_sm(int v) { g_gather_ctas_per_sm = v; }
 
-// Deferred host-tier rows: warp per row, ROWS rows in flight per warp, a small grid
-// (PCIe latency needs few rows in flight; the SMs stay free for the next window).
-template <int ROWS>
-__global__ void __launch_bounds__(kDeferThreads) k_gather_deferred(const char* __restrict__ host_rows, uint32_t row_bytes,
-                                                         const DeferredRow* __restrict__ list,
-                                                         const uint32_t* __restrict__ count, char* out) {
+// Deferred host-tier rows by TMA bulk copies: a 32-thread CTA stages up to R list
+// entries in shared memory, then one lane issues R cp.async.bulk reads of whole rows
+// from the pinned host table (UVA; completion counted on one mbarrier per row) and, as
+// each lands, a bulk write of the row to its destination. R rows (32 KB) stay in flight
+// per CTA while the CTA holds one warp's issue slots and no registers to speak of, so
+// the PCIe-latency-bound reads leave the SMs to the next window's sampling kernels.
+// (tools/tma_host_probe.cu: one such CTA per SM reaches the box's host-read limit.)
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__global__ void __launch_bounds__(32) k_gather_deferred_tma(const char* __restrict__ host_rows, uint32_t row_bytes,
+                                                            const DeferredRow* __restrict__ list,
+                                                            const uint32_t* __restrict__ count, char* out, int R) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem);          // [R] mbarriers
+    uint64_t* src = bar + R;                                     // [R] host byte offsets
+    uint64_t* dst = src + R;                                     // [R] destination rows
+    char* buf = reinterpret_cast<char*>(smem) + ((size_t)24 * R + 127) / 128 * 128;  // [R][row_bytes]
     const uint32_t n = *count;
-    const uint32_t per_row = row_bytes / 16;
-    const int lane = threadIdx.x & 31;
-    const uint32_t warps = gridDim.x * (blockDim.x / 32);
-    const uint32_t wid = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-    for (uint32_t r0 = wid * ROWS; r0 < n; r0 += warps * ROWS) {
-        uint64_t my_dst = 0;
-        uint32_t my_id = 0;
-        if (lane < ROWS && r0 + lane < n) {
-            const DeferredRow e = list[r0 + lane];
-            my_dst = e.dst_row;
-            my_id = e.id;
-        }
-        uint4 v[ROWS];
-#pragma unroll
-        for (int j = 0; j < ROWS; ++j) {
-            const uint32_t id = __shfl_sync(kFull, my_id, j);
-            v[j] = (r0 + j < n && (uint32_t)lane < per_row)
-                       ? ld_stream16(host_rows + (uint64_t)id * row_bytes + 16 * lane)
-                       : make_uint4(0, 0, 0, 0);
-        }
-#pragma unroll
-        for (int j = 0; j < ROWS; ++j) {
-            const uint64_t dst = __shfl_sync(kFull, my_dst, j);
-            if (r0 + j < n && (uint32_t)lane < per_row) st_stream16(out + dst * row_bytes + 16 * lane, v[j]);
-        }
+    const int lane = threadIdx.x;
+    if (lane == 0) {
+        for (int k = 0; k < R; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[k])));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    __syncwarp();
+    uint32_t phase = 0;
+    for (uint32_t r0 = blockIdx.x * (uint32_t)R; r0 < n; r0 += gridDim.x * (uint32_t)R) {
+        const uint32_t m = min((uint32_t)R, n - r0);
+        for (uint32_t k = lane; k < m; k += 32) {
+            const DeferredRow e = list[r0 + k];
+            src[k] = (uint64_t)e.id * row_bytes;
+            dst[k] = e.dst_row;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            for (uint32_t k = 0; k < m; ++k) {
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&bar[k])),
+                             "r"(row_bytes)
+                             : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        smem_addr(buf + (size_t)k * row_bytes)),
+                    "l"(host_rows + src[k]), "r"(row_bytes), "r"(smem_addr(&bar[k]))
+                    : "memory");
+            }
+            for (uint32_t k = 0; k < m; ++k) {
+                uint32_t done = 0;
+                while (!done)
+                    asm volatile(
+                        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                        : "=r"(done)
+                        : "r"(smem_addr(&bar[k])), "r"(phase)
+                        : "memory");
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                                 out + dst[k] * row_bytes),
+                             "r"(smem_addr(buf + (size_t)k * row_bytes)), "r"(row_bytes)
+                             : "memory");
+            }
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // the buffers may be refilled
+        }
+        phase ^= 1u;  // only the CTA's last round can be partial
+        __syncwarp();
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // writes complete before exit
+}
+
+static int defer_rows_in_flight(uint32_t row_bytes) {
+    int r = (int)(32768u / row_bytes);
+    return r > 64 ? 64 : (r < 1 ? 1 : r);
 }
 
 // accumulate_hotness bincount (sampling.py:171-173) with warp aggregation for hot ids
@@ -383,8 +417,10 @@ static int gather_impl(const gc_feature_store_t* store, const uint32_t* d_ids, u
             GC_TRY(cudaEventRecord(e0, s), "event record");
             GC_TRY(cudaStreamWaitEvent(hs, e0, 0), "stream wait");
         }
-        k_gather_deferred<kDeferRows><<<g_defer_ctas, kDeferThreads, 0, hs>>>(static_cast<const char*>(store->host_rows), store->row_bytes,
-                                                   p.defer, p.defer_count, p.out);
+        const int R = defer_rows_in_flight(store->row_bytes);
+        const size_t smem = ((size_t)24 * R + 127) / 128 * 128 + (size_t)R * store->row_bytes;
+        k_gather_deferred_tma<<<g_defer_ctas, 32, smem, hs>>>(static_cast<const char*>(store->host_rows),
+                                                               store->row_bytes, p.defer, p.defer_count, p.out, R);
         GC_CHECK_LAUNCH("gc_gather_deferred");
         if (hs != s) {
             GC_TRY(cudaEventRecord(e1, hs), "event record");

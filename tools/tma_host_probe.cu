@@ -34,6 +34,16 @@ __global__ void k_gather_sm(const uint4* __restrict__ table, const uint32_t* __r
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+// issue-bound filler shaped like the hop kernel (6 x 256-thread CTAs per SM, 40 regs)
+__global__ void __launch_bounds__(256, 6) k_spin(uint32_t iters, uint32_t* sink) {
+    uint32_t a = threadIdx.x, b = blockIdx.x;
+    for (uint32_t i = 0; i < iters; ++i) {
+        a = a * 1664525u + b;
+        b = min(a ^ b, b + 7u);
+    }
+    if (a == 0x12345678u) sink[0] = b;
+}
+
 template <int R>
 __global__ void __launch_bounds__(32) k_gather_tma(const char* __restrict__ table, const uint32_t* __restrict__ ids,
                                                    uint64_t rows, char* __restrict__ out) {
@@ -125,6 +135,39 @@ int main(int argc, char** argv) {
     run("TMA, 2 x 32-thread CTAs/SM, R=32", [&] { k_gather_tma<32><<<sms * 2, 32>>>(dtable, ids, rows, out); });
     run("TMA, 4 x 32-thread CTAs/SM, R=32", [&] { k_gather_tma<32><<<sms * 4, 32>>>(dtable, ids, rows, out); });
     run("TMA, 4 x 32-thread CTAs/SM, R=64", [&] { k_gather_tma<64><<<sms * 4, 32>>>(dtable, ids, rows, out); });
+    // the host-row gather concurrent with other work on a second stream: HBM copies
+    // (memory-bound) or a spin kernel that keeps every SM's issue slots busy
+    {
+        cudaStream_t s1, s2;
+        CK(cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+        char *big_a, *big_b;
+        const size_t big = 8ull << 30;
+        CK(cudaMalloc(&big_a, big));
+        CK(cudaMalloc(&big_b, big));
+        for (int mode = 0; mode < 3; ++mode) {
+            if (mode == 2)  // the filler reserves the whole carveout for shared memory: room for TMA CTAs
+                CK(cudaFuncSetAttribute(k_spin, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+            cudaEvent_t h0, h1;
+            CK(cudaEventCreate(&h0));
+            CK(cudaEventCreate(&h1));
+            CK(cudaDeviceSynchronize());
+            for (int i = 0; i < 6; ++i) {
+                if (mode == 0)
+                    CK(cudaMemcpyAsync(big_b, big_a, big, cudaMemcpyDeviceToDevice, s2));
+                else
+                    k_spin<<<sms * 6, 256, 0, s2>>>(4000000u, (uint32_t*)big_b);
+            }
+            CK(cudaEventRecord(h0, s1));
+            k_gather_tma<32><<<sms * 2, 32, 0, s1>>>(dtable, ids, rows, out);
+            CK(cudaEventRecord(h1, s1));
+            CK(cudaDeviceSynchronize());
+            float ms = 0;
+            CK(cudaEventElapsedTime(&ms, h0, h1));
+            printf("TMA host gather while %-28s %8.3f ms  %6.1f GB/s\n",
+                   mode == 0 ? "8 GB D2D copies run:" : mode == 1 ? "SMs spin (hop-like occupancy):" : "SMs spin, carveout 100% smem:", ms, rows * kRowBytes / (ms * 1e6));
+        }
+    }
     // correctness of the TMA copy against the table
     char* check = (char*)malloc(rows * kRowBytes);
     CK(cudaMemcpy(check, out, rows * kRowBytes, cudaMemcpyDeviceToHost));
