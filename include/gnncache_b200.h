@@ -191,6 +191,11 @@ int gc_unique_compact(const gc_visited_t* visited, uint32_t num_batches, uint32_
 int gc_relabel(const uint32_t* d_ids, uint64_t ids_stride, const uint32_t* d_ids_count, uint32_t max_count,
                uint32_t num_batches, const uint32_t* d_rank_table, uint64_t bitmap_words, uint32_t* d_local,
                void* stream);
+/* The same with 16-bit local ids (every batch of the window has <= 65536 distinct
+ * vertices): d_local holds u16, element stride ids_stride. */
+int gc_relabel16(const uint32_t* d_ids, uint64_t ids_stride, const uint32_t* d_ids_count, uint32_t max_count,
+                 uint32_t num_batches, const uint32_t* d_rank_table, uint64_t bitmap_words, uint16_t* d_local,
+                 void* stream);
 /* Mark ids in the per-batch visited sets (seeds of a zero-hop config). */
 int gc_mark_visited(const uint32_t* d_ids, uint64_t ids_stride, const uint32_t* d_count, uint32_t max_count,
                     uint32_t num_batches, const gc_visited_t* visited, void* stream);
@@ -259,7 +264,7 @@ typedef struct {
     int32_t hops;                                    /* L; levels 0..L */
     const int32_t* counts;                           /* [L+1, W] real positions per level */
     int64_t counts_stride;                           /* W */
-    const int32_t* local[GC_TREE_MAX_LEVELS];        /* level k relabelled ids [W, local_stride[k]] */
+    const int32_t* local[GC_TREE_MAX_LEVELS];        /* level k relabelled ids [W, local_stride[k]] (u16 when local_bits == 16) */
     int64_t local_stride[GC_TREE_MAX_LEVELS];
     const int32_t* offsets[GC_TREE_MAX_LEVELS];      /* hop h child offsets [W, offsets_stride[h]] */
     int64_t offsets_stride[GC_TREE_MAX_LEVELS];
@@ -267,6 +272,7 @@ typedef struct {
     int64_t seeds_stride;
     const int64_t* labels;                           /* class per vertex [n] (nullable) */
     int64_t caps[GC_TREE_MAX_LEVELS];                /* padded slots per level */
+    int32_t local_bits;                              /* 16: local[] hold u16 ids (gc_relabel16); else u32 */
 } gc_tree_src_t;
 
 /* Stage batch *d_batch (device scalar, so a captured graph replays for any batch):
@@ -348,10 +354,10 @@ int gc_copy_d2h_mapped(const void* d_src, void* h_dst, uint64_t bytes, void* str
 /* Pack a padded window array for delivery (SampleGatherPipeline.window_to_host): batch
  * b's rows [0, d_ptr[b+1] - d_ptr[b]) of `row_bytes` bytes at d_src + b*src_stride_bytes
  * go to d_dst from row d_ptr[b] on; max_rows bounds every batch's row count (grid size).
- * narrow16: the rows are u32 values stored as their low 16 bits (relabelled ids of a
- * window whose batches have <= 65536 distinct vertices). One launch per array. */
+ * mode: 0 copy (rows of u32 words), 1 u32 -> u16 (low 16 bits: relabelled ids of a window
+ * whose batches have <= 65536 distinct vertices), 2 copy u16, 3 u16 -> u32. */
 int gc_pack_segments(const void* d_src, uint64_t src_stride_bytes, uint64_t row_bytes, const int64_t* d_ptr,
-                     uint32_t num_batches, uint64_t max_rows, int narrow16, void* d_dst, void* stream);
+                     uint32_t num_batches, uint64_t max_rows, int mode, void* d_dst, void* stream);
 
 /* Host tier through the CUDA VMM API (cuMemCreate, CU_MEM_LOCATION_TYPE_HOST_NUMA):
  * pinned host memory mapped for the CPU and every GPU at one address with the

@@ -100,6 +100,7 @@ class GcTreeSrc(ctypes.Structure):
         ("seeds_stride", ctypes.c_int64),
         ("labels", ctypes.c_void_p),
         ("caps", ctypes.c_int64 * GC_TREE_MAX_LEVELS),
+        ("local_bits", ctypes.c_int32),
     ]
 
 
@@ -135,6 +136,7 @@ SIGNATURES = {
     "gc_unique_temp_bytes": (SZ, [U32, ctypes.POINTER(GcVisited)]),
     "gc_unique_compact": (ctypes.c_int, [ctypes.POINTER(GcVisited), U32, V, U64, V, V, V, ctypes.c_int, V, SZ, V]),
     "gc_relabel": (ctypes.c_int, [V, U64, V, U32, U32, V, U64, V, V]),
+    "gc_relabel16": (ctypes.c_int, [V, U64, V, U32, U32, V, U64, V, V]),
     "gc_mark_visited": (ctypes.c_int, [V, U64, V, U32, U32, ctypes.POINTER(GcVisited), V]),
     "gc_synth_features": (ctypes.c_int, [U64, U64, U32, V, V]),
     "gc_bitmap_clear": (ctypes.c_int, [ctypes.POINTER(GcVisited), U32, V, U64, V, U32, V]),

@@ -304,16 +304,19 @@ __device__ __forceinline__ uint32_t rank_of(const uint2* __restrict__ rt, uint32
 #endif
 constexpr int kRelabelGroups = GC_RELABEL_GROUPS;
 
-// VEC ids per thread per step (16-byte streaming loads/stores when the batch stride
-// keeps rows 16-byte aligned), so VEC independent rank-table loads are in flight
-template <int VEC>
+// VEC ids per thread per step (16-byte streaming loads when the batch stride keeps
+// rows 16-byte aligned), so VEC independent rank-table loads are in flight. Local ids
+// are stored as OUT (u32, or u16 when every batch of the window has at most 65536
+// distinct vertices: a quarter less traffic for the pass, which moves 4 + sizeof(OUT)
+// bytes per sampled id).
+template <int VEC, typename OUT>
 __global__ void k_relabel(const uint32_t* __restrict__ ids, uint64_t stride, const uint32_t* __restrict__ count,
-                          const uint2* __restrict__ rank, uint64_t bwords, uint32_t* __restrict__ local) {
+                          const uint2* __restrict__ rank, uint64_t bwords, OUT* __restrict__ local) {
     const uint32_t b = blockIdx.y;
     const uint32_t c = count[b];
     const uint2* rt = rank + b * bwords;
     const uint32_t* in = ids + b * stride;
-    uint32_t* out = local + b * stride;
+    OUT* out = local + b * stride;
     if constexpr (VEC == 4) {
         const uint32_t c4 = c / 4;
         const uint32_t step = gridDim.x * blockDim.x;
@@ -334,14 +337,21 @@ __global__ void k_relabel(const uint32_t* __restrict__ ids, uint64_t stride, con
                 r[j].w = rank_of(rt, u[j].w);
             }
 #pragma unroll
-            for (int j = 0; j < kRelabelGroups; ++j)
-                if (k + j * step < c4) __stcs(reinterpret_cast<uint4*>(out) + k + j * step, r[j]);
+            for (int j = 0; j < kRelabelGroups; ++j) {
+                if (k + j * step >= c4) continue;
+                if constexpr (sizeof(OUT) == 4) {
+                    __stcs(reinterpret_cast<uint4*>(out) + k + j * step, r[j]);
+                } else {  // four u16 in one 8-byte store
+                    const uint2 v = make_uint2((r[j].x & 0xFFFFu) | (r[j].y << 16), (r[j].z & 0xFFFFu) | (r[j].w << 16));
+                    __stcs(reinterpret_cast<uint2*>(out) + k + j * step, v);
+                }
+            }
         }
         const uint32_t k = c4 * 4 + blockIdx.x * blockDim.x + threadIdx.x;
-        if (k < c) out[k] = rank_of(rt, in[k]);
+        if (k < c) out[k] = (OUT)rank_of(rt, in[k]);
     } else {
         for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < c; k += gridDim.x * blockDim.x)
-            out[k] = rank_of(rt, __ldcs(in + k));
+            out[k] = (OUT)rank_of(rt, __ldcs(in + k));
     }
 }
 
@@ -378,6 +388,30 @@ static unsigned grid_x(uint32_t max_count, int block) {
     if (g < 1) g = 1;
     if (g > 1024) g = 1024;
     return (unsigned)g;
+}
+
+}  // namespace gc
+
+namespace gc {
+template <typename OUT>
+static int relabel(const uint32_t* d_ids, uint64_t ids_stride, const uint32_t* d_ids_count, uint32_t max_count,
+                   uint32_t num_batches, const uint32_t* d_rank_table, uint64_t bitmap_words, OUT* d_local,
+                   void* stream, const char* what) {
+    GC_REQUIRE(num_batches < 65536, GC_ERR_VALUE, "gc_relabel: at most 65535 batches per call");
+    if (num_batches == 0 || max_count == 0) return GC_OK;
+    const auto* rt = reinterpret_cast<const uint2*>(d_rank_table);
+    const bool vec = ids_stride % 4 == 0 && (uintptr_t)d_ids % 16 == 0 && (uintptr_t)d_local % (4 * sizeof(OUT)) == 0;
+    if (vec) {
+        dim3 grid(grid_x((max_count + 4 * kRelabelGroups - 1) / (4 * kRelabelGroups), 256), num_batches);
+        k_relabel<4, OUT><<<grid, 256, 0, as_stream(stream)>>>(d_ids, ids_stride, d_ids_count, rt, bitmap_words,
+                                                               d_local);
+    } else {
+        dim3 grid(grid_x(max_count, 256), num_batches);
+        k_relabel<1, OUT><<<grid, 256, 0, as_stream(stream)>>>(d_ids, ids_stride, d_ids_count, rt, bitmap_words,
+                                                               d_local);
+    }
+    GC_CHECK_LAUNCH(what);
+    return GC_OK;
 }
 
 }  // namespace gc
@@ -475,19 +509,15 @@ int gc_unique_compact(const gc_visited_t* visited, uint32_t num_batches, uint32_
 int gc_relabel(const uint32_t* d_ids, uint64_t ids_stride, const uint32_t* d_ids_count, uint32_t max_count,
                uint32_t num_batches, const uint32_t* d_rank_table, uint64_t bitmap_words, uint32_t* d_local,
                void* stream) {
-    GC_REQUIRE(num_batches < 65536, GC_ERR_VALUE, "gc_relabel: at most 65535 batches per call");
-    if (num_batches == 0 || max_count == 0) return GC_OK;
-    const auto* rt = reinterpret_cast<const uint2*>(d_rank_table);
-    const bool vec = ids_stride % 4 == 0 && (uintptr_t)d_ids % 16 == 0 && (uintptr_t)d_local % 16 == 0;
-    if (vec) {
-        dim3 grid(grid_x((max_count + 4 * kRelabelGroups - 1) / (4 * kRelabelGroups), 256), num_batches);
-        k_relabel<4><<<grid, 256, 0, as_stream(stream)>>>(d_ids, ids_stride, d_ids_count, rt, bitmap_words, d_local);
-    } else {
-        dim3 grid(grid_x(max_count, 256), num_batches);
-        k_relabel<1><<<grid, 256, 0, as_stream(stream)>>>(d_ids, ids_stride, d_ids_count, rt, bitmap_words, d_local);
-    }
-    GC_CHECK_LAUNCH("gc_relabel");
-    return GC_OK;
+    return relabel(d_ids, ids_stride, d_ids_count, max_count, num_batches, d_rank_table, bitmap_words, d_local, stream,
+                   "gc_relabel");
+}
+
+int gc_relabel16(const uint32_t* d_ids, uint64_t ids_stride, const uint32_t* d_ids_count, uint32_t max_count,
+                 uint32_t num_batches, const uint32_t* d_rank_table, uint64_t bitmap_words, uint16_t* d_local,
+                 void* stream) {
+    return relabel(d_ids, ids_stride, d_ids_count, max_count, num_batches, d_rank_table, bitmap_words, d_local, stream,
+                   "gc_relabel16");
 }
 
 int gc_mark_visited(const uint32_t* d_ids, uint64_t ids_stride, const uint32_t* d_count, uint32_t max_count,

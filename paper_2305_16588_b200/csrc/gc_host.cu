@@ -173,45 +173,55 @@ __global__ void k_copy_to_mapped(const uint32_t* __restrict__ src, uint32_t* dst
 }
 
 // Segment pack of a padded window array (grid.y = batch): batch b's first
-// (ptr[b+1] - ptr[b]) rows, each `words` u32, move to the packed array at row ptr[b];
-// NARROW stores each u32 as its low 16 bits.
-template <bool NARROW>
-__global__ void k_pack_segments(const uint32_t* __restrict__ src, uint64_t stride_words, uint64_t words,
-                                const int64_t* __restrict__ ptr, void* __restrict__ dst) {
+// (ptr[b+1] - ptr[b]) rows, each `elems` IN values, move to the packed array at row
+// ptr[b] as OUT values (u32 -> u16 keeps the low 16 bits).
+template <typename IN, typename OUT>
+__global__ void k_pack_segments(const IN* __restrict__ src, uint64_t stride_elems, uint64_t elems,
+                                const int64_t* __restrict__ ptr, OUT* __restrict__ dst) {
     const uint32_t b = blockIdx.y;
     const int64_t r0 = ptr[b];
-    const uint64_t n = (uint64_t)(ptr[b + 1] - r0) * words;
-    const uint32_t* s = src + b * stride_words;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t x = s[i];
-        if (NARROW)
-            static_cast<uint16_t*>(dst)[(uint64_t)r0 * words + i] = (uint16_t)x;
-        else
-            static_cast<uint32_t*>(dst)[(uint64_t)r0 * words + i] = x;
-    }
+    const uint64_t n = (uint64_t)(ptr[b + 1] - r0) * elems;
+    const IN* s = src + b * stride_elems;
+    OUT* d = dst + (uint64_t)r0 * elems;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        d[i] = (OUT)s[i];
 }
 }  // namespace gc
 
 extern "C" {
 
 int gc_pack_segments(const void* d_src, uint64_t src_stride_bytes, uint64_t row_bytes, const int64_t* d_ptr,
-                     uint32_t num_batches, uint64_t max_rows, int narrow16, void* d_dst, void* stream) {
-    GC_REQUIRE(row_bytes % 4 == 0 && src_stride_bytes % 4 == 0, GC_ERR_VALUE,
-               "gc_pack_segments: row and stride bytes must be multiples of 4");
+                     uint32_t num_batches, uint64_t max_rows, int mode, void* d_dst, void* stream) {
+    GC_REQUIRE(mode >= 0 && mode <= 3, GC_ERR_VALUE, "gc_pack_segments: mode is 0..3");
+    const uint64_t in_bytes = mode >= 2 ? 2 : 4;
+    GC_REQUIRE(row_bytes % in_bytes == 0 && src_stride_bytes % in_bytes == 0, GC_ERR_VALUE,
+               "gc_pack_segments: row and stride bytes must be multiples of the element size");
     GC_REQUIRE(num_batches <= 65535, GC_ERR_VALUE, "gc_pack_segments: at most 65535 batches");
     if (num_batches == 0 || row_bytes == 0 || max_rows == 0) return GC_OK;
     GC_REQUIRE(d_src && d_ptr && d_dst, GC_ERR_VALUE, "gc_pack_segments: null pointer");
-    const uint64_t words = row_bytes / 4;
-    uint64_t gx = (max_rows * words + 255) / 256;
+    const uint64_t elems = row_bytes / in_bytes, stride = src_stride_bytes / in_bytes;
+    uint64_t gx = (max_rows * elems + 255) / 256;
     const uint64_t cap = (uint64_t)sm_count() * 8 / num_batches + 1;  // ~8 CTAs per SM over the window
     if (gx > cap) gx = cap;
     const dim3 grid((unsigned)gx, num_batches);
-    if (narrow16)
-        gc::k_pack_segments<true><<<grid, 256, 0, as_stream(stream)>>>(static_cast<const uint32_t*>(d_src),
-                                                                     src_stride_bytes / 4, words, d_ptr, d_dst);
-    else
-        gc::k_pack_segments<false><<<grid, 256, 0, as_stream(stream)>>>(static_cast<const uint32_t*>(d_src),
-                                                                      src_stride_bytes / 4, words, d_ptr, d_dst);
+    cudaStream_t s = as_stream(stream);
+    switch (mode) {
+        case 0:
+            gc::k_pack_segments<uint32_t, uint32_t><<<grid, 256, 0, s>>>(static_cast<const uint32_t*>(d_src), stride,
+                                                                         elems, d_ptr, static_cast<uint32_t*>(d_dst));
+            break;
+        case 1:
+            gc::k_pack_segments<uint32_t, uint16_t><<<grid, 256, 0, s>>>(static_cast<const uint32_t*>(d_src), stride,
+                                                                         elems, d_ptr, static_cast<uint16_t*>(d_dst));
+            break;
+        case 2:
+            gc::k_pack_segments<uint16_t, uint16_t><<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(d_src), stride,
+                                                                         elems, d_ptr, static_cast<uint16_t*>(d_dst));
+            break;
+        default:
+            gc::k_pack_segments<uint16_t, uint32_t><<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(d_src), stride,
+                                                                         elems, d_ptr, static_cast<uint32_t*>(d_dst));
+    }
     GC_CHECK_LAUNCH("gc_pack_segments");
     return GC_OK;
 }

@@ -91,7 +91,10 @@ __global__ void k_tree_stage(gc_tree_src_t s, const int32_t* __restrict__ d_batc
         const int64_t i = p - base;
         const int64_t cnt = s.counts[(int64_t)k * s.counts_stride + b];
         const bool real = i < cnt;
-        loc[p] = real ? s.local[k][(int64_t)b * s.local_stride[k] + i] : 0;
+        const int64_t li = (int64_t)b * s.local_stride[k] + i;
+        loc[p] = !real ? 0
+                 : s.local_bits == 16 ? (int32_t)reinterpret_cast<const uint16_t*>(s.local[k])[li]
+                                      : s.local[k][li];
         if (k == 0 && labels) labels[i] = real ? s.labels[(uint32_t)s.seeds[(int64_t)b * s.seeds_stride + i]] : -100;
         if (k < L) {
             const int64_t nbase = base + s.caps[k];

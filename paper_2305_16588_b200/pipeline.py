@@ -342,9 +342,12 @@ class SampleGatherPipeline:
 
         def pack(name, buf, sizes, narrow=False):
             # one gc_pack_segments launch: batch b's first sizes[b] rows of the padded
-            # [nb, cap, ...] buffer land at row ptr[b] of a packed device array
+            # [nb, cap, ...] buffer land at row ptr[b] of a packed device array; ids
+            # stored as u16 (int16) travel as such when narrow, else widen to int32
             total = int(sizes.sum())
-            dtype = torch.int16 if narrow else buf.dtype
+            u16_in = buf.dtype == torch.int16
+            dtype = torch.int16 if narrow else (torch.int32 if u16_in else buf.dtype)
+            mode = (2 if narrow else 3) if u16_in else (1 if narrow else 0)
             tail = tuple(buf.shape[2:])
             packed = dev_buffer(f"_dev_{name}", (total,) + tail, dtype)[:total]
             if total:
@@ -357,7 +360,7 @@ class SampleGatherPipeline:
                 dp[: p.size].copy_(hp[: p.size], non_blocking=True)
                 row_bytes = buf.element_size() * int(np.prod(tail, dtype=np.int64))
                 _lib.check(lib.gc_pack_segments(buf.data_ptr(), buf.stride(0) * buf.element_size(), row_bytes,
-                                                dp.data_ptr(), nb, int(sizes.max()), int(narrow), packed.data_ptr(),
+                                                dp.data_ptr(), nb, int(sizes.max()), mode, packed.data_ptr(),
                                                 _lib.stream_handle(main)), "pack_segments")
             host = st.get(name)
             if host is None or host.shape[0] < total or host.shape[1:] != packed.shape[1:] or host.dtype != packed.dtype:

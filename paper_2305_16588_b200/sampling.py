@@ -204,8 +204,13 @@ class WindowSampler:
         self.ucount = torch.zeros(W, dtype=i32, device=dev)
         # relabel rank table: {exclusive popcount prefix, bitmap word} per word
         self.rank = torch.empty((W, 2 * self.words), dtype=i32, device=dev) if relabel else None
-        self.local_seeds = torch.empty((W, self.B), dtype=i32, device=dev) if relabel else None
-        self.local_nbrs = [torch.empty_like(t) for t in self.nbrs] if relabel else None
+        # local ids as u16 (held in int16 tensors) when no batch can have more than 65536
+        # distinct vertices: a quarter less traffic for the relabel pass and half the bytes
+        # its consumers read; decode with local_ids()
+        self.local_bits = 16 if relabel and self.ucap <= 1 << 16 else 32
+        ldt = torch.int16 if self.local_bits == 16 else i32
+        self.local_seeds = torch.empty((W, self.B), dtype=ldt, device=dev) if relabel else None
+        self.local_nbrs = [torch.empty(t.shape, dtype=ldt, device=dev) for t in self.nbrs] if relabel else None
         hop_tmp = max([self.lib.gc_hop_expand_temp_bytes(W, caps[h]) for h in range(self.H)] + [256])
         self.hop_tmp = torch.empty(hop_tmp, dtype=torch.uint8, device=dev)
         uq_tmp = self.lib.gc_unique_temp_bytes(W, self.visited)
@@ -282,12 +287,10 @@ class WindowSampler:
             arrays = [(self.seeds, self.counts[0], self.local_seeds, self.B)] + [
                 (self.nbrs[h], self.counts[h + 1], self.local_nbrs[h], self.caps[h + 1]) for h in range(self.H)
             ]
+            fn = self.lib.gc_relabel16 if self.local_bits == 16 else self.lib.gc_relabel
             for ids, cnt, loc, cap in arrays:
-                _lib.check(
-                    self.lib.gc_relabel(ids.data_ptr(), ids.shape[1], cnt.data_ptr(), cap, self.active,
-                                        self.rank.data_ptr(), self.words, loc.data_ptr(), s),
-                    "relabel",
-                )
+                _lib.check(fn(ids.data_ptr(), ids.shape[1], cnt.data_ptr(), cap, self.active, self.rank.data_ptr(),
+                              self.words, loc.data_ptr(), s), "relabel")
 
     def check_capacity(self, reset: bool = False) -> int:
         """Largest distinct count of any batch since the last reset (one sync); raises
@@ -473,6 +476,13 @@ class GpuTrace:
 
 
 MAX_WINDOW = 65535  # batches per window: the hop/pack kernels put the batch in grid.y
+
+
+def local_ids(t: torch.Tensor) -> torch.Tensor:
+    """WindowSampler local ids as int64, whatever their storage (u16 held in int16, or int32)."""
+    if t.dtype == torch.int16:
+        return t.to(torch.int32).bitwise_and_(0xFFFF).long()
+    return t.long()
 
 
 def _window_for(sampler_caps: list[int], words: int, num_batches: int, budget_bytes: int = 2 << 30) -> int:

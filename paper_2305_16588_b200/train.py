@@ -25,6 +25,8 @@ import torch
 import torch.nn as nn
 import torch.nn.functional as F
 
+from .sampling import local_ids
+
 
 @dataclass
 class TreeBatch:
@@ -144,10 +146,10 @@ def tree_batch_from_window(pipe, b: int, labels: torch.Tensor, counts=None, ucou
     counts = sp.counts[:, b].tolist() if counts is None else [int(c) for c in counts[:, b]]
     u = int(sp.ucount[b].item()) if ucount is None else int(ucount[b])
     feats = pipe.features[b, :u]
-    local = [sp.local_seeds[b, : counts[0]].long()]
+    local = [local_ids(sp.local_seeds[b, : counts[0]])]
     offsets = []
     for h in range(sp.H):
-        local.append(sp.local_nbrs[h][b, : counts[h + 1]].long())
+        local.append(local_ids(sp.local_nbrs[h][b, : counts[h + 1]]))
         offsets.append(sp.offsets[h][b, : counts[h] + 1].long())
     seeds = sp.seeds[b, : counts[0]].long() & 0xFFFFFFFF
     return TreeBatch(feats, local, offsets, labels[seeds])
@@ -286,6 +288,7 @@ class TreeTrainer:
         src.seeds_stride = sampler.seeds.stride(0)
         self.labels = labels.to(device=dev, dtype=torch.int64).contiguous()
         src.labels = self.labels.data_ptr()
+        src.local_bits = sampler.local_bits
         self.src = src
         # per layer: input width d, aggregate width cols (2d SAGE / d GCN), + ones column
         # (the bias), padded to 8 so every row is 16-byte aligned in bf16

@@ -19,6 +19,13 @@ import pytest
 import gnncache_oracle as O
 
 pytestmark = pytest.mark.gpu
+
+
+def local_ids(t):
+    """Relabelled ids as int64 (the sampler stores u16 in int16 when a window's batches fit)."""
+    from paper_2305_16588_b200.sampling import local_ids as decode
+
+    return decode(t)
 torch = pytest.importorskip("torch")
 
 ROOT = Path(__file__).resolve().parents[1]
@@ -73,11 +80,11 @@ def test_bench_c2_pipeline_matches_oracle():
             u = int(sp.ucount[b])
             assert u == len(uniq) <= pipe.feat_cap
             assert np.array_equal(sp.unique[b, :u].cpu().numpy().view(np.uint32), uniq)
-            assert np.array_equal(sp.local_seeds[b, : len(seeds)].cpu().numpy(), O.relabel(uniq, seeds))
+            assert np.array_equal(local_ids(sp.local_seeds[b, : len(seeds)]).cpu().numpy(), O.relabel(uniq, seeds))
             for h, (_, off, nbr) in enumerate(hops):
                 t = int(counts[h + 1, b])
                 assert t == len(nbr), (epoch, b, h)
                 assert np.array_equal(sp.offsets[h][b, : len(off)].cpu().numpy(), off), (epoch, b, h)
                 assert np.array_equal(sp.nbrs[h][b, :t].cpu().numpy().view(np.uint32), nbr), (epoch, b, h)
-                assert np.array_equal(sp.local_nbrs[h][b, :t].cpu().numpy(), O.relabel(uniq, nbr)), (epoch, b, h)
+                assert np.array_equal(local_ids(sp.local_nbrs[h][b, :t]).cpu().numpy(), O.relabel(uniq, nbr)), (epoch, b, h)
             assert np.array_equal(pipe.features[b, :u].cpu().numpy(), O.synthetic_features(uniq, dim)), (epoch, b)

@@ -21,6 +21,13 @@ import pytest
 import gnncache_oracle as O
 
 pytestmark = pytest.mark.gpu
+
+
+def local_ids(t):
+    """Relabelled ids as int64 (the sampler stores u16 in int16 when a window's batches fit)."""
+    from paper_2305_16588_b200.sampling import local_ids as decode
+
+    return decode(t)
 torch = pytest.importorskip("torch")
 
 ROOT = Path(__file__).resolve().parents[1]
@@ -90,7 +97,7 @@ def _rank_main(rank, world, port, shm_name, q):
                     t = int(counts[h + 1, bi])
                     ok &= np.array_equal(sp.nbrs[h][bi, :t].cpu().numpy().view(np.uint32), nbr)
                     ok &= np.array_equal(sp.offsets[h][bi, : len(off)].cpu().numpy(), off)
-                    ok &= np.array_equal(sp.local_nbrs[h][bi, :t].cpu().numpy(), O.relabel(uniq, nbr))
+                    ok &= np.array_equal(local_ids(sp.local_nbrs[h][bi, :t]).cpu().numpy(), O.relabel(uniq, nbr))
                 ok &= np.array_equal(p.features[bi, :u].cpu().numpy(), O.synthetic_features(uniq, DIM))
                 if not ok:
                     bad.append(b)

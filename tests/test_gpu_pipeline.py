@@ -8,6 +8,13 @@ import pytest
 import gnncache_oracle as O
 
 pytestmark = pytest.mark.gpu
+
+
+def local_ids(t):
+    """Relabelled ids as int64 (the sampler stores u16 in int16 when a window's batches fit)."""
+    from paper_2305_16588_b200.sampling import local_ids as decode
+
+    return decode(t)
 torch = pytest.importorskip("torch")
 
 
@@ -52,13 +59,13 @@ def test_epoch_windows_match_oracle(window, batch, fanouts, deg, sparse):
             uniq = O.distinct_vertices(seeds, hops)
             u = int(sp.ucount[bi])
             assert np.array_equal(sp.unique[bi, :u].cpu().numpy().view(np.uint32), uniq)
-            assert np.array_equal(sp.local_seeds[bi, : len(seeds)].cpu().numpy(), O.relabel(uniq, seeds))
+            assert np.array_equal(local_ids(sp.local_seeds[bi, : len(seeds)]).cpu().numpy(), O.relabel(uniq, seeds))
             for h, (_, off, nbr) in enumerate(hops):
                 t = int(counts[h + 1, bi])
                 assert t == len(nbr)
                 assert np.array_equal(sp.nbrs[h][bi, :t].cpu().numpy().view(np.uint32), nbr)
                 assert np.array_equal(sp.offsets[h][bi, : len(off)].cpu().numpy(), off)
-                assert np.array_equal(sp.local_nbrs[h][bi, :t].cpu().numpy(), O.relabel(uniq, nbr))
+                assert np.array_equal(local_ids(sp.local_nbrs[h][bi, :t]).cpu().numpy(), O.relabel(uniq, nbr))
             assert np.array_equal(p.features[bi, :u].cpu().numpy(), table[uniq])
             seen.append(b)
 
@@ -376,12 +383,11 @@ def test_window_to_host_packs_every_batch(relabel, lanes, compact):
                 l0, l1 = out["local_ptr"][h][b : b + 2]
                 assert o1 - o0 == f + 1 and l1 - l0 == t
                 assert torch.equal(out["offsets"][h][o0:o1], sp.offsets[h][b, : f + 1].cpu())
-                ids = sp.local_nbrs[h] if relabel else sp.nbrs[h]
+                want = local_ids(sp.local_nbrs[h][b, :t]) if relabel else sp.nbrs[h][b, :t].long()
                 got = out["local"][h][l0:l1]
                 if out["local_bits"] == 16:
                     assert got.dtype == torch.int16
-                    got = got.to(torch.int32) & 0xFFFF
-                assert torch.equal(got, ids[b, :t].cpu())
+                assert torch.equal(local_ids(got), want.cpu())
         seen.append(nbw)
 
     pipe.run_epoch(pipe.plan_epoch(pool, P.KeyedRng(3).derive(0, 0, 0)), on_window=check)
