@@ -517,13 +517,13 @@ def run_b200(args):
         "clocks": clocks.summary(),
     }
 
-    if args.train_epochs > 0:
-        line["graphsage_epoch"] = train_run(args, g, cfg, pipe, pool, root, clique, local_idx, world)
     if not args.no_e2e:
         line["e2e"] = e2e_run(args, g, cfg, store, pool, root, clique, local_idx, world)
         # the training-feed view: same API and H2D, results left in HBM for the trainer
         line["e2e_device_consumer"] = e2e_run(args, g, cfg, store, pool, root, clique, local_idx, world,
                                               results_to_host=False)
+    if args.train_epochs > 0:
+        line["graphsage_epoch"] = train_run(args, g, cfg, pipe, pool, root, clique, local_idx, world)
     if world > 1:
         line["config"]["dist_backend"] = dist.get_backend()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
