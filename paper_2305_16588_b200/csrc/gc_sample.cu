@@ -28,11 +28,10 @@ namespace gc {
 #ifndef GC_HOP_THREADS
 #define GC_HOP_THREADS 256  // 128 measured 2% slower at C2 hop 3
 #endif
-constexpr int kHopThreads = GC_HOP_THREADS;  // CTA = one tile of kTilePos frontier positions
+constexpr int kHopThreads = GC_HOP_THREADS;  // CTA threads; a tile is kTilePos x PPT frontier positions
 constexpr int kTilePos = kHopThreads;
 // staged output items per round: 24 KB of u32 edge indices (plain CSR) or 40 KB of
 // u64 (tiered), so a 512-position tile of fanout 10 stages in one round
-constexpr int kItemCap = 16 * kHopThreads;
 __host__ __device__ constexpr int item_cap(bool tiered) { return tiered ? 20 * kHopThreads : 24 * kHopThreads; }
 // emission items in flight per thread: a full tile of 256 positions with take =
 // fanout stages exactly `fanout` items per thread, so for the small networks S - 1
