@@ -45,7 +45,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--window", type=int, default=256)
     ap.add_argument("--lanes", type=int, default=2, help="concurrent window lanes (inter-batch pipeline)")
-    ap.add_argument("--presample-epochs", type=int, default=4,
+    ap.add_argument("--presample-epochs", type=int, default=32,
                     help="presampling epochs behind the plan (more: less optimistic estimate, better cache)")
     ap.add_argument("--graph", type=int, default=1, help="1: each timed epoch is one CUDA-graph launch")
     ap.add_argument("--sweep-lanes", default="", help="extra schedules to time after the main run, e.g. 1,3,2d,2w64 (d: host rows deferred, wN: window)")
