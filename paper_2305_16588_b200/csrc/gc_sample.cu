@@ -310,29 +310,26 @@ __host__ __device__ constexpr int peeled_candidates() {
     return S == 4 ? 2 : S == 6 ? 5 : S == 8 ? 7 : S == 11 ? 9 : S == 16 ? 12 : S == 21 ? 17 : S == 26 ? 22 : 27;
 }
 
-// CHECKED = false: the tile stages in one round (r0 = 0, every item in range), so the
-// per-item window test is dropped
-template <int S, bool CHECKED, typename Item>
-__device__ __forceinline__ bool select_thread(uint64_t hc, uint32_t deg, uint32_t fanout, uint64_t o0, uint32_t excl,
-                                              uint32_t r0, uint32_t r1, Item* s_items, uint32_t k32) {
-    constexpr int IB = 7;
-    constexpr uint32_t kKeep = ~((1u << IB) - 1u);
-    constexpr int TRI = peeled_candidates<S>() & ~1;  // peeled in pairs
-    uint32_t t[S];
-#pragma unroll
-    for (int s = 0; s < S; ++s) t[s] = 0xFFFFFFFFu;
-    const PairHashHigh hh(hc);  // deg <= 64: key bits 63..38 from the specialised hash
-#pragma unroll
-    for (int j = 0; j < TRI; j += 2) {
-        const uint32_t c = kGoldenLow + j;
-        insert_pair<S>(t, (hh.hi_counter(c, k32) & kKeep) | c, (hh.hi_counter(c + 1, k32) & kKeep) | (c + 1));
-    }
-    const uint32_t cend = kGoldenLow + deg;
-    uint32_t c = kGoldenLow + TRI;
+// Packed key of hash counter c: (key[63:39] << 7) | c
+__device__ __forceinline__ uint32_t packed_key(const PairHashHigh& hh, uint32_t c, uint32_t k32) {
+    return (hh.hi_counter(c, k32) & ~127u) | c;
+}
+
+// The remaining candidates [c, cend) of one position, in pairs
+template <int S>
+__device__ __forceinline__ void fill_tail(uint32_t (&t)[S], const PairHashHigh& hh, uint32_t c, uint32_t cend,
+                                          uint32_t k32) {
 #pragma unroll 2
-    for (; c + 1 < cend; c += 2)
-        insert_pair<S>(t, (hh.hi_counter(c, k32) & kKeep) | c, (hh.hi_counter(c + 1, k32) & kKeep) | (c + 1));
-    if (c < cend) insert_slot<S>(t, (hh.hi_counter(c, k32) & kKeep) | c);
+    for (; c + 1 < cend; c += 2) insert_pair<S>(t, packed_key(hh, c, k32), packed_key(hh, c + 1, k32));
+    if (c < cend) insert_slot<S>(t, packed_key(hh, c, k32));
+}
+
+// Ties and staging of a filled network. CHECKED = false: the tile stages in one round
+// (r0 = 0, every item in range), so the per-item window test is dropped.
+template <int S, bool CHECKED, typename Item>
+__device__ __forceinline__ bool stage_network(const uint32_t (&t)[S], uint32_t fanout, uint64_t o0, uint32_t excl,
+                                              uint32_t r0, uint32_t r1, Item* s_items) {
+    constexpr int IB = 7;
     const uint64_t base = o0 - kGoldenLow;
     if (!CHECKED && fanout == S - 1) {
         // the widest fanout of the network (C2 hop 3: 5 of S = 6): every slot is
@@ -360,6 +357,61 @@ __device__ __forceinline__ bool select_thread(uint64_t hc, uint32_t deg, uint32_
                 s_items[excl + s] = (Item)e;
         }
     return true;
+}
+
+// Thread-per-position choice path for deg <= 64 and fanout < S: the thread streams
+// its deg keys through a branchless S-slot min/max insertion network on packed
+// 32-bit values (25-bit key prefix << 7 | c, c = (G & 0xFF) + j the hash counter),
+// which keeps the S smallest in order. Two equal prefixes among ranks 0..fanout mean
+// the packed order may differ from the exact (key, j) order: return false and let a
+// warp redo the position exactly. deg > fanout >= TRI - 1, so the first TRI
+// candidates are inserted with the network peeled: slots still holding +inf fold away.
+template <int S, bool CHECKED, typename Item>
+__device__ __forceinline__ bool select_thread(uint64_t hc, uint32_t deg, uint32_t fanout, uint64_t o0, uint32_t excl,
+                                              uint32_t r0, uint32_t r1, Item* s_items, uint32_t k32) {
+    constexpr int TRI = peeled_candidates<S>() & ~1;  // peeled in pairs
+    uint32_t t[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) t[s] = 0xFFFFFFFFu;
+    const PairHashHigh hh(hc);  // deg <= 64: key bits 63..38 from the specialised hash
+#pragma unroll
+    for (int j = 0; j < TRI; j += 2) {
+        const uint32_t c = kGoldenLow + j;
+        insert_pair<S>(t, packed_key(hh, c, k32), packed_key(hh, c + 1, k32));
+    }
+    fill_tail<S>(t, hh, kGoldenLow + TRI, kGoldenLow + deg, k32);
+    return stage_network<S, CHECKED>(t, fanout, o0, excl, r0, r1, s_items);
+}
+
+// Two positions of one thread through their networks together (PPT = 2, both on the
+// thread path, one staging round): the candidates both have go through one loop whose
+// body holds two independent insertion chains, so the scheduler has twice the
+// independent work per warp; the longer list finishes alone.
+template <int S, typename Item>
+__device__ __forceinline__ void select_thread_two(const uint64_t (&hc)[2], const uint32_t (&deg)[2],
+                                                  const uint64_t (&o0)[2], const uint32_t (&excl)[2], uint32_t fanout,
+                                                  Item* s_items, uint32_t k32, bool (&need_warp)[2]) {
+    constexpr int TRI = peeled_candidates<S>() & ~1;
+    uint32_t ta[S], tb[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) ta[s] = tb[s] = 0xFFFFFFFFu;
+    const PairHashHigh ha(hc[0]), hb(hc[1]);
+#pragma unroll
+    for (int j = 0; j < TRI; j += 2) {
+        const uint32_t c = kGoldenLow + j;
+        insert_pair<S>(ta, packed_key(ha, c, k32), packed_key(ha, c + 1, k32));
+        insert_pair<S>(tb, packed_key(hb, c, k32), packed_key(hb, c + 1, k32));
+    }
+    const uint32_t cboth = kGoldenLow + min(deg[0], deg[1]);
+    uint32_t c = kGoldenLow + TRI;
+    for (; c + 1 < cboth; c += 2) {
+        insert_pair<S>(ta, packed_key(ha, c, k32), packed_key(ha, c + 1, k32));
+        insert_pair<S>(tb, packed_key(hb, c, k32), packed_key(hb, c + 1, k32));
+    }
+    fill_tail<S>(ta, ha, c, kGoldenLow + deg[0], k32);
+    fill_tail<S>(tb, hb, c, kGoldenLow + deg[1], k32);
+    need_warp[0] = !stage_network<S, false>(ta, fanout, o0[0], excl[0], 0u, 0u, s_items);
+    need_warp[1] = !stage_network<S, false>(tb, fanout, o0[1], excl[1], 0u, 0u, s_items);
 }
 
 // Warp-cooperative selection of one position (long lists, wide fanouts, tie redo).
@@ -591,8 +643,26 @@ __global__ void __launch_bounds__(kHopThreads, hop_min_blocks<S>()) k_hop_expand
         const uint32_t r1 = min(total, r0 + kCap);
         // ---- phase 2a: stage the source edge index of every output item in [r0, r1)
         bool need_warp[PPT];
+        bool done_two = false;
+#ifndef GC_NO_DUAL
+        if constexpr (PPT == 2 && S > 0) {
+            const auto choice = [&](int q) {
+                return valid[q] && !p.exact_only && deg[q] > p.fanout && deg[q] <= 64 && p.fanout < (uint32_t)S;
+            };
+            if (rounds <= 1 && choice(0) && choice(1)) {
+                bool nw[2];
+                select_thread_two<S>(reinterpret_cast<const uint64_t(&)[2]>(hc), reinterpret_cast<const uint32_t(&)[2]>(deg),
+                                     reinterpret_cast<const uint64_t(&)[2]>(o0), reinterpret_cast<const uint32_t(&)[2]>(excl),
+                                     p.fanout, s_items, p.k32, nw);
+                need_warp[0] = nw[0];
+                need_warp[1] = nw[1];
+                done_two = true;
+            }
+        }
+#endif
 #pragma unroll
         for (int q = 0; q < PPT; ++q) {
+            if (done_two) break;
             need_warp[q] = false;
             const bool thread_copy = deg[q] <= p.fanout && deg[q] <= 64;
             const bool thread_choice =
