@@ -345,24 +345,31 @@ def test_epoch_graph_replay_tiered_matches_eager(lanes):
                 assert torch.equal(xa[bi, :u].cpu(), host_table[sa.unique[bi, :u].cpu().long() & 0xFFFFFFFF])
 
 
-@pytest.mark.parametrize("relabel,lanes,compact", [(True, 1, False), (False, 1, False), (True, 2, False),
-                                                    (True, 1, True), (False, 1, True)])
-def test_window_to_host_packs_every_batch(relabel, lanes, compact):
+@pytest.mark.parametrize("relabel,lanes,compact,big", [(True, 1, False, False), (False, 1, False, False),
+                                                        (True, 2, False, False), (True, 1, True, False),
+                                                        (False, 1, True, False), (True, 1, True, True),
+                                                        (True, 1, False, True)])
+def test_window_to_host_packs_every_batch(relabel, lanes, compact, big):
     """window_to_host: one packed pinned copy per array equals the per-batch slices of
     the padded device buffers, batch boundaries included; staging is reused. compact:
     relabelled ids travel as 16-bit values (global ids never do); wait=False returns an
-    event the host waits on before reading."""
+    event the host waits on before reading. big: the unique capacity exceeds 65536, so
+    the sampler keeps u32 local ids (narrowed by the packing when compact), else u16
+    (widened by the packing when not compact) — every gc_pack_segments mode."""
     import paper_2305_16588_b200 as P
     from paper_2305_16588_b200.cache import FeatureStore
     from paper_2305_16588_b200.graph import synthetic_features_device
     from paper_2305_16588_b200.pipeline import SampleGatherPipeline
 
-    n, dim, batch, fanouts = 30_000, 100, 96, (7, 3)
+    n, dim, batch, fanouts = (100_000, 32, 1024, (15, 10)) if big else (30_000, 100, 96, (7, 3))
     g = P.generate_synthetic(n, 12, 1.2, seed=12)
-    pool = np.sort(np.random.default_rng(13).choice(n, 1000, replace=False)).astype(np.int64)  # last batch partial
+    npool = 3000 if big else 1000
+    pool = np.sort(np.random.default_rng(13).choice(n, npool, replace=False)).astype(np.int64)  # last batch partial
     store = FeatureStore.resident(synthetic_features_device(0, n, dim))
-    pipe = SampleGatherPipeline(g, P.SamplingConfig(fanouts=fanouts, batch_size=batch), store, len(pool), window=4,
-                                relabel=relabel, lanes=lanes)
+    pipe = SampleGatherPipeline(g, P.SamplingConfig(fanouts=fanouts, batch_size=batch), store, len(pool),
+                                window=2 if big else 4, relabel=relabel, lanes=lanes)
+    if relabel:
+        assert pipe.sampler.local_bits == (32 if big else 16)
     staging, seen = {}, []
 
     def check(p, w0, nbw):
@@ -391,5 +398,5 @@ def test_window_to_host_packs_every_batch(relabel, lanes, compact):
         seen.append(nbw)
 
     pipe.run_epoch(pipe.plan_epoch(pool, P.KeyedRng(3).derive(0, 0, 0)), on_window=check)
-    assert sum(seen) == -(-len(pool) // batch) and len(seen) == 3
+    assert sum(seen) == -(-len(pool) // batch) and len(seen) == (2 if big else 3)
     assert staging["features"].is_pinned()
