@@ -300,6 +300,19 @@ int gc_tree_aggregate_backward(const void* d_dA, int dtype, int64_t dA_stride, i
                                const void* d_h, int64_t h_stride, void* d_g, int64_t g_stride, int nlevels,
                                const int64_t* level_caps, const int32_t* d_level_counts, void* stream);
 
+/* Classifier head of the tree trainer: for seed rows [0, rows) of the top layer's
+ * pre-activations z (dtype 0 fp32 / 1 bf16), top = relu(z), logits = top W^T + b
+ * (W fp32 [classes, hid], cast to the activation type as operands, fp32 sums),
+ * cross entropy over labels (< 0: padding) averaged over *d_nvalid rows -> *d_loss;
+ * d_dW [classes, hid] and d_db [classes] receive the gradients and d_g [rows, hid]
+ * (dtype) the gradient with respect to z (ReLU mask applied). Deterministic
+ * (fixed-order sums); d_work holds gc_tree_head_work_floats(rows, classes, hid) floats. */
+size_t gc_tree_head_work_floats(int64_t rows, int classes, int hid);
+int gc_tree_head(const void* d_z, int dtype, int64_t z_stride, int hid, int64_t rows, const float* d_W,
+                 const float* d_b, int classes, const int64_t* d_labels, const int32_t* d_nvalid, float* d_loss,
+                 float* d_dW, float* d_db, void* d_g, int64_t g_stride, float* d_work, size_t work_floats,
+                 void* stream);
+
 /* ------------------------------------------- K6/K7: cost model (planner.py:42-261) */
 
 /* Column sums and first argmax over K rows (planner.py:50-55): rows are int64 [K][n]. */

@@ -165,6 +165,9 @@ SIGNATURES = {
                            [ctypes.POINTER(GcFeatureStore), V, U64, V, U32, U32, V, U64, V, V, U64, V, V]),
     "gc_host_unregister": (ctypes.c_int, [V]),
     "gc_copy_d2h_mapped": (ctypes.c_int, [V, V, U64, V]),
+    "gc_tree_head_work_floats": (SZ, [I64, ctypes.c_int, ctypes.c_int]),
+    "gc_tree_head": (ctypes.c_int, [V, ctypes.c_int, I64, ctypes.c_int, I64, V, V, ctypes.c_int, V, V, V, V, V, V,
+                                    I64, V, SZ, V]),
     "gc_pack_segments": (ctypes.c_int, [V, U64, U64, V, U32, U64, ctypes.c_int, V, V]),
     "gc_host_alloc_numa": (ctypes.c_int, [SZ, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(SZ)]),
     "gc_host_free_numa": (ctypes.c_int, [V, SZ]),

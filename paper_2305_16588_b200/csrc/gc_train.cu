@@ -353,6 +353,148 @@ static inline unsigned warp_grid(int64_t rows) {
     return (unsigned)(g < 1 ? 1 : g);
 }
 
+
+// ---- classifier head: logits, cross entropy and its backward in three launches
+// (replaces ~20 small torch kernels per step). T is the activation type: inputs are
+// rounded to it exactly as the torch path casts them (bf16 operands, fp32 sums).
+template <typename T>
+__device__ __forceinline__ float act_round(float x) {
+    if constexpr (sizeof(T) == 2) return __bfloat162float(__float2bfloat16(x));
+    return x;
+}
+__device__ __forceinline__ float act_load(const float* p) { return *p; }
+__device__ __forceinline__ float act_load(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+template <typename T>
+__device__ __forceinline__ T act_cast(float x);
+template <>
+__device__ __forceinline__ float act_cast<float>(float x) { return x; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 act_cast<__nv_bfloat16>(float x) { return __float2bfloat16(x); }
+
+
+// One CTA of kHeadWarps warps per seed row r: top = relu(z[r]); logits = top . W_act^T
+// + b (warps split the classes, lanes the hidden units: coalesced rows of W, fixed-order
+// warp sums); log-softmax; rowloss[r] = -logp[y] / nvalid; dlog[r] = (softmax -
+// onehot(y)) / nvalid (0 for padding, label < 0); g[r] = (dlog_act . W_act) * (z[r] > 0)
+// with threads over the hidden units. A row is little work, so several warps share it:
+// the kernel is latency-bound and needs the parallelism.
+constexpr int kHeadWarps = 8;
+
+template <typename T>
+__global__ void __launch_bounds__(32 * kHeadWarps) k_tree_head_rows(
+    const T* __restrict__ z, int64_t z_stride, int hid, int64_t rows, const float* __restrict__ W,
+    const float* __restrict__ bias, int C, const int64_t* __restrict__ labels, const int32_t* __restrict__ nvalid,
+    float* __restrict__ dlog, float* __restrict__ rowloss, T* __restrict__ g, int64_t g_stride) {
+    extern __shared__ float sh[];
+    float* top = sh;       // [hid]
+    float* dl = sh + hid;  // [C]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t r = blockIdx.x;
+    const T* zr = z + r * z_stride;
+    for (int h = threadIdx.x; h < hid; h += blockDim.x) {
+        const float v = act_load(zr + h);
+        top[h] = v > 0.f ? v : 0.f;
+    }
+    __syncthreads();
+    for (int c = warp; c < C; c += kHeadWarps) {
+        const float* w = W + (int64_t)c * hid;
+        float part = 0.f;
+        for (int h = lane; h < hid; h += 32) part = fmaf(top[h], act_round<T>(__ldg(w + h)), part);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
+        if (lane == 0) dl[c] = part + bias[c];
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const float nv = (float)max(*nvalid, 1);
+        const int64_t y = labels[r];
+        float mx = -INFINITY;
+        for (int c = lane; c < C; c += 32) mx = fmaxf(mx, dl[c]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+        float se = 0.f;
+        for (int c = lane; c < C; c += 32) se += __expf(dl[c] - mx);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(kFull, se, o);
+        const float lse = mx + __logf(se);
+        const bool valid = y >= 0;
+        if (lane == 0) rowloss[r] = 0.f;
+        __syncwarp();
+        for (int c = lane; c < C; c += 32) {
+            const float lp = dl[c] - lse;
+            if (valid && c == y) rowloss[r] = -lp / nv;
+            const float d = valid ? (__expf(lp) - (c == y ? 1.f : 0.f)) / nv : 0.f;
+            dl[c] = d;
+            dlog[r * C + c] = d;
+        }
+    }
+    __syncthreads();
+    T* gr = g + r * g_stride;
+    for (int h = threadIdx.x; h < hid; h += blockDim.x) {
+        float acc = 0.f;
+        for (int c = 0; c < C; ++c) acc = fmaf(act_round<T>(dl[c]), act_round<T>(__ldg(W + (int64_t)c * hid + h)), acc);
+        gr[h] = act_cast<T>(top[h] > 0.f ? acc : 0.f);
+    }
+}
+
+constexpr int kHeadChunkRows = 32;
+
+// dW partials: part[chunk][c][h] = sum over the chunk's rows of dlog_act[r,c] * top[r,h],
+// and part[chunk][c][hid] = the chunk's sum of dlog[r,c] (the bias gradient)
+template <typename T>
+__global__ void k_tree_head_dw(const T* __restrict__ z, int64_t z_stride, int hid, int64_t rows, int C,
+                               const float* __restrict__ dlog, float* __restrict__ part) {
+    const int c = blockIdx.x;
+    const int64_t r0 = (int64_t)blockIdx.y * kHeadChunkRows;
+    const int64_t r1 = min(rows, r0 + kHeadChunkRows);
+    float* out = part + ((int64_t)blockIdx.y * C + c) * (hid + 1);
+    for (int h = threadIdx.x; h < hid; h += blockDim.x) {
+        float acc = 0.f;
+        for (int64_t r = r0; r < r1; ++r) {
+            const float t = act_load(z + r * z_stride + h);
+            acc = fmaf(act_round<T>(dlog[r * C + c]), t > 0.f ? t : 0.f, acc);
+        }
+        out[h] = acc;
+    }
+    if (threadIdx.x < 32) {  // the chunk's bias-gradient share, lanes over rows, fixed order
+        float acc = 0.f;
+        for (int64_t r = r0 + threadIdx.x; r < r1; r += 32) acc += dlog[r * C + c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+        if (threadIdx.x == 0) out[hid] = acc;
+    }
+}
+
+// dW and db: sums of the chunk partials in chunk order; loss: one CTA reduces rowloss
+__global__ void k_tree_head_final(const float* __restrict__ part, int chunks, int C, int hid, int64_t rows,
+                                  const float* __restrict__ rowloss, float* __restrict__ dW, float* __restrict__ db,
+                                  float* __restrict__ loss) {
+    const int64_t n = (int64_t)C * (hid + 1);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        float acc = 0.f;
+        for (int k = 0; k < chunks; ++k) acc += part[k * n + i];
+        const int64_t c = i / (hid + 1), h = i - c * (hid + 1);
+        if (h < hid)
+            dW[c * hid + h] = acc;
+        else
+            db[c] = acc;
+    }
+    if (blockIdx.x == 0) {
+        __shared__ float s_w[32];
+        float acc = 0.f;
+        for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) acc += rowloss[r];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+        if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = acc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float t = 0.f;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_w[w];
+            *loss = t;
+        }
+    }
+}
+
 }  // namespace gc
 
 extern "C" {
@@ -456,6 +598,50 @@ int gc_tree_aggregate_backward(const void* d_dA, int dtype, int64_t dA_stride, i
         else k_tree_aggregate_bwd<__nv_bfloat16, 1><<<g, 256, 0, s>>>(a, tasks);
     }
     GC_CHECK_LAUNCH("gc_tree_aggregate_backward");
+    return GC_OK;
+}
+
+size_t gc_tree_head_work_floats(int64_t rows, int classes, int hid) {
+    const int64_t chunks = (rows + kHeadChunkRows - 1) / kHeadChunkRows;
+    return (size_t)(rows * classes + rows + chunks * classes * ((int64_t)hid + 1));
+}
+
+int gc_tree_head(const void* d_z, int dtype, int64_t z_stride, int hid, int64_t rows, const float* d_W,
+                 const float* d_b, int classes, const int64_t* d_labels, const int32_t* d_nvalid, float* d_loss,
+                 float* d_dW, float* d_db, void* d_g, int64_t g_stride, float* d_work, size_t work_floats,
+                 void* stream) {
+    GC_REQUIRE(dtype == 0 || dtype == 1, GC_ERR_VALUE, "gc_tree_head: dtype is 0 (fp32) or 1 (bf16)");
+    GC_REQUIRE(hid >= 1 && classes >= 1 && rows >= 1, GC_ERR_VALUE, "gc_tree_head: empty shape");
+    GC_REQUIRE(d_work && work_floats >= gc_tree_head_work_floats(rows, classes, hid), GC_ERR_VALUE,
+               "gc_tree_head: work buffer too small");
+    const size_t smem = (size_t)(hid + classes) * sizeof(float);
+    GC_REQUIRE(smem <= 48 * 1024, GC_ERR_VALUE, "gc_tree_head: hidden + classes too wide");
+    cudaStream_t s = as_stream(stream);
+    float* dlog = d_work;
+    float* rowloss = dlog + rows * classes;
+    float* part = rowloss + rows;
+    const int chunks = (int)((rows + kHeadChunkRows - 1) / kHeadChunkRows);
+    const unsigned g1 = (unsigned)rows;
+    const dim3 g2(classes, chunks);
+    const int t2 = hid < 256 ? (hid + 31) / 32 * 32 : 256;
+    if (dtype == 0) {
+        k_tree_head_rows<float><<<g1, 32 * kHeadWarps, smem, s>>>(
+            static_cast<const float*>(d_z), z_stride, hid, rows, d_W, d_b, classes, d_labels, d_nvalid, dlog, rowloss,
+            static_cast<float*>(d_g), g_stride);
+        k_tree_head_dw<float><<<g2, t2, 0, s>>>(static_cast<const float*>(d_z), z_stride, hid, rows, classes, dlog,
+                                                 part);
+    } else {
+        using bf = __nv_bfloat16;
+        k_tree_head_rows<bf><<<g1, 32 * kHeadWarps, smem, s>>>(
+            static_cast<const bf*>(d_z), z_stride, hid, rows, d_W, d_b, classes, d_labels, d_nvalid, dlog, rowloss,
+            static_cast<bf*>(d_g), g_stride);
+        k_tree_head_dw<bf><<<g2, t2, 0, s>>>(static_cast<const bf*>(d_z), z_stride, hid, rows, classes, dlog, part);
+    }
+    const int64_t n = (int64_t)classes * (hid + 1);
+    unsigned g3 = (unsigned)((n + 255) / 256);
+    if (g3 < 1) g3 = 1;
+    k_tree_head_final<<<g3, 256, 0, s>>>(part, chunks, classes, hid, rows, rowloss, d_dW, d_db, d_loss);
+    GC_CHECK_LAUNCH("gc_tree_head");
     return GC_OK;
 }
 

@@ -344,6 +344,14 @@ class TreeTrainer:
             self.A.append(A)
             self.Z.append(torch.zeros((rows, hid), dtype=self.act, device=dev))
         self.loss = torch.zeros((), dtype=torch.float32, device=dev)
+        # classifier head (gc_tree_head): gradient w.r.t. the top layer's pre-activations
+        # of the seed rows, and the kernel's work buffer
+        from . import _lib as _L
+
+        ncls, hid_top = self.Wc.shape
+        self.g_top = torch.empty((self.base[1], hid_top), dtype=self.act, device=dev)
+        self.head_work = torch.empty(int(_L.lib().gc_tree_head_work_floats(self.base[1], ncls, hid_top)),
+                                     dtype=torch.float32, device=dev)
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.backend = dist.get_backend(group) if self.world > 1 else None
@@ -378,23 +386,18 @@ class TreeTrainer:
                                                  self.cbeg.data_ptr(), self.cdeg.data_ptr(), rows, self.mode + 2,
                                                  A.data_ptr(), self.dt, A.stride(0), None, 0, s), "tree_aggregate")
             torch.mm(A, Wa[l].t(), out=self.Z[l])
+        # classifier head in one native call: relu, logits (activation-type operands, fp32
+        # sums), cross entropy averaged over the batch's real seeds (level_counts[0]; padded
+        # seeds carry label -100), dWc, dbc and the gradient g w.r.t. the seed rows of z
         B = self.base[1]
         ztop = self.Z[L - 1][:B]
-        top = torch.relu(ztop)
-        logits = _mm_f32(top, self.Wc.to(act).t()) + self.bc
-        y = self.labels_b
-        valid = (y >= 0).to(torch.float32)
-        nvalid = valid.sum().clamp_(min=1.0)
-        yc = y.clamp(min=0)
-        logp = torch.log_softmax(logits, dim=1)
-        torch.div(-(logp.gather(1, yc.view(-1, 1)).squeeze(1) * valid).sum(), nvalid, out=self.loss)
-        # backward
-        dlog = logp.exp_()
-        dlog.scatter_add_(1, yc.view(-1, 1), -torch.ones_like(valid).view(-1, 1))
-        dlog.mul_((valid / nvalid).view(-1, 1))
-        self.dWc.copy_(_mm_f32(dlog.t().to(act), top))
-        torch.sum(dlog, 0, out=self.dbc)
-        g = (dlog.to(act) @ self.Wc.to(act)) * (ztop > 0)
+        ncls, hid_top = self.Wc.shape
+        _lib.check(lib.gc_tree_head(ztop.data_ptr(), self.dt, ztop.stride(0), hid_top, B, self.Wc.data_ptr(),
+                                    self.bc.data_ptr(), ncls, self.labels_b.data_ptr(), self.level_counts.data_ptr(),
+                                    self.loss.data_ptr(), self.dWc.data_ptr(), self.dbc.data_ptr(),
+                                    self.g_top.data_ptr(), self.g_top.stride(0), self.head_work.data_ptr(),
+                                    self.head_work.numel(), s), "tree_head")
+        g = self.g_top
         for l in range(L - 1, -1, -1):
             d, cols, ext, hid = self.shape[l]
             self.dW[l].copy_(_mm_f32(g.t(), self.A[l]))  # the ones column gives the bias gradient
