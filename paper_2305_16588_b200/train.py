@@ -201,6 +201,26 @@ def train_epoch(pipe, plan, model: GraphSAGE, opt, labels: torch.Tensor, max_bat
 _MM_OUT_DTYPE = [None]  # does torch.mm(..., out_dtype=) work here (decided once, outside graph capture)
 
 
+def _mm_f32_into(out: torch.Tensor, a: torch.Tensor, b: torch.Tensor) -> None:
+    """out = a @ b in fp32, written in place when torch supports it (no extra copy)."""
+    if a.dtype == torch.float32:
+        torch.mm(a, b, out=out)
+        return
+    if _MM_OUT_INTO[0] is None:
+        try:
+            torch.mm(a[:1], b[:, :1], out_dtype=torch.float32, out=torch.empty((1, 1), device=a.device))
+            _MM_OUT_INTO[0] = True
+        except (RuntimeError, TypeError):
+            _MM_OUT_INTO[0] = False
+    if _MM_OUT_INTO[0]:
+        torch.mm(a, b, out_dtype=torch.float32, out=out)
+    else:
+        out.copy_(_mm_f32(a, b))
+
+
+_MM_OUT_INTO = [None]
+
+
 def _mm_f32(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
     """a @ b accumulated and returned in fp32 (bf16 operands stay on the tensor cores)."""
     if a.dtype == torch.float32:
@@ -307,12 +327,16 @@ class TreeTrainer:
         n = sum(sizes)
         self.flat = torch.zeros(n, dtype=torch.float32, device=dev)
         self.gflat = torch.zeros(n + 1, dtype=torch.float32, device=dev)  # + ranks contributing this step
-        self.W, self.dW = [], []
+        # the activation-type copy of the parameters the GEMMs read (bf16 runs), refreshed
+        # by one cast per step
+        self.flat_act = self.flat if self.act == torch.float32 else torch.empty(n, dtype=self.act, device=dev)
+        self.W, self.dW, self.W_act = [], [], []
         o = 0
         with torch.no_grad():
             for layer, (d, cols, ext, hid) in zip(self.layers, self.shape):
                 W = self.flat[o : o + hid * ext].view(hid, ext)
                 self.dW.append(self.gflat[o : o + hid * ext].view(hid, ext))
+                self.W_act.append(self.flat_act[o : o + hid * ext].view(hid, ext))
                 o += hid * ext
                 if isinstance(layer, SAGELayer):
                     parts = [(layer.lin_self.weight, W[:, :d]), (layer.lin_neigh.weight, W[:, d : 2 * d]),
@@ -371,7 +395,11 @@ class TreeTrainer:
                    "tree_stage")
         feats = self._features
         dim = feats.shape[-1]
-        Wa = [W.to(act) for W in self.W]
+        if act == torch.float32:
+            Wa = self.W
+        else:  # one cast of the whole parameter buffer; the layers' weights are views into it
+            self.flat_act.copy_(self.flat)
+            Wa = self.W_act
         for l in range(L):
             d, cols, ext, hid = self.shape[l]
             A, rows = self.A[l], self.base[L - l]
@@ -400,7 +428,7 @@ class TreeTrainer:
         g = self.g_top
         for l in range(L - 1, -1, -1):
             d, cols, ext, hid = self.shape[l]
-            self.dW[l].copy_(_mm_f32(g.t(), self.A[l]))  # the ones column gives the bias gradient
+            _mm_f32_into(self.dW[l], g.t(), self.A[l])  # the ones column gives the bias gradient
             if l == 0:
                 break
             dA = g @ Wa[l][:, :cols]
