@@ -859,7 +859,8 @@ def e2e_run(args, g, cfg, store, pool, root, clique, local_idx, world, results_t
         moved["windows"] += 1
         moved["u16"] += out["local_bits"] == 16
         moved["d2h"] += sum(t.numel() * t.element_size() for t in (out["unique"], out["features"],
-                                                                     *out["offsets"], *out["local"]))
+                                                                     *out.get("counts", out.get("offsets")),
+                                                                     *out["local"]))
 
     def step(e):
         dev_pool = host_pool.to("cuda", non_blocking=True)

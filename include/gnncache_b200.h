@@ -368,7 +368,9 @@ int gc_copy_d2h_mapped(const void* d_src, void* h_dst, uint64_t bytes, void* str
  * b's rows [0, d_ptr[b+1] - d_ptr[b]) of `row_bytes` bytes at d_src + b*src_stride_bytes
  * go to d_dst from row d_ptr[b] on; max_rows bounds every batch's row count (grid size).
  * mode: 0 copy (rows of u32 words), 1 u32 -> u16 (low 16 bits: relabelled ids of a window
- * whose batches have <= 65536 distinct vertices), 2 copy u16, 3 u16 -> u32. */
+ * whose batches have <= 65536 distinct vertices), 2 copy u16, 3 u16 -> u32, 4 u32 offsets
+ * -> u8 counts (row i becomes src[i+1] - src[i]; d_ptr counts the rows, i.e. a hop's
+ * frontier positions, and src holds one more offset per batch). */
 int gc_pack_segments(const void* d_src, uint64_t src_stride_bytes, uint64_t row_bytes, const int64_t* d_ptr,
                      uint32_t num_batches, uint64_t max_rows, int mode, void* d_dst, void* stream);
 

@@ -186,14 +186,28 @@ __global__ void k_pack_segments(const IN* __restrict__ src, uint64_t stride_elem
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
         d[i] = (OUT)s[i];
 }
+
+// Offsets -> per-row counts: batch b's rows [0, ptr[b+1] - ptr[b]) of u32 offsets become
+// the u8 differences s[i+1] - s[i] (a hop's per-position sample counts, <= fanout).
+__global__ void k_pack_counts(const uint32_t* __restrict__ src, uint64_t stride_elems, const int64_t* __restrict__ ptr,
+                              uint8_t* __restrict__ dst) {
+    const uint32_t b = blockIdx.y;
+    const int64_t r0 = ptr[b];
+    const uint64_t n = (uint64_t)(ptr[b + 1] - r0);
+    const uint32_t* s = src + b * stride_elems;
+    uint8_t* d = dst + r0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        d[i] = (uint8_t)(s[i + 1] - s[i]);
+}
 }  // namespace gc
 
 extern "C" {
 
 int gc_pack_segments(const void* d_src, uint64_t src_stride_bytes, uint64_t row_bytes, const int64_t* d_ptr,
                      uint32_t num_batches, uint64_t max_rows, int mode, void* d_dst, void* stream) {
-    GC_REQUIRE(mode >= 0 && mode <= 3, GC_ERR_VALUE, "gc_pack_segments: mode is 0..3");
-    const uint64_t in_bytes = mode >= 2 ? 2 : 4;
+    GC_REQUIRE(mode >= 0 && mode <= 4, GC_ERR_VALUE, "gc_pack_segments: mode is 0..4");
+    GC_REQUIRE(mode != 4 || row_bytes == 4, GC_ERR_VALUE, "gc_pack_segments: mode 4 takes rows of one u32 offset");
+    const uint64_t in_bytes = (mode == 2 || mode == 3) ? 2 : 4;
     GC_REQUIRE(row_bytes % in_bytes == 0 && src_stride_bytes % in_bytes == 0, GC_ERR_VALUE,
                "gc_pack_segments: row and stride bytes must be multiples of the element size");
     GC_REQUIRE(num_batches <= 65535, GC_ERR_VALUE, "gc_pack_segments: at most 65535 batches");
@@ -213,6 +227,10 @@ int gc_pack_segments(const void* d_src, uint64_t src_stride_bytes, uint64_t row_
         case 1:
             gc::k_pack_segments<uint32_t, uint16_t><<<grid, 256, 0, s>>>(static_cast<const uint32_t*>(d_src), stride,
                                                                          elems, d_ptr, static_cast<uint16_t*>(d_dst));
+            break;
+        case 4:
+            gc::k_pack_counts<<<grid, 256, 0, s>>>(static_cast<const uint32_t*>(d_src), stride, d_ptr,
+                                                   static_cast<uint8_t*>(d_dst));
             break;
         case 2:
             gc::k_pack_segments<uint16_t, uint16_t><<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(d_src), stride,

@@ -34,6 +34,21 @@ def _as_i64(key: int) -> int:
     return key - (1 << 64) if key >= 1 << 63 else key
 
 
+def offsets_from_counts(counts, counts_ptr) -> tuple[torch.Tensor, np.ndarray]:
+    """One hop's packed offsets from window_to_host's compact per-position counts:
+    returns (offsets int32 [sum (F + 1)], offsets_ptr int64 [nb + 1]) laid out as the
+    non-compact 'offsets'[h] / 'offsets_ptr'[h] (each batch's offsets start at 0)."""
+    c = counts.numpy() if isinstance(counts, torch.Tensor) else np.asarray(counts)
+    cp = np.asarray(counts_ptr, dtype=np.int64)
+    nb = len(cp) - 1
+    optr = cp + np.arange(nb + 1, dtype=np.int64)
+    out = np.zeros(int(optr[-1]), dtype=np.int32)
+    for b in range(nb):
+        c0, c1 = int(cp[b]), int(cp[b + 1])
+        out[optr[b] + 1 : optr[b + 1]] = np.cumsum(c[c0:c1], dtype=np.int64)
+    return torch.from_numpy(out), optr
+
+
 @dataclass
 class EpochPlan:
     pool: torch.Tensor  # int64 [L] device
@@ -292,7 +307,10 @@ class SampleGatherPipeline:
         'unique_ptr', 'offsets_ptr'[h], 'local_ptr'[h] (int64 numpy [nb + 1]).
         compact_ids: relabelled ids of a window whose batches all have <= 65536
         distinct vertices travel as 16-bit values ('local'[h] int16 holding the uint16
-        bit pattern, out['local_bits'] = 16) — a third less PCIe traffic at C2.
+        bit pattern, out['local_bits'] = 16), and, when every fanout is <= 255, each
+        hop's offsets travel as per-position u8 sample counts ('counts'[h] uint8
+        [sum F_h] with 'counts_ptr'[h]; offsets_from_counts() rebuilds 'offsets'[h]) —
+        less than half the PCIe bytes of u32 ids and offsets at C2.
         The packing is sync-free (segment rows from the host-side sizes) and each
         array's D2H copy runs on a copy stream while the next array is packed; the
         kernels enqueued after this call may overwrite the window's buffers at once
@@ -340,14 +358,18 @@ class SampleGatherPipeline:
                 st[key] = t
             return t
 
-        def pack(name, buf, sizes, narrow=False):
+        def pack(name, buf, sizes, narrow=False, counts=False):
             # one gc_pack_segments launch: batch b's first sizes[b] rows of the padded
             # [nb, cap, ...] buffer land at row ptr[b] of a packed device array; ids
-            # stored as u16 (int16) travel as such when narrow, else widen to int32
+            # stored as u16 (int16) travel as such when narrow, else widen to int32;
+            # counts: offsets become the u8 differences of consecutive entries
             total = int(sizes.sum())
             u16_in = buf.dtype == torch.int16
-            dtype = torch.int16 if narrow else (torch.int32 if u16_in else buf.dtype)
-            mode = (2 if narrow else 3) if u16_in else (1 if narrow else 0)
+            if counts:
+                dtype, mode = torch.uint8, 4
+            else:
+                dtype = torch.int16 if narrow else (torch.int32 if u16_in else buf.dtype)
+                mode = (2 if narrow else 3) if u16_in else (1 if narrow else 0)
             tail = tuple(buf.shape[2:])
             packed = dev_buffer(f"_dev_{name}", (total,) + tail, dtype)[:total]
             if total:
@@ -376,8 +398,10 @@ class SampleGatherPipeline:
                 host[:total].copy_(packed, non_blocking=True)
             return host[:total]
 
-        out = {"unique_ptr": ptr(ucount), "offsets_ptr": [], "local_ptr": [], "offsets": [], "local": [],
+        as_counts = compact_ids and max(sp.fanouts, default=0) <= 255
+        out = {"unique_ptr": ptr(ucount), "offsets_ptr": [], "local_ptr": [], "local": [],
                "local_bits": 16 if u16 else 32}
+        out.update({"counts": [], "counts_ptr": []} if as_counts else {"offsets": []})
         out["unique"] = pack("unique", sp.unique, ucount)
         if self.store is not None:
             out["features"] = pack("features", self.features, ucount)
@@ -385,7 +409,11 @@ class SampleGatherPipeline:
             f, t = counts[h] + 1, counts[h + 1]
             out["offsets_ptr"].append(ptr(f))
             out["local_ptr"].append(ptr(t))
-            out["offsets"].append(pack(f"offsets{h}", sp.offsets[h], f))
+            if as_counts:
+                out["counts_ptr"].append(ptr(counts[h]))
+                out["counts"].append(pack(f"counts{h}", sp.offsets[h], counts[h], counts=True))
+            else:
+                out["offsets"].append(pack(f"offsets{h}", sp.offsets[h], f))
             ids = sp.local_nbrs[h] if sp.local_nbrs is not None else sp.nbrs[h]  # relabel=False: global ids
             out["local"].append(pack(f"local{h}", ids, t, narrow=u16))
         ready = torch.cuda.Event()

@@ -110,3 +110,19 @@ def test_write_hotness_overflow(tmp_path):
     h = HotnessMatrices(0, np.array([[1 << 32]], dtype=np.int64), np.zeros((1, 1), np.int64), 0)
     with pytest.raises(OverflowError):
         write_hotness(tmp_path / "o.bin", [h])
+
+
+def test_offsets_from_counts_rebuilds_packed_offsets():
+    """window_to_host(compact_ids=True) ships each hop's offsets as u8 per-position
+    counts; offsets_from_counts restores the packed int32 layout (each batch from 0),
+    empty batches included."""
+    from paper_2305_16588_b200.pipeline import offsets_from_counts
+
+    rng = np.random.default_rng(5)
+    sizes = [3, 0, 7, 1]
+    segs = [rng.integers(0, 16, s).astype(np.uint8) for s in sizes]
+    cptr = np.concatenate(([0], np.cumsum(sizes))).astype(np.int64)
+    off, optr = offsets_from_counts(np.concatenate(segs), cptr)
+    want = np.concatenate([np.concatenate(([0], np.cumsum(s, dtype=np.int64))) for s in segs]).astype(np.int32)
+    assert off.dtype.is_floating_point is False and np.array_equal(off.numpy(), want)
+    assert np.array_equal(optr, np.concatenate(([0], np.cumsum(np.array(sizes) + 1))))

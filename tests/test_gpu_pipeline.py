@@ -355,11 +355,12 @@ def test_window_to_host_packs_every_batch(relabel, lanes, compact, big):
     relabelled ids travel as 16-bit values (global ids never do); wait=False returns an
     event the host waits on before reading. big: the unique capacity exceeds 65536, so
     the sampler keeps u32 local ids (narrowed by the packing when compact), else u16
-    (widened by the packing when not compact) — every gc_pack_segments mode."""
+    (widened by the packing when not compact) — every gc_pack_segments mode; compact
+    offsets travel as u8 counts and offsets_from_counts rebuilds them."""
     import paper_2305_16588_b200 as P
     from paper_2305_16588_b200.cache import FeatureStore
     from paper_2305_16588_b200.graph import synthetic_features_device
-    from paper_2305_16588_b200.pipeline import SampleGatherPipeline
+    from paper_2305_16588_b200.pipeline import SampleGatherPipeline, offsets_from_counts
 
     n, dim, batch, fanouts = (100_000, 32, 1024, (15, 10)) if big else (30_000, 100, 96, (7, 3))
     g = P.generate_synthetic(n, 12, 1.2, seed=12)
@@ -378,6 +379,15 @@ def test_window_to_host_packs_every_batch(relabel, lanes, compact, big):
             out["ready"].synchronize()
         assert out["local_bits"] == (16 if compact and relabel else 32)
         sp = p.sampler
+        if compact:  # offsets travel as u8 per-position counts
+            assert "offsets" not in out and all(c.dtype == torch.uint8 for c in out["counts"])
+            offsets = []
+            for h in range(len(fanouts)):
+                o, optr = offsets_from_counts(out["counts"][h], out["counts_ptr"][h])
+                assert np.array_equal(optr, out["offsets_ptr"][h])
+                offsets.append(o)
+        else:
+            offsets = out["offsets"]
         for b in range(nbw):
             u0, u1 = out["unique_ptr"][b : b + 2]
             u = int(sp.ucount[b])
@@ -389,7 +399,7 @@ def test_window_to_host_packs_every_batch(relabel, lanes, compact, big):
                 o0, o1 = out["offsets_ptr"][h][b : b + 2]
                 l0, l1 = out["local_ptr"][h][b : b + 2]
                 assert o1 - o0 == f + 1 and l1 - l0 == t
-                assert torch.equal(out["offsets"][h][o0:o1], sp.offsets[h][b, : f + 1].cpu())
+                assert torch.equal(offsets[h][o0:o1], sp.offsets[h][b, : f + 1].cpu())
                 want = local_ids(sp.local_nbrs[h][b, :t]) if relabel else sp.nbrs[h][b, :t].long()
                 got = out["local"][h][l0:l1]
                 if out["local_bits"] == 16:
