@@ -57,6 +57,10 @@ int gc_abi_version(void);
  * whole window (default 16: the GPU is full). Fewer leave SM room for another lane's
  * kernels while a PCIe-bound gather runs. */
 #define GC_OPT_GATHER_CTAS_PER_SM 3
+/* GC_OPT_UNIQUE_BATCH_CTAS: gc_unique_compact's dense path runs one CTA per batch (one
+ * launch) when the window has at least this many batches, else three per-tile passes
+ * (0, the default: the SM count). Both give identical outputs. */
+#define GC_OPT_UNIQUE_BATCH_CTAS 4
 int gc_set_option(int option, int value);
 const char* gc_last_error(void);
 /* device ordinal of the calling thread's current device; -1 if none */

@@ -26,6 +26,7 @@ GC_MAX_PEERS = 8
 GC_OPT_EXACT_SELECTION = 1
 GC_OPT_DEFER_CTAS = 2
 GC_OPT_GATHER_CTAS_PER_SM = 3
+GC_OPT_UNIQUE_BATCH_CTAS = 4
 GC_TIER_HOST = 0xFFFFFFFF
 
 _c_u64p = ctypes.c_void_p  # every device pointer crosses as an opaque address

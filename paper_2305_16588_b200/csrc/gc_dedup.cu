@@ -107,6 +107,77 @@ __global__ void __launch_bounds__(kUniqThreads) k_unique(UniqueParams p) {
     }
 }
 
+// Dense compaction with one 1024-thread CTA per batch, for windows of at least a
+// GPU's worth of batches (C2: 235): the CTA walks its batch's bitmap in 4096-word
+// chunks (the next chunk's loads in flight while the current one is scanned and
+// emitted), so there is one launch instead of three and no per-tile CTA turnover.
+// Same outputs as k_unique_counts + k_unique_tile_scan + k_unique.
+constexpr int kFusedThreads = 1024;
+constexpr uint32_t kFusedWords = kFusedThreads * kWordsPerThread;
+
+__global__ void __launch_bounds__(kFusedThreads) k_unique_batch(UniqueParams p) {
+    __shared__ uint32_t s_warp[2][32];
+    const uint32_t b = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    uint32_t* row = p.bm + b * p.bwords;
+    uint32_t* out = p.uniq + b * p.ustride;
+    uint4* rt = p.rank ? reinterpret_cast<uint4*>(p.rank + b * p.bwords) : nullptr;
+    uint32_t run = 0;
+    uint64_t w0 = (uint64_t)tid * kWordsPerThread;
+    uint4 x = w0 < p.bwords ? *reinterpret_cast<const uint4*>(row + w0) : make_uint4(0, 0, 0, 0);
+    for (uint32_t it = 0; (uint64_t)it * kFusedWords < p.bwords; ++it) {
+        const uint64_t wn = w0 + kFusedWords;
+        const uint4 xn = wn < p.bwords ? *reinterpret_cast<const uint4*>(row + wn) : make_uint4(0, 0, 0, 0);
+        const uint32_t c0 = __popc(x.x), c1 = __popc(x.y), c2 = __popc(x.z), c3 = __popc(x.w);
+        const uint32_t cnt = c0 + c1 + c2 + c3;
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += y;
+        }
+        uint32_t* sw = s_warp[it & 1];  // alternating: no barrier before the next chunk's writes
+        if (lane == 31) sw[wid] = incl;
+        __syncthreads();
+        if (wid == 0) {
+            uint32_t v = sw[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(kFull, v, o);
+                if (lane >= o) v += y;
+            }
+            sw[lane] = v;
+        }
+        __syncthreads();
+        const uint32_t base = run + (wid ? sw[wid - 1] : 0u) + incl - cnt;
+        run += sw[31];
+        if (cnt) {
+            if (rt) {
+                if (x.x | x.y) rt[w0 / 2] = make_uint4(base, x.x, base + c0, x.y);
+                if (x.z | x.w) rt[w0 / 2 + 1] = make_uint4(base + c0 + c1, x.z, base + c0 + c1 + c2, x.w);
+            }
+            uint32_t pos = base;
+            const uint32_t words[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                uint32_t w = words[k];
+                const uint32_t vbase = (uint32_t)((w0 + k) * 32);
+                while (w) {
+                    const uint32_t u = vbase + (__ffs(w) - 1);
+                    if (pos < p.ustride) out[pos] = u;  // capacity guard, as in k_unique
+                    ++pos;
+                    if (p.feat) atomicAdd((unsigned long long*)(p.feat + u), 1ull);
+                    w &= w - 1;
+                }
+            }
+            if (p.clear) *reinterpret_cast<uint4*>(row + w0) = make_uint4(0, 0, 0, 0);
+        }
+        x = xn;
+        w0 = wn;
+    }
+    if (tid == 0) p.ucount[b] = run;
+}
+
 // Sparse compaction, fully parallel over the non-empty 32-word blocks (1024 vertices):
 //   k_block_lists   one CTA per batch: summary bits -> ascending list of non-empty
 //                   blocks (and the summary is cleared as it is read)
@@ -378,6 +449,11 @@ __global__ void k_mark(const uint32_t* __restrict__ ids, uint64_t stride, const 
         mark_visited(row, srow, ids[b * stride + k]);
 }
 
+// GC_OPT_UNIQUE_BATCH_CTAS: windows of at least this many batches take the
+// CTA-per-batch dense compaction (0: the SM count)
+static int g_unique_batch_min = 0;
+void set_unique_batch_min(int v) { g_unique_batch_min = v; }
+
 static unsigned uniq_tiles(const gc_visited_t* v) {
     uint64_t t = (v->words + kWordsPerTile - 1) / kWordsPerTile;
     return t ? (unsigned)t : 1u;
@@ -484,6 +560,7 @@ int gc_unique_compact(const gc_visited_t* visited, uint32_t num_batches, uint32_
         return GC_OK;
     }
     const unsigned tiles = uniq_tiles(visited);
+    const uint32_t batch_ctas_from = g_unique_batch_min ? (uint32_t)g_unique_batch_min : sm_count();
     UniqueParams p{};
     p.bm = visited->bitmap;
     p.bwords = visited->words;
@@ -495,6 +572,11 @@ int gc_unique_compact(const gc_visited_t* visited, uint32_t num_batches, uint32_
     p.feat = d_feat_lookups;
     p.clear = clear_bitmap;
     p.tile_count = static_cast<uint32_t*>(d_temp);
+    if (num_batches >= batch_ctas_from) {
+        k_unique_batch<<<num_batches, kFusedThreads, 0, s>>>(p);
+        GC_CHECK_LAUNCH("gc_unique_compact batch");
+        return GC_OK;
+    }
     GC_REQUIRE(num_batches < 65536, GC_ERR_VALUE, "gc_unique_compact: at most 65535 batches per call");
     const dim3 grid(tiles, num_batches);
     k_unique_counts<<<grid, kUniqThreads, 0, s>>>(p);

@@ -800,6 +800,11 @@ int gc_set_option(int option, int value) {
         gc::set_defer_ctas(value);
         return GC_OK;
     }
+    if (option == GC_OPT_UNIQUE_BATCH_CTAS) {
+        GC_REQUIRE(value >= 0, GC_ERR_VALUE, "gc_set_option: GC_OPT_UNIQUE_BATCH_CTAS out of range");
+        gc::set_unique_batch_min(value);
+        return GC_OK;
+    }
     GC_REQUIRE(option == GC_OPT_EXACT_SELECTION, GC_ERR_VALUE, "gc_set_option: unknown option");
     g_exact_only = value ? 1 : 0;
     return GC_OK;

@@ -25,10 +25,24 @@ def _device():
     torch.cuda.set_device(0)
 
 
+@pytest.fixture(params=[False, True], ids=["tile_passes", "cta_per_batch"])
+def unique_batch_path(request):
+    """Dense compaction through the per-tile passes, or forced onto the CTA-per-batch
+    kernel (taken by windows of >= SM-count batches, e.g. C2's 235) for every window."""
+    from paper_2305_16588_b200 import _lib
+
+    lib = _lib.lib()
+    _lib.check(lib.gc_set_option(_lib.GC_OPT_UNIQUE_BATCH_CTAS, 1 if request.param else 0))
+    yield request.param
+    _lib.check(lib.gc_set_option(_lib.GC_OPT_UNIQUE_BATCH_CTAS, 0))
+
+
 @pytest.mark.parametrize("sparse", [False, True])
 @pytest.mark.parametrize("window,batch,fanouts,deg", [(0, 256, (15, 10, 5), 26), (3, 100, (25, 10), 14),
                                                        (2, 77, (4, 4), 40), (5, 64, (3,), 200)])
-def test_epoch_windows_match_oracle(window, batch, fanouts, deg, sparse):
+def test_epoch_windows_match_oracle(window, batch, fanouts, deg, sparse, unique_batch_path):
+    if sparse and unique_batch_path:
+        pytest.skip("the CTA-per-batch kernel is a dense-bitmap path")
     import paper_2305_16588_b200 as P
     from paper_2305_16588_b200.cache import FeatureStore
     from paper_2305_16588_b200.graph import synthetic_features_device
@@ -74,8 +88,10 @@ def test_epoch_windows_match_oracle(window, batch, fanouts, deg, sparse):
 
 
 @pytest.mark.parametrize("sparse", [False, True])
-def test_epoch_presampling_counters_match_reference_semantics(sparse):
+def test_epoch_presampling_counters_match_reference_semantics(sparse, unique_batch_path):
     """Hotness fused into the window pipeline equals the oracle epoch trace."""
+    if sparse and unique_batch_path:
+        pytest.skip("the CTA-per-batch kernel is a dense-bitmap path")
     import paper_2305_16588_b200 as P
     from paper_2305_16588_b200.pipeline import SampleGatherPipeline
     from paper_2305_16588_b200.sampling import DeviceHotness
