@@ -190,6 +190,8 @@ int gc_unique_compact(const gc_visited_t* visited, uint32_t num_batches, uint32_
                       uint64_t unique_stride, uint32_t* d_unique_count, uint32_t* d_rank_table,
                       uint64_t* d_feat_lookups, int clear_bitmap, void* d_temp, size_t temp_bytes,
                       void* stream);
+/* Kernels one gc_unique_compact call launches for this window (launch accounting). */
+int gc_unique_compact_launches(uint32_t num_batches, const gc_visited_t* visited);
 /* Relabel (not in the reference; CPU restatement np.searchsorted(unique, ids)):
  * d_local[b*stride + k] = index of d_ids[b*stride + k] in batch b's unique list. */
 int gc_relabel(const uint32_t* d_ids, uint64_t ids_stride, const uint32_t* d_ids_count, uint32_t max_count,

@@ -136,6 +136,7 @@ SIGNATURES = {
     "gc_summary_words": (U64, [I64]),
     "gc_unique_temp_bytes": (SZ, [U32, ctypes.POINTER(GcVisited)]),
     "gc_unique_compact": (ctypes.c_int, [ctypes.POINTER(GcVisited), U32, V, U64, V, V, V, ctypes.c_int, V, SZ, V]),
+    "gc_unique_compact_launches": (ctypes.c_int, [U32, ctypes.POINTER(GcVisited)]),
     "gc_relabel": (ctypes.c_int, [V, U64, V, U32, U32, V, U64, V, V]),
     "gc_relabel16": (ctypes.c_int, [V, U64, V, U32, U32, V, U64, V, V]),
     "gc_mark_visited": (ctypes.c_int, [V, U64, V, U32, U32, ctypes.POINTER(GcVisited), V]),

@@ -588,6 +588,12 @@ int gc_unique_compact(const gc_visited_t* visited, uint32_t num_batches, uint32_
     return GC_OK;
 }
 
+int gc_unique_compact_launches(uint32_t num_batches, const gc_visited_t* visited) {
+    if (!visited || num_batches == 0) return 0;
+    if (visited->summary) return 4;
+    return num_batches >= (g_unique_batch_min ? (uint32_t)g_unique_batch_min : sm_count()) ? 1 : 3;
+}
+
 int gc_relabel(const uint32_t* d_ids, uint64_t ids_stride, const uint32_t* d_ids_count, uint32_t max_count,
                uint32_t num_batches, const uint32_t* d_rank_table, uint64_t bitmap_words, uint32_t* d_local,
                void* stream) {

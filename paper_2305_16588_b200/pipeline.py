@@ -269,8 +269,8 @@ class SampleGatherPipeline:
         side = self._relabel_sides[self._lane] if (self._relabel_sides and self.store is not None
                                                    and self.timer is None) else None
         sp.dedup(hot, relabel_stream=side)
-        # compaction: tile counts, scan, emit (+ block lists when sparse); one relabel per level
-        self.launches += (4 if sp.summary is not None else 3) + (H + 1 if sp.relabel else 0)
+        # compaction (1, 3 or 4 kernels, see gc_unique_compact_launches); one relabel per level
+        self.launches += sp.lib.gc_unique_compact_launches(nb, sp.visited) + (H + 1 if sp.relabel else 0)
         if end is not None:
             end.record()
         if self.store is not None:

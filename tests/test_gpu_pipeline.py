@@ -426,3 +426,33 @@ def test_window_to_host_packs_every_batch(relabel, lanes, compact, big):
     pipe.run_epoch(pipe.plan_epoch(pool, P.KeyedRng(3).derive(0, 0, 0)), on_window=check)
     assert sum(seen) == -(-len(pool) // batch) and len(seen) == (2 if big else 3)
     assert staging["features"].is_pinned()
+
+
+@pytest.mark.parametrize("sparse,window", [(False, 3), (True, 3), (False, 0)])
+def test_launch_accounting_matches_profiler(sparse, window, unique_batch_path):
+    """pipe.launches (the bench's gpu_launches) equals the number of this library's
+    kernels the CUDA profiler sees for an eager epoch."""
+    if sparse and unique_batch_path:
+        pytest.skip("the CTA-per-batch kernel is a dense-bitmap path")
+    from torch.profiler import ProfilerActivity, profile
+
+    import paper_2305_16588_b200 as P
+    from paper_2305_16588_b200.cache import FeatureStore
+    from paper_2305_16588_b200.graph import synthetic_features_device
+    from paper_2305_16588_b200.pipeline import SampleGatherPipeline
+
+    n = 30_000
+    g = P.generate_synthetic(n, 12, 1.2, seed=5)
+    pool = np.arange(0, n, 7, dtype=np.int64)
+    store = FeatureStore.resident(synthetic_features_device(0, n, 64))
+    pipe = SampleGatherPipeline(g, P.SamplingConfig(fanouts=(10, 5), batch_size=256), store, len(pool),
+                                window=window or None, sparse_visited=sparse)
+    plan = pipe.plan_epoch(pool, P.KeyedRng(4).derive(0, 0, 0))
+    pipe.run_epoch(plan)  # warm-up (lazy allocations)
+    torch.cuda.synchronize()
+    before = pipe.launches
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        pipe.run_epoch(plan)
+        torch.cuda.synchronize()
+    seen = sum(e.count for e in prof.key_averages() if "gc::" in e.key)
+    assert seen == pipe.launches - before > 0
