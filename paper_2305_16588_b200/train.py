@@ -221,6 +221,25 @@ def _mm_f32_into(out: torch.Tensor, a: torch.Tensor, b: torch.Tensor) -> None:
 _MM_OUT_INTO = [None]
 
 
+def _splitk_parts(rows: int) -> int:
+    """Row chunks of the fp32 weight-gradient GEMM (split-K): one torch.mm over 170K rows
+    leaves cuBLAS's SIMT kernel a handful of output tiles; tools/splitk_probe.py."""
+    return 32 if rows >= 65536 else (8 if rows >= 8192 else 1)
+
+
+def _dw_split_into(out: torch.Tensor, g: torch.Tensor, A: torch.Tensor, part: torch.Tensor) -> None:
+    """out = g^T A in fp32 as P strided-batched GEMMs over row chunks plus a fixed-order
+    sum of the P partials (deterministic; remainder rows added last)."""
+    P, rows = part.shape[0], g.shape[0]
+    ch = rows // P
+    gv = g.as_strided((P, ch, g.shape[1]), (ch * g.stride(0), g.stride(0), 1))
+    av = A.as_strided((P, ch, A.shape[1]), (ch * A.stride(0), A.stride(0), 1))
+    torch.bmm(gv.transpose(1, 2), av, out=part)
+    torch.sum(part, 0, out=out)
+    if P * ch < rows:
+        out.addmm_(g[P * ch :].t(), A[P * ch :])
+
+
 def _mm_f32(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
     """a @ b accumulated and returned in fp32 (bf16 operands stay on the tensor cores)."""
     if a.dtype == torch.float32:
@@ -367,6 +386,11 @@ class TreeTrainer:
             A[:, cols] = 1.0
             self.A.append(A)
             self.Z.append(torch.zeros((rows, hid), dtype=self.act, device=dev))
+        # split-K partials of the fp32 weight gradients (bf16 runs use the tensor cores)
+        self.dW_parts = []
+        for l, (d, cols, ext, hid) in enumerate(self.shape):
+            P = _splitk_parts(self.base[L - l]) if self.act == torch.float32 else 1
+            self.dW_parts.append(torch.empty((P, hid, ext), dtype=torch.float32, device=dev) if P > 1 else None)
         self.loss = torch.zeros((), dtype=torch.float32, device=dev)
         # classifier head (gc_tree_head): gradient w.r.t. the top layer's pre-activations
         # of the seed rows, and the kernel's work buffer
@@ -428,7 +452,11 @@ class TreeTrainer:
         g = self.g_top
         for l in range(L - 1, -1, -1):
             d, cols, ext, hid = self.shape[l]
-            _mm_f32_into(self.dW[l], g.t(), self.A[l])  # the ones column gives the bias gradient
+            # the ones column of A gives the bias gradient
+            if self.dW_parts[l] is not None:
+                _dw_split_into(self.dW[l], g, self.A[l], self.dW_parts[l])
+            else:
+                _mm_f32_into(self.dW[l], g.t(), self.A[l])
             if l == 0:
                 break
             dA = g @ Wa[l][:, :cols]
