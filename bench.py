@@ -42,17 +42,21 @@ C3 = {
     "training_fraction": 0.1,
     "master_seed": 7,
     "budget_frac_per_gpu": 0.1,
-    "window": 256,  # batches per launch window
-    "feat_rows_cap": 60_000,  # distinct rows per batch the window buffers hold (checked before timing)
+    "window": 2048,  # batches per launch window
+    "feat_rows_cap": 20_000,  # distinct rows per batch the window buffers hold (checked before timing)
+    "lanes": 1,
+    # host-tier rows deferred to a second kernel that reads each window's in address
+    # order: 64.3K -> 94.1K batches/s at C3 (profiles/r02_host_tier_pages.md)
+    "defer_host": True,
 }
 # BASELINE configs[3] and [4]: the same flow at their shapes (python bench.py --tier-workload c4|c5)
 C4 = {**C3, "workload": "C4 UK-2007-shaped synthetic (GCN 2-layer input): 105M vertices, 3.7B edges, 128-d; "
                         "topology partially host-resident (UVA), cache partitioned over the clique",
-      "num_vertices": 105_000_000, "avg_degree": 35, "window": 128, "feat_rows_cap": 160_000}
+      "num_vertices": 105_000_000, "avg_degree": 35, "window": 2048, "feat_rows_cap": 32_768}
 C5 = {**C3, "workload": "C5 Friendster-shaped synthetic: 65M vertices, 3.6B edges, 256-d features, tight HBM budget "
                         "(5% of topology+feature bytes per GPU)",
-      "num_vertices": 65_000_000, "avg_degree": 55, "feature_dim": 256, "budget_frac_per_gpu": 0.05, "window": 64,
-      "feat_rows_cap": 160_000}
+      "num_vertices": 65_000_000, "avg_degree": 55, "feature_dim": 256, "budget_frac_per_gpu": 0.05, "window": 512, "lanes": 2,
+      "feat_rows_cap": 32_768}
 TIER_WORKLOADS = {"c3": C3, "c4": C4, "c5": C5}
 PCIE_NOMINAL_GBS = 64.0  # PCIe Gen5 x16, north_star's tier roofline
 NVLINK_GBS = 900.0  # NVLink 5 per direction
@@ -97,6 +101,14 @@ def parse():
     ap.add_argument("--c3-warmup", type=int, default=3)
     ap.add_argument("--c3-presample-epochs", type=int, default=32,
                     help="presampling epochs behind the cache plan (the reference default is 1; 32 epochs take ~3.4 s at C3 on one B200 and bring the plan's in-sample PCIe prediction within 0.01%% of fresh epochs)")
+    ap.add_argument("--c3-window", type=int, default=0, help="three-tier window in batches (0: the workload's)")
+    ap.add_argument("--c3-fcap", type=int, default=0, help="three-tier distinct rows per batch held (0: the workload's)")
+    ap.add_argument("--c3-lanes", type=int, default=0, help="three-tier pipeline lanes (0: the workload's)")
+    ap.add_argument("--c3-defer", type=int, default=-1,
+                    help="1: host-tier rows deferred to a second kernel that reads them in address order; "
+                         "0: inline in the gather; -1: the workload's")
+    ap.add_argument("--c3-defer-ctas", type=int, default=0, help="CTAs of the deferred host-row kernel (0: default)")
+    ap.add_argument("--c3-only", action="store_true", help="skip the C2 sections (three-tier section alone)")
     ap.add_argument("--c3-budget-frac", type=float, default=0.0,
                     help="per-GPU cache budget / (topology + feature bytes), 0 = the workload's; the clique's is "
                          "world x this")
@@ -384,6 +396,13 @@ def run_b200(args):
         else:
             dist.init_process_group(backend)
 
+    if args.c3_only:
+        out = c3_run(args, rank, local, world)
+        if rank == 0:
+            print(json.dumps({f"{args.tier_workload}_three_tier": out}), flush=True)
+        if world > 1:
+            dist.destroy_process_group()
+        return
     g, pools, layout = build_inputs(args.num_vertices, world)
     pool = pools[rank]
     cfg = SamplingConfig(fanouts=tuple(CONFIG["fanouts"]), batch_size=CONFIG["batch_size"],
@@ -599,16 +618,18 @@ def c3_run(args, rank, local, world):
     torch.cuda.synchronize()
     t_cache = time.perf_counter() - t0
     nb = math.ceil(len(pool) / B)
-    win, fcap = min(C3["window"], nb), C3["feat_rows_cap"]
-    pipe = SampleGatherPipeline(g, cfg, cr.features, len(pool), window=win, feat_rows_cap=fcap,
-                                topology=cr.topology, lanes=2)
-    root = P.KeyedRng(P.derive_seed(seed, 5))
-    plans = [pipe.plan_epoch(pool, root.derive(e, 0, rank)) for e in range(args.c3_warmup + args.c3_steps)]
-    timed = plans[args.c3_warmup :]
+    win = min(args.c3_window or C3["window"], nb)
+    fcap = args.c3_fcap or C3["feat_rows_cap"]
+    lanes = args.c3_lanes or C3["lanes"]
+    defer = bool(C3["defer_host"] if args.c3_defer < 0 else args.c3_defer)
     # untimed passes over the timed epochs, one lane: algorithmic bytes, the capacity
-    # check (before timing), per-stage device times
+    # check (before timing), per-stage device times (built and freed before the timed
+    # pipeline, so the two never hold their window buffers at once)
     seq = SampleGatherPipeline(g, cfg, cr.features, len(pool), window=win, feat_rows_cap=fcap,
-                               topology=cr.topology, lanes=1)
+                               topology=cr.topology, lanes=1, defer_host=defer)
+    root = P.KeyedRng(P.derive_seed(seed, 5))
+    plans = [seq.plan_epoch(pool, root.derive(e, 0, rank)) for e in range(args.c3_warmup + args.c3_steps)]
+    timed = plans[args.c3_warmup :]
     acc = {"sampling": 0, "dedup": 0, "gather": 0}
 
     def account(p, w0, nbw):
@@ -628,6 +649,13 @@ def c3_run(args, rank, local, world):
     torch.cuda.synchronize()
     stages = {k: v[1] / len(timed) for k, v in timer.summary().items()}
     del seq
+    torch.cuda.empty_cache()
+    pipe = SampleGatherPipeline(g, cfg, cr.features, len(pool), window=win, feat_rows_cap=fcap,
+                                topology=cr.topology, lanes=lanes, defer_host=defer)
+    if args.c3_defer_ctas:
+        from paper_2305_16588_b200 import _lib
+
+        _lib.check(_lib.lib().gc_set_option(_lib.GC_OPT_DEFER_CTAS, args.c3_defer_ctas))
     for pl in plans[: args.c3_warmup]:
         pipe.run_epoch_graph(pl)
     torch.cuda.synchronize()
@@ -658,6 +686,15 @@ def c3_run(args, rank, local, world):
     t_tier = {"hbm": hbm_b / (peak * 1e9), "nvlink": nvl_b / (NVLINK_GBS * 1e9), "pcie": pcie_b / (PCIE_NOMINAL_GBS * 1e9)}
     my_roof_s = max(t_tier.values())  # this rank's epochs at the tier roofline
     my_frac = my_roof_s / (my_ms / 1000.0)
+    # the host tier's random-row read rate on this box, over this table, through the
+    # product's own host-tier gather (all ranks at once): the rate the inline gather is
+    # held to, which the address-ordered deferred read beats (profiles/r02_host_tier_pages.md)
+    from paper_2305_16588_b200.bandwidth import random_read_gbs
+
+    barrier()
+    host_row_gbs = random_read_gbs(host.tensor.data_ptr(), host.nbytes, row)
+    barrier()
+    host_achieved_gbs = pcie_b / (my_ms / 1000.0) / 1e9
     measured_txn = t["host_txn"] + f["host"] * row_txns
     # whole clique: device time is the max over ranks; bytes and transactions add up
     total_ms = max_over_ranks(my_ms)
@@ -672,7 +709,10 @@ def c3_run(args, rank, local, world):
         "steps": len(timed), "warmup": args.c3_warmup, "ms_per_step": total_ms / len(timed),
         "config": {**C3, "num_vertices": n, "num_edges": g.num_edges, "scale": args.c3_scale,
                    "budget_bytes_clique": budget, "budget_frac_per_gpu": budget_frac,
-                   "batches_per_step_per_gpu": nb, "window_batches": pipe.window, "lanes": pipe.lanes,
+                   "batches_per_step_per_gpu": nb, "window_batches": pipe.window, "feat_rows_cap": fcap,
+                   "lanes": pipe.lanes,
+                   "host_rows": "deferred: per window, read in address order after the local/peer gather"
+                                if defer else "inline in the gather",
                    "cuda_graph": True, "parallelism": f"dp{world}, cache partitioned over {world} GPU(s)",
                    "host_tier": "one node-shared pinned table (/dev/shm + cudaHostRegister), UVA reads",
                    "l2": "inputs (tens of GB of topology and features at scale 1) far larger than L2"},
@@ -692,7 +732,13 @@ def c3_run(args, rank, local, world):
                           "bound_rank0": max(t_tier, key=t_tier.get),
                           "measured_us_per_batch_rank0": my_ms * 1000 / batches,
                           "frac_min_over_ranks": min_frac,
-                          "frac_clique": roof_sum / (total_ms / 1000.0)},
+                          "frac_clique": roof_sum / (total_ms / 1000.0),
+                          "host_tier_rank0": {
+                              "random_row_read_gbs": host_row_gbs,
+                              "achieved_gbs_over_the_epoch": host_achieved_gbs,
+                              "note": f"random {row} B rows over the {host.nbytes / 1e9:.0f} GB host table measured "
+                                      "with the host-tier gather on this box; achieved = host-tier bytes / epoch "
+                                      "time"}},
         "tiers_per_batch_rank0": {**{k: v / batches for k, v in t.items()},
                                   **{f"rows_{k}": v / batches for k, v in f.items()}},
         "stages_ms_per_epoch_rank0": stages,

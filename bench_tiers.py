@@ -48,7 +48,7 @@ def main():
     ap.add_argument("--presample-epochs", type=int, default=32,
                     help="presampling epochs behind the plan (more: less optimistic estimate, better cache)")
     ap.add_argument("--graph", type=int, default=1, help="1: each timed epoch is one CUDA-graph launch")
-    ap.add_argument("--sweep-lanes", default="", help="extra schedules to time after the main run, e.g. 1,3,2d,2w64 (d: host rows deferred, wN: window)")
+    ap.add_argument("--sweep-lanes", default="", help="extra schedules to time after the main run, e.g. 1,3,2d,2du,2w64 (d: host rows deferred, read in address order; du: deferred, list order; wN: window)")
     ap.add_argument("--alpha-sweep", type=int, default=0,
                     help="validate the cost model: time one epoch at this many alpha points (+ both objectives' picks)")
     ap.add_argument("--pcie-gbs", type=float, default=64.0, help="nominal PCIe Gen5 x16 GB/s for the tier roofline")
@@ -133,9 +133,11 @@ def main():
 
         head, _, gsm = tag.partition("g")
         head, _, win = head.partition("w")
-        lanes, defer = int(head.rstrip("d")), head.endswith("d")
+        # "2du": deferred host rows read in list order instead of address order
+        lanes, defer = int(head.rstrip("du")), "d" in head
         wsize = int(win) if win else a.window
         _lib.check(_lib.lib().gc_set_option(_lib.GC_OPT_GATHER_CTAS_PER_SM, int(gsm) if gsm else 16))
+        _lib.check(_lib.lib().gc_set_option(_lib.GC_OPT_DEFER_ORDER, 0 if "u" in head else 1))
         del pipe
         torch.cuda.empty_cache()
         pipe = SampleGatherPipeline(g, cfg, fstore, len(pool), window=min(wsize, nb), feat_rows_cap=60_000,
@@ -149,6 +151,7 @@ def main():
         torch.cuda.synchronize()
         sweep[tag] = nb * a.steps / (e0.elapsed_time(e1) / 1000.0)
         _lib.check(_lib.lib().gc_set_option(_lib.GC_OPT_GATHER_CTAS_PER_SM, 16))
+        _lib.check(_lib.lib().gc_set_option(_lib.GC_OPT_DEFER_ORDER, 1))
     seq = pipe
     if a.lanes > 1 or sweep:
         del pipe

@@ -61,6 +61,10 @@ int gc_abi_version(void);
  * launch) when the window has at least this many batches, else three per-tile passes
  * (0, the default: the SM count). Both give identical outputs. */
 #define GC_OPT_UNIQUE_BATCH_CTAS 4
+/* GC_OPT_DEFER_ORDER: 1 (default) = gc_gather_deferred reads the window's host rows in
+ * ascending id (address) order (a bucket sort of the deferred list first); 0 = in the
+ * order the gather listed them. Both give identical outputs. */
+#define GC_OPT_DEFER_ORDER 5
 int gc_set_option(int option, int value);
 const char* gc_last_error(void);
 /* device ordinal of the calling thread's current device; -1 if none */

@@ -53,9 +53,10 @@ class MeasuredBandwidths:
 
 
 def random_read_gbs(host_ptr: int, table_bytes: int, read_bytes: int, reads: int = 1 << 20, reps: int = 3,
-                    seed: int = 0) -> float:
+                    seed: int = 0, sorted_chunk: int = 0) -> float:
     """GB/s of `reads` random, `read_bytes`-aligned reads of `read_bytes` each from the
-    mapped host buffer at `host_ptr`, through gc_gather (the host-tier path of K4)."""
+    mapped host buffer at `host_ptr`, through gc_gather (the host-tier path of K4).
+    sorted_chunk > 0 issues the ids in ascending order within each run of that many."""
     from .cache import FeatureStore
 
     if read_bytes % 16 or read_bytes <= 0:
@@ -70,6 +71,11 @@ def random_read_gbs(host_ptr: int, table_bytes: int, read_bytes: int, reads: int
     g = torch.Generator(device="cuda")
     g.manual_seed(seed)
     ids = torch.randint(0, n, (1, reads), dtype=torch.int64, device="cuda", generator=g).to(torch.int32)
+    if sorted_chunk > 0:
+        k = -(-reads // sorted_chunk) * sorted_chunk
+        pad = torch.full((1, k), torch.iinfo(torch.int32).max, dtype=torch.int32, device="cuda")
+        pad[:, :reads] = ids
+        ids = pad.view(-1, sorted_chunk).sort(dim=1).values.view(1, -1)[:, :reads].contiguous()
     cnt = torch.tensor([reads], dtype=torch.int32, device="cuda")
     out = torch.empty((1, reads, dim), dtype=torch.float32, device="cuda")
     fs.gather(ids, cnt, out)  # warm-up

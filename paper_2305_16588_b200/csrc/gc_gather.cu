@@ -148,12 +148,16 @@ __global__ void __launch_bounds__(256, VPL == 1 ? GC_GATHER_MIN_BLOCKS : 4) k_ga
         }
         if (p.defer) {
             // host rows go to the deferred list (read later by a few warps over PCIe);
-            // one atomic per warp
+            // one atomic per warp, plus the largest listed id (the address sort's range)
             const bool d = my_src != nullptr && my_tier == 2;
             const unsigned m = __ballot_sync(kFull, d);
             if (m) {
                 uint32_t base = 0;
-                if (lane == __ffs(m) - 1) base = atomicAdd(p.defer_count, (uint32_t)__popc(m));
+                const uint32_t mx = __reduce_max_sync(kFull, d ? my_id : 0u);
+                if (lane == __ffs(m) - 1) {
+                    base = atomicAdd(p.defer_count, (uint32_t)__popc(m));
+                    atomicMax(p.defer_count + 1, mx);
+                }
                 base = __shfl_sync(kFull, base, __ffs(m) - 1);
                 if (d) {
                     DeferredRow e;
@@ -296,6 +300,72 @@ __global__ void __launch_bounds__(32) k_gather_deferred_tma(const char* __restri
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // writes complete before exit
 }
 
+// Address order for the deferred host rows (GC_OPT_DEFER_ORDER = 1). Random 512-byte
+// reads from a 56 GiB pinned table reach 26 GB/s on the B200 box, the same ids issued in
+// ascending order 41 GB/s (tools/host_page_probe.py, profiles/r02_host_tier_pages.md):
+// the host-side address translation, not the link, limits random reads. So the window's
+// list is bucket-sorted by id (65536 buckets over [0, max id]: histogram, one-CTA scan,
+// scatter) before the TMA kernel walks it; CTAs claim consecutive runs, so the reads in
+// flight at any moment cover a narrow address range. Order within a bucket is free:
+// every entry names its destination row, so the output does not depend on it.
+constexpr uint32_t kDeferBuckets = 1u << 16;
+static int g_defer_order = 1;
+void set_defer_order(int v) { g_defer_order = v; }
+
+__device__ __forceinline__ uint32_t defer_shift(const uint32_t* hdr) {
+    const int bits = 32 - __clz(hdr[1] | 1u);
+    return bits > 16 ? (uint32_t)(bits - 16) : 0u;
+}
+
+__global__ void __launch_bounds__(256) k_defer_hist(const DeferredRow* __restrict__ list, const uint32_t* hdr,
+                                                    uint32_t* __restrict__ hist) {
+    const uint32_t n = hdr[0], sh = defer_shift(hdr);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        atomicAdd(&hist[list[i].id >> sh], 1u);
+}
+
+// exclusive scan of the 65536 bucket counts in place: 1024 threads x 64 counts
+__global__ void __launch_bounds__(1024) k_defer_scan(uint32_t* __restrict__ hist) {
+    __shared__ uint32_t s_sum[1024];
+    const uint32_t t = threadIdx.x;
+    uint4* h = reinterpret_cast<uint4*>(hist + t * 64);
+    uint32_t sum = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const uint4 v = h[k];
+        sum += v.x + v.y + v.z + v.w;
+    }
+    s_sum[t] = sum;
+    __syncthreads();
+    for (uint32_t o = 1; o < 1024; o <<= 1) {
+        const uint32_t v = t >= o ? s_sum[t - o] : 0u;
+        __syncthreads();
+        s_sum[t] += v;
+        __syncthreads();
+    }
+    uint32_t run = s_sum[t] - sum;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        uint4 v = h[k];
+        const uint4 c = v;
+        v.x = run;
+        v.y = v.x + c.x;
+        v.z = v.y + c.y;
+        v.w = v.z + c.z;
+        run = v.w + c.w;
+        h[k] = v;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_defer_scatter(const DeferredRow* __restrict__ list, const uint32_t* hdr,
+                                                       uint32_t* __restrict__ cursor, DeferredRow* __restrict__ sorted) {
+    const uint32_t n = hdr[0], sh = defer_shift(hdr);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const DeferredRow e = list[i];
+        sorted[atomicAdd(&cursor[e.id >> sh], 1u)] = e;
+    }
+}
+
 static int defer_rows_in_flight(uint32_t row_bytes) {
     int r = (int)(32768u / row_bytes);
     return r > 64 ? 64 : (r < 1 ? 1 : r);
@@ -367,13 +437,13 @@ static int gather_impl(const gc_feature_store_t* store, const uint32_t* d_ids, u
     const bool vec16 = store->row_bytes % 16 == 0 && ((uintptr_t)d_out % 16 == 0);
     const uint32_t per_row = store->row_bytes / (vec16 ? 16 : 4);
     cudaStream_t s = as_stream(stream);
-    const bool defer = d_defer != nullptr && vec16 && per_row <= 32 && store->location && store->host_rows;
+    const bool defer = d_defer != nullptr && vec16 && per_row <= 128 && store->location && store->host_rows;
     if (defer) {
         GC_REQUIRE(defer_bytes >= gc_gather_defer_bytes(max_count, num_batches), GC_ERR_VALUE,
                    "gc_gather_deferred: defer buffer too small");
         p.defer_count = static_cast<uint32_t*>(d_defer);
         p.defer = reinterpret_cast<DeferredRow*>(static_cast<char*>(d_defer) + 256);
-        GC_TRY(cudaMemsetAsync(p.defer_count, 0, sizeof(uint32_t), s), "gc_gather_deferred memset");
+        GC_TRY(cudaMemsetAsync(p.defer_count, 0, 2 * sizeof(uint32_t), s), "gc_gather_deferred memset");
     }
     uint64_t work = (uint64_t)max_count * per_row;
     uint64_t gx = (work + 255) / 256;
@@ -417,10 +487,23 @@ static int gather_impl(const gc_feature_store_t* store, const uint32_t* d_ids, u
             GC_TRY(cudaEventRecord(e0, s), "event record");
             GC_TRY(cudaStreamWaitEvent(hs, e0, 0), "stream wait");
         }
+        const DeferredRow* list = p.defer;
+        if (g_defer_order) {
+            const uint64_t cap = (uint64_t)max_count * num_batches;
+            DeferredRow* sorted = p.defer + cap;
+            uint32_t* hist = reinterpret_cast<uint32_t*>(sorted + cap);
+            GC_TRY(cudaMemsetAsync(hist, 0, kDeferBuckets * sizeof(uint32_t), hs), "gc_gather_deferred memset");
+            const int g = sm_count() * 4;
+            k_defer_hist<<<g, 256, 0, hs>>>(p.defer, p.defer_count, hist);
+            k_defer_scan<<<1, 1024, 0, hs>>>(hist);
+            k_defer_scatter<<<g, 256, 0, hs>>>(p.defer, p.defer_count, hist, sorted);
+            GC_CHECK_LAUNCH("gc_gather_deferred sort");
+            list = sorted;
+        }
         const int R = defer_rows_in_flight(store->row_bytes);
         const size_t smem = ((size_t)24 * R + 127) / 128 * 128 + (size_t)R * store->row_bytes;
         k_gather_deferred_tma<<<g_defer_ctas, 32, smem, hs>>>(static_cast<const char*>(store->host_rows),
-                                                               store->row_bytes, p.defer, p.defer_count, p.out, R);
+                                                               store->row_bytes, list, p.defer_count, p.out, R);
         GC_CHECK_LAUNCH("gc_gather_deferred");
         if (hs != s) {
             GC_TRY(cudaEventRecord(e1, hs), "event record");
@@ -433,7 +516,8 @@ static int gather_impl(const gc_feature_store_t* store, const uint32_t* d_ids, u
 }
 
 uint64_t gc_gather_defer_bytes(uint32_t max_count, uint32_t num_batches) {
-    return 256 + (uint64_t)max_count * num_batches * sizeof(DeferredRow);
+    // header (count, max id), the list, its address-sorted copy, the bucket counts
+    return 256 + 2 * (uint64_t)max_count * num_batches * sizeof(DeferredRow) + kDeferBuckets * sizeof(uint32_t);
 }
 
 int gc_gather(const gc_feature_store_t* store, const uint32_t* d_ids, uint64_t ids_stride, const uint32_t* d_count,

@@ -118,11 +118,15 @@ class SampleGatherPipeline:
                 feats = torch.empty((self.window, sp.ucap, store.spec.dimension), dtype=torch.float32, device="cuda")
             self.lane_features.append(feats)
         self.lane_streams = [torch.cuda.Stream() for _ in range(lanes)] if lanes > 1 else []
-        # host-tier rows (PCIe-bound, few CTAs) on a high-priority stream: its CTAs take
-        # SM slots as soon as any free up and run under the other lanes' sampling
-        # measured at C3 (profiles/r01_tiers_c3_lanes.md): deferring host rows to a
-        # small-grid kernel does not overlap — its CTAs find no free registers while
-        # the sampling kernels fill the SMs — so it is off unless asked for
+        # defer_host: a window's host-tier rows are listed by the gather and read by a
+        # second small-grid kernel in ascending address order (gc_gather_deferred,
+        # GC_OPT_DEFER_ORDER). Random host rows are held to ~26 GB/s by the box's
+        # host-side address translation; address order over a large window reads
+        # faster: C3 64.3K -> 94.1K batches/s with windows of 2048 batches on one lane,
+        # C4 35.1K -> 53.3K (profiles/r02_host_tier_pages.md). It does not overlap the
+        # next window's sampling (r01_tiers_c3_lanes.md: its CTAs find no free
+        # registers), so it pays with large windows and is off unless asked for.
+        # With lanes > 1 it runs on a high-priority stream.
         self.defer_host = False if defer_host is None else bool(defer_host)
         self.host_stream = torch.cuda.Stream(priority=-1) if self.defer_host and lanes > 1 else None
         self.sampler = self.lane_samplers[0]

@@ -221,18 +221,49 @@ def test_gather_deferred_host_rows_bit_exact(dim):
         ids[b, : min(counts[b], cap)] = np.sort(rng.choice(n, min(counts[b], cap), replace=False))
     d_ids = torch.from_numpy(ids.astype(np.uint32).view(np.int32)).cuda()
     d_cnt = torch.from_numpy(counts.astype(np.int32)).cuda()
+    from paper_2305_16588_b200 import _lib
+
     outs = []
-    for deferred in (False, True):
+    for deferred, order in ((False, 1), (True, 0), (True, 1)):  # order 1: host rows in address order
+        _lib.check(_lib.lib().gc_set_option(_lib.GC_OPT_DEFER_ORDER, order))
         out = torch.full((W, cap, dim), float("nan"), dtype=torch.float32, device="cuda")
         store.reset_counters()
         store.gather(d_ids, d_cnt, out, deferred=deferred)
         outs.append((out.cpu().numpy(), store.tier_counts()))
-    (a, ta), (b_, tb) = outs
-    assert ta == tb and tb["host"] > 0
+    _lib.check(_lib.lib().gc_set_option(_lib.GC_OPT_DEFER_ORDER, 1))
+    a, ta = outs[0]
+    assert ta["host"] > 0
+    for b_, tb in outs[1:]:
+        assert ta == tb
+        for b in range(W):
+            k = min(counts[b], cap)
+            assert np.array_equal(b_[b, :k], table[ids[b, :k]])
+            assert np.array_equal(a[b, :k], b_[b, :k])
+
+
+def test_gather_deferred_address_order_wide_ids():
+    """The address-ordered deferred read (bucket sort on the id's top 16 significant
+    bits) over 2^22 host rows of 16 bytes, unsorted ids with duplicates across batches:
+    bit-exact against the table."""
+    from paper_2305_16588_b200 import _lib
+    from paper_2305_16588_b200.cache import FeatureStore
+
+    n, dim, W, cap = 1 << 22, 4, 7, 9000
+    table = O.synthetic_features(np.arange(n), dim)
+    rng = np.random.default_rng(5)
+    parts = [rng.choice(n, 100_000, replace=False)]
+    store = FeatureStore.from_assignment(table, parts, self_rank=0)
+    ids = rng.integers(0, n, size=(W, cap))
+    counts = rng.integers(0, cap + 1, size=W)
+    d_ids = torch.from_numpy(ids.astype(np.uint32).view(np.int32)).cuda()
+    d_cnt = torch.from_numpy(counts.astype(np.int32)).cuda()
+    _lib.check(_lib.lib().gc_set_option(_lib.GC_OPT_DEFER_ORDER, 1))
+    out = torch.full((W, cap, dim), float("nan"), dtype=torch.float32, device="cuda")
+    store.gather(d_ids, d_cnt, out, deferred=True)
+    got = out.cpu().numpy()
     for b in range(W):
-        k = min(counts[b], cap)
-        assert np.array_equal(b_[b, :k], table[ids[b, :k]])
-        assert np.array_equal(a[b, :k], b_[b, :k])
+        k = counts[b]
+        assert np.array_equal(got[b, :k], table[ids[b, :k]])
 
 
 def test_synthetic_features_device_matches_oracle():
