@@ -42,21 +42,25 @@ C3 = {
     "training_fraction": 0.1,
     "master_seed": 7,
     "budget_frac_per_gpu": 0.1,
-    "window": 2048,  # batches per launch window
-    "feat_rows_cap": 20_000,  # distinct rows per batch the window buffers hold (checked before timing)
-    "lanes": 1,
+    "window": 1536,  # batches per launch window
+    "feat_rows_cap": 16_384,  # distinct rows per batch the window buffers hold (checked before timing)
+    "lanes": 2,
     # host-tier rows deferred to a second kernel that reads each window's in address
-    # order: 64.3K -> 94.1K batches/s at C3 (profiles/r02_host_tier_pages.md)
+    # order, 32 CTAs x 256 rows in flight on a high-priority stream (they hold ~32 SMs'
+    # shared memory, the next window's sampling runs on the rest): 64.3K -> 112K
+    # batches/s at C3 (profiles/r02_host_tier_pages.md)
     "defer_host": True,
+    "defer_ctas": 32,
+    "defer_rows": 256,
 }
 # BASELINE configs[3] and [4]: the same flow at their shapes (python bench.py --tier-workload c4|c5)
 C4 = {**C3, "workload": "C4 UK-2007-shaped synthetic (GCN 2-layer input): 105M vertices, 3.7B edges, 128-d; "
                         "topology partially host-resident (UVA), cache partitioned over the clique",
-      "num_vertices": 105_000_000, "avg_degree": 35, "window": 2048, "feat_rows_cap": 32_768}
+      "num_vertices": 105_000_000, "avg_degree": 35, "window": 1024, "feat_rows_cap": 24_576}
 C5 = {**C3, "workload": "C5 Friendster-shaped synthetic: 65M vertices, 3.6B edges, 256-d features, tight HBM budget "
                         "(5% of topology+feature bytes per GPU)",
-      "num_vertices": 65_000_000, "avg_degree": 55, "feature_dim": 256, "budget_frac_per_gpu": 0.05, "window": 512, "lanes": 2,
-      "feat_rows_cap": 32_768}
+      "num_vertices": 65_000_000, "avg_degree": 55, "feature_dim": 256, "budget_frac_per_gpu": 0.05, "window": 1024,
+      "feat_rows_cap": 24_576, "defer_rows": 128}
 TIER_WORKLOADS = {"c3": C3, "c4": C4, "c5": C5}
 PCIE_NOMINAL_GBS = 64.0  # PCIe Gen5 x16, north_star's tier roofline
 NVLINK_GBS = 900.0  # NVLink 5 per direction
@@ -108,6 +112,8 @@ def parse():
                     help="1: host-tier rows deferred to a second kernel that reads them in address order; "
                          "0: inline in the gather; -1: the workload's")
     ap.add_argument("--c3-defer-ctas", type=int, default=0, help="CTAs of the deferred host-row kernel (0: default)")
+    ap.add_argument("--c3-defer-rows", type=int, default=-1,
+                    help="rows in flight per deferred host-row CTA (-1: the workload's, 0: the library default)")
     ap.add_argument("--c3-only", action="store_true", help="skip the C2 sections (three-tier section alone)")
     ap.add_argument("--c3-budget-frac", type=float, default=0.0,
                     help="per-GPU cache budget / (topology + feature bytes), 0 = the workload's; the clique's is "
@@ -652,10 +658,13 @@ def c3_run(args, rank, local, world):
     torch.cuda.empty_cache()
     pipe = SampleGatherPipeline(g, cfg, cr.features, len(pool), window=win, feat_rows_cap=fcap,
                                 topology=cr.topology, lanes=lanes, defer_host=defer)
-    if args.c3_defer_ctas:
-        from paper_2305_16588_b200 import _lib
+    from paper_2305_16588_b200 import _lib
 
-        _lib.check(_lib.lib().gc_set_option(_lib.GC_OPT_DEFER_CTAS, args.c3_defer_ctas))
+    defer_ctas = args.c3_defer_ctas or C3.get("defer_ctas", 0)
+    defer_rows = args.c3_defer_rows if args.c3_defer_rows >= 0 else C3.get("defer_rows", 0)
+    if defer_ctas:
+        _lib.check(_lib.lib().gc_set_option(_lib.GC_OPT_DEFER_CTAS, defer_ctas))
+    _lib.check(_lib.lib().gc_set_option(_lib.GC_OPT_DEFER_ROWS, defer_rows))
     for pl in plans[: args.c3_warmup]:
         pipe.run_epoch_graph(pl)
     torch.cuda.synchronize()

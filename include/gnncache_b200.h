@@ -65,6 +65,10 @@ int gc_abi_version(void);
  * ascending id (address) order (a bucket sort of the deferred list first); 0 = in the
  * order the gather listed them. Both give identical outputs. */
 #define GC_OPT_DEFER_ORDER 5
+/* GC_OPT_DEFER_ROWS: rows in flight per CTA of gc_gather_deferred's host-row kernel
+ * (0, the default: ~32 KB of rows, at most 64). With GC_OPT_DEFER_CTAS, a few CTAs with
+ * many rows each hold only a few SMs (shared memory), leaving the others free. */
+#define GC_OPT_DEFER_ROWS 6
 int gc_set_option(int option, int value);
 const char* gc_last_error(void);
 /* device ordinal of the calling thread's current device; -1 if none */

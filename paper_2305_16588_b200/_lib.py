@@ -28,6 +28,7 @@ GC_OPT_DEFER_CTAS = 2
 GC_OPT_GATHER_CTAS_PER_SM = 3
 GC_OPT_UNIQUE_BATCH_CTAS = 4
 GC_OPT_DEFER_ORDER = 5
+GC_OPT_DEFER_ROWS = 6
 GC_TIER_HOST = 0xFFFFFFFF
 
 _c_u64p = ctypes.c_void_p  # every device pointer crosses as an opaque address

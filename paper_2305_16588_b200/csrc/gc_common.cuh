@@ -126,6 +126,7 @@ unsigned sm_count();
 void set_defer_ctas(int ctas);  // gc_gather.cu
 void set_gather_ctas_per_sm(int v);  // gc_gather.cu
 void set_defer_order(int v);         // gc_gather.cu
+void set_defer_rows(int v);          // gc_gather.cu
 void set_unique_batch_min(int v);  // gc_dedup.cu
 int cuda_status(cudaError_t err, const char* what);
 

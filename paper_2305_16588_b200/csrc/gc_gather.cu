@@ -366,7 +366,14 @@ __global__ void __launch_bounds__(256) k_defer_scatter(const DeferredRow* __rest
     }
 }
 
+// rows in flight per host-row CTA: 0 = ~32 KB of rows (at most 64); otherwise the
+// GC_OPT_DEFER_ROWS value (a few fat CTAs — e.g. 16 x 384 rows — hold only a few SMs'
+// shared memory, leaving the rest to the next window's sampling)
+static int g_defer_rows = 0;
+void set_defer_rows(int v) { g_defer_rows = v; }
+
 static int defer_rows_in_flight(uint32_t row_bytes) {
+    if (g_defer_rows > 0) return g_defer_rows;
     int r = (int)(32768u / row_bytes);
     return r > 64 ? 64 : (r < 1 ? 1 : r);
 }
@@ -502,6 +509,12 @@ static int gather_impl(const gc_feature_store_t* store, const uint32_t* d_ids, u
         }
         const int R = defer_rows_in_flight(store->row_bytes);
         const size_t smem = ((size_t)24 * R + 127) / 128 * 128 + (size_t)R * store->row_bytes;
+        static size_t smem_opt_in = 48 * 1024;
+        if (smem > smem_opt_in) {
+            GC_TRY(cudaFuncSetAttribute(k_gather_deferred_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                   "gc_gather_deferred: rows in flight exceed shared memory");
+            smem_opt_in = smem;
+        }
         k_gather_deferred_tma<<<g_defer_ctas, 32, smem, hs>>>(static_cast<const char*>(store->host_rows),
                                                                store->row_bytes, list, p.defer_count, p.out, R);
         GC_CHECK_LAUNCH("gc_gather_deferred");

@@ -790,6 +790,11 @@ using namespace gc;
 extern "C" {
 
 int gc_set_option(int option, int value) {
+    if (option == GC_OPT_DEFER_ROWS) {
+        GC_REQUIRE(value >= 0 && value <= 4096, GC_ERR_VALUE, "gc_set_option: GC_OPT_DEFER_ROWS out of range");
+        gc::set_defer_rows(value);
+        return GC_OK;
+    }
     if (option == GC_OPT_DEFER_ORDER) {
         GC_REQUIRE(value == 0 || value == 1, GC_ERR_VALUE, "gc_set_option: GC_OPT_DEFER_ORDER must be 0 or 1");
         gc::set_defer_order(value);
