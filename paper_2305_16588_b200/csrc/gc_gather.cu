@@ -325,6 +325,7 @@ __global__ void __launch_bounds__(256) k_defer_hist(const DeferredRow* __restric
 }
 
 // exclusive scan of the 65536 bucket counts in place: 1024 threads x 64 counts
+static_assert(kDeferBuckets == 1024u * 64u, "k_defer_scan covers 1024 x 64 buckets");
 __global__ void __launch_bounds__(1024) k_defer_scan(uint32_t* __restrict__ hist) {
     __shared__ uint32_t s_sum[1024];
     const uint32_t t = threadIdx.x;

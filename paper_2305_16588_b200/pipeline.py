@@ -122,11 +122,12 @@ class SampleGatherPipeline:
         # second small-grid kernel in ascending address order (gc_gather_deferred,
         # GC_OPT_DEFER_ORDER). Random host rows are held to ~26 GB/s by the box's
         # host-side address translation; address order over a large window reads
-        # faster: C3 64.3K -> 94.1K batches/s with windows of 2048 batches on one lane,
-        # C4 35.1K -> 53.3K (profiles/r02_host_tier_pages.md). It does not overlap the
-        # next window's sampling (r01_tiers_c3_lanes.md: its CTAs find no free
-        # registers), so it pays with large windows and is off unless asked for.
-        # With lanes > 1 it runs on a high-priority stream.
+        # faster. With lanes > 1 it runs on one high-priority stream; given a few fat
+        # host-row CTAs (GC_OPT_DEFER_CTAS / GC_OPT_DEFER_ROWS, e.g. 32 x 256 rows) it
+        # holds only those SMs and the other lane's sampling runs beside it: C3 64.3K ->
+        # 112K batches/s with two lanes of 1536-batch windows
+        # (profiles/r02_host_tier_pages.md). It pays with large windows, so it is off
+        # unless asked for.
         self.defer_host = False if defer_host is None else bool(defer_host)
         self.host_stream = torch.cuda.Stream(priority=-1) if self.defer_host and lanes > 1 else None
         self.sampler = self.lane_samplers[0]
