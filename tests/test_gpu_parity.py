@@ -206,7 +206,9 @@ def test_gather_three_tiers_bit_exact(dim):
 @pytest.mark.parametrize("dim", [64, 100, 128, 256])
 def test_gather_deferred_host_rows_bit_exact(dim):
     """gc_gather_deferred (host rows by a second small-grid kernel) == gc_gather, over a
-    window of batches with ragged counts and a capacity clamp."""
+    window of batches with ragged counts and a capacity clamp: list order, address order,
+    a few fat CTAs (32 x 256 rows for 512-byte rows, as the C3 bench runs it) and a tiny
+    grid (3 CTAs x 5 rows: many rounds per CTA, a partial last round)."""
     from paper_2305_16588_b200.cache import FeatureStore
 
     n, W, cap = 30_000, 5, 3000
@@ -224,13 +226,19 @@ def test_gather_deferred_host_rows_bit_exact(dim):
     from paper_2305_16588_b200 import _lib
 
     outs = []
-    for deferred, order in ((False, 1), (True, 0), (True, 1)):  # order 1: host rows in address order
+    # (deferred, address order, host-row CTAs, rows in flight per CTA; 0 = defaults)
+    for deferred, order, ctas, rows in ((False, 1, 0, 0), (True, 0, 0, 0), (True, 1, 0, 0), (True, 1, 32, 131072 // (4 * dim)),
+                                        (True, 1, 3, 5)):
         _lib.check(_lib.lib().gc_set_option(_lib.GC_OPT_DEFER_ORDER, order))
+        _lib.check(_lib.lib().gc_set_option(_lib.GC_OPT_DEFER_CTAS, ctas or 296))
+        _lib.check(_lib.lib().gc_set_option(_lib.GC_OPT_DEFER_ROWS, rows))
         out = torch.full((W, cap, dim), float("nan"), dtype=torch.float32, device="cuda")
         store.reset_counters()
         store.gather(d_ids, d_cnt, out, deferred=deferred)
         outs.append((out.cpu().numpy(), store.tier_counts()))
     _lib.check(_lib.lib().gc_set_option(_lib.GC_OPT_DEFER_ORDER, 1))
+    _lib.check(_lib.lib().gc_set_option(_lib.GC_OPT_DEFER_CTAS, 296))
+    _lib.check(_lib.lib().gc_set_option(_lib.GC_OPT_DEFER_ROWS, 0))
     a, ta = outs[0]
     assert ta["host"] > 0
     for b_, tb in outs[1:]:
