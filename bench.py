@@ -646,7 +646,7 @@ def c3_run(args, rank, local, world):
 
     for pl in timed:
         seq.run_epoch(pl, on_window=account)
-    seq.check_capacity(reset=True)
+    max_distinct = seq.check_capacity(reset=True)
     timer = StageTimer()
     seq.timer = timer
     for pl in timed:
@@ -720,6 +720,7 @@ def c3_run(args, rank, local, world):
         "config": {**C3, "num_vertices": n, "num_edges": g.num_edges, "scale": args.c3_scale,
                    "budget_bytes_clique": budget, "budget_frac_per_gpu": budget_frac,
                    "batches_per_step_per_gpu": nb, "window_batches": pipe.window, "feat_rows_cap": fcap,
+                   "max_distinct_rows_per_batch_rank0": int(max_distinct),
                    "lanes": pipe.lanes,
                    "host_rows": "deferred: per window, read in address order after the local/peer gather"
                                 if defer else "inline in the gather",
