@@ -626,6 +626,12 @@ def c3_run(args, rank, local, world):
     t_cache = time.perf_counter() - t0
     nb = math.ceil(len(pool) / B)
     win = min(args.c3_window or C3["window"], nb)
+    # equal windows: a short last window is a pipeline stage with nothing to overlap
+    # (C3: 7 windows of 1549 instead of 7 x 1536 + 88, +1.4%); at most 2% larger
+    k = math.ceil(nb / win)
+    if k > 1 and math.ceil(nb / (k - 1)) <= 1.02 * win:
+        k -= 1
+    win = math.ceil(nb / k)
     fcap = args.c3_fcap or C3["feat_rows_cap"]
     lanes = args.c3_lanes or C3["lanes"]
     defer = bool(C3["defer_host"] if args.c3_defer < 0 else args.c3_defer)
