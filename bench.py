@@ -114,6 +114,7 @@ def parse():
     ap.add_argument("--c3-defer-ctas", type=int, default=0, help="CTAs of the deferred host-row kernel (0: default)")
     ap.add_argument("--c3-defer-rows", type=int, default=-1,
                     help="rows in flight per deferred host-row CTA (-1: the workload's, 0: the library default)")
+    ap.add_argument("--c3-graph", type=int, default=1, help="1: each timed three-tier epoch is one CUDA-graph launch")
     ap.add_argument("--c3-only", action="store_true", help="skip the C2 sections (three-tier section alone)")
     ap.add_argument("--c3-budget-frac", type=float, default=0.0,
                     help="per-GPU cache budget / (topology + feature bytes), 0 = the workload's; the clique's is "
@@ -672,8 +673,9 @@ def c3_run(args, rank, local, world):
     if defer_ctas:
         _lib.check(_lib.lib().gc_set_option(_lib.GC_OPT_DEFER_CTAS, defer_ctas))
     _lib.check(_lib.lib().gc_set_option(_lib.GC_OPT_DEFER_ROWS, defer_rows))
+    run = pipe.run_epoch_graph if args.c3_graph else pipe.run_epoch
     for pl in plans[: args.c3_warmup]:
-        pipe.run_epoch_graph(pl)
+        run(pl)
     torch.cuda.synchronize()
     cr.topology.reset_counters()
     cr.features.reset_counters()
@@ -683,7 +685,7 @@ def c3_run(args, rank, local, world):
     for pl in timed:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        pipe.run_epoch_graph(pl)
+        run(pl)
         e1.record()
         torch.cuda.synchronize()
         ms.append(e0.elapsed_time(e1))
@@ -730,7 +732,7 @@ def c3_run(args, rank, local, world):
                    "lanes": pipe.lanes,
                    "host_rows": "deferred: per window, read in address order after the local/peer gather"
                                 if defer else "inline in the gather",
-                   "cuda_graph": True, "parallelism": f"dp{world}, cache partitioned over {world} GPU(s)",
+                   "cuda_graph": bool(args.c3_graph), "parallelism": f"dp{world}, cache partitioned over {world} GPU(s)",
                    "host_tier": "one node-shared pinned table (/dev/shm + cudaHostRegister), UVA reads",
                    "l2": "inputs (tens of GB of topology and features at scale 1) far larger than L2"},
         "plan": {"presample_epochs": cfg.presample_epochs, "alpha": cr.plan.alpha,
