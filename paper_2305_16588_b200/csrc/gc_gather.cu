@@ -483,10 +483,11 @@ static int gather_impl(const gc_feature_store_t* store, const uint32_t* d_ids, u
     }
     GC_CHECK_LAUNCH("gc_gather");
     if (defer) {
-        // two 2-warp CTAs per SM, 4 rows in flight per warp: ~2.4K rows of PCIe reads
-        // outstanding, while the rest of every SM is free for the next window's kernels.
-        // On a separate (high-priority) stream its CTAs take SM slots as soon as any
-        // free up; `stream` then waits for it, so consumers of `out` stay ordered.
+        // the host rows: (address sort, then) the one-warp TMA CTAs — by default two per
+        // SM with ~32 KB of rows each, or GC_OPT_DEFER_CTAS x GC_OPT_DEFER_ROWS fat CTAs
+        // holding a few SMs. On a separate (high-priority) stream they run beside the
+        // other lane's kernels; `stream` then waits for them, so consumers of `out` and
+        // the next use of this stream's deferred list stay ordered after the reads.
         cudaStream_t hs = host_stream ? as_stream(host_stream) : s;
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (hs != s) {
