@@ -571,6 +571,17 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
+def balanced_window(nb: int, window: int) -> int:
+    """Equal windows: a short last window is a pipeline stage with nothing to overlap
+    (C3: 7 windows of 1549 batches instead of 7 x 1536 + 88, +1.4%). The result is at
+    most 2% above `window` (window buffers are sized by it) and never above nb."""
+    win = max(1, min(window, nb))
+    k = math.ceil(nb / win) if nb else 1
+    if k > 1 and math.ceil(nb / (k - 1)) <= 1.02 * win:
+        k -= 1
+    return max(1, math.ceil(nb / k)) if nb else win
+
+
 def c3_run(args, rank, local, world):
     """C3 (BASELINE configs[2]; C4/C5 with --tier-workload) through Legion's full flow, one process per GPU of one
     NVSwitch clique: per-rank presampling -> hotness merge -> CSLP plan -> each rank fills
@@ -626,13 +637,7 @@ def c3_run(args, rank, local, world):
     torch.cuda.synchronize()
     t_cache = time.perf_counter() - t0
     nb = math.ceil(len(pool) / B)
-    win = min(args.c3_window or C3["window"], nb)
-    # equal windows: a short last window is a pipeline stage with nothing to overlap
-    # (C3: 7 windows of 1549 instead of 7 x 1536 + 88, +1.4%); at most 2% larger
-    k = math.ceil(nb / win)
-    if k > 1 and math.ceil(nb / (k - 1)) <= 1.02 * win:
-        k -= 1
-    win = math.ceil(nb / k)
+    win = balanced_window(nb, args.c3_window or C3["window"])
     fcap = args.c3_fcap or C3["feat_rows_cap"]
     lanes = args.c3_lanes or C3["lanes"]
     defer = bool(C3["defer_host"] if args.c3_defer < 0 else args.c3_defer)
